@@ -1,0 +1,458 @@
+"""Benchmark: global BA solve (GN x PCG, sparse + dense) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--impl ours|reference]
+
+A step is one full `AlignmentProblem.solve` (pair filter + 10 GN iterations,
+<= 50 PCG each, default EnergyWeights/SolverConfig) of the configuration's
+synthetic scene from its initial poses.  The headline workload is
+BASELINE.json configs[3]: 500 keyframes at 160x120 (cfg4), which fits one
+B200.  `value` is device time (CUDA events on the solver's stream) with every
+input resident in HBM; `e2e` is the same solve through the public API with
+the frame caches and correspondences copied from pinned host memory each
+step and the poses read back.  The CPU baseline is the oracle port timed on
+a bounded sample of the same workload and extrapolated to a full solve.
+
+Multi-GPU (torchrun, one process per GPU): N=1 is the only path measurable
+in this round; N>1 runs one replica per rank.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "global BA solve ms (GN x PCG, sparse+dense)"
+WORKLOADS = {
+    "cfg3": "global inter-chunk BA: 100 keyframes, sparse + dense at 80x60",
+    "cfg4": "global BA: 500 keyframes, sparse + dense at 160x120",
+    "cfg5": "large-scene stress: 2000 keyframes, sparse + dense at 80x60",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg4", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# workload
+
+
+def pin_caches(caches):
+    """Copy every cache plane into pinned host memory (numpy views of pinned
+    torch tensors) so H2D in the e2e leg runs from pinned buffers."""
+    import torch
+    from paper_1604_01093_b200.cache import CachedFrame
+
+    def pinned(a):
+        t = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        return t.numpy()
+
+    out = {}
+    for f, c in caches.items():
+        out[f] = CachedFrame(c.index, c.intensity_low, pinned(c.grad_low), c.depth_low,
+                             pinned(c.points_low), pinned(c.normals_low), c.intrinsics_low,
+                             pinned(c.valid_depth), pinned(c.valid_normal))
+    return out
+
+
+def canonical_bytes(hw, n_dir, n_corr, n_undirected, n_vars):
+    """SURVEY.md 8(d) canonical algorithmic bytes."""
+    return {
+        "linearize": 68 * hw * n_dir + 216 * n_dir + 104 * n_corr,
+        "pcg_iteration": 56 * n_corr + 176 * n_undirected + 80 * n_vars,
+    }
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle extrapolation (cpu_baseline / --impl reference)
+
+
+def _time_edges(args):
+    """Worker: oracle linearise + frozen energy on a list of directed edges."""
+    scene_name, edges = args
+    from oracle import scanfuse_oracle as O
+    from paper_1604_01093_b200 import synth
+    scene = _scene_cache(scene_name)
+    poses = {f: O.pose_of(p) for f, p in scene.init.items()}
+    t0 = time.perf_counter()
+    for (i, j) in edges:
+        ci, cj = scene.caches[i], scene.caches[j]
+        pts, ref = O.assoc_photo(poses, i, j, ci, cj)
+        res, J = O.photo_lin(poses, i, j, pts, ref, cj)
+        Jr = J.reshape(-1, 6)
+        _ = Jr.T @ Jr, Jr.T @ res.reshape(-1)
+        gp, gn, gt = O.assoc_geo(poses, i, j, ci, cj)
+        r2, J2 = O.geo_lin(poses, i, j, gp, gn, gt)
+        _ = J2.T @ J2, J2.T @ r2
+        O.photo_res(poses, i, j, pts, ref, cj)
+        O.geo_res(poses, i, j, gp, gn, gt)
+    return time.perf_counter() - t0
+    _ = synth  # noqa
+
+
+def _time_pairs(args):
+    scene_name, pairs = args
+    from oracle import scanfuse_oracle as O
+    scene = _scene_cache(scene_name)
+    poses = {f: O.pose_of(p) for f, p in scene.init.items()}
+    t0 = time.perf_counter()
+    passed = 0
+    for (a, b) in pairs:
+        if O.view_angle_deg(poses[a], poses[b]) >= 60.0:
+            continue
+        if O.frustum_overlap(scene.caches[a], poses[a], scene.caches[b], poses[b]) <= 0.0:
+            continue
+        if O.frustum_overlap(scene.caches[b], poses[b], scene.caches[a], poses[a]) <= 0.0:
+            continue
+        passed += 1
+    return time.perf_counter() - t0, passed
+
+
+_SCENES = {}
+
+
+def _scene_cache(name):
+    if name not in _SCENES:
+        from paper_1604_01093_b200 import synth
+        _SCENES[name] = synth.make(name)
+    return _SCENES[name]
+
+
+def cpu_extrapolate(scene_name, edges_undirected, records, workers: int, pair_sample=400,
+                    edge_sample=48, seed=0):
+    """Full-solve CPU time (ms) extrapolated from a timed sample of the oracle.
+
+    filter    = per-pair time x n(n-1)/2 pairs
+    dense GN  = per-directed-edge (associate + linearise + accumulate + frozen
+                energy) time x E_d x #dense GN iterations
+    sparse GN = one timed sparse linearisation x #GN iterations
+    PCG       = one timed oracle matvec x #PCG matvecs (incl. restarts)
+    """
+    from oracle import scanfuse_oracle as O
+    scene = _scene_cache(scene_name)
+    n = len(scene.frame_ids)
+    rng = np.random.default_rng(seed)
+    P = n * (n - 1) // 2
+    # pair-filter sample: pairs uniformly over the upper triangle
+    pairs = set()
+    while len(pairs) < min(pair_sample, P):
+        a, b = sorted(rng.choice(n, size=2, replace=False))
+        pairs.add((int(a), int(b)))
+    pairs = sorted(pairs)
+    if edges_undirected is None:
+        edges_undirected = []
+    edge_pool = list(edges_undirected) if edges_undirected else [(k, k + 1) for k in range(n - 1)]
+    pick = rng.choice(len(edge_pool), size=min(edge_sample, len(edge_pool)), replace=False)
+    sample_edges = [edge_pool[k] for k in pick]
+
+    def run(fn, items):
+        chunks = [items[k::workers] for k in range(workers)]
+        chunks = [c for c in chunks if c]
+        t0 = time.perf_counter()
+        if workers == 1:
+            outs = [fn((scene_name, chunks[0]))]
+        else:
+            import multiprocessing as mp
+            with mp.get_context("fork").Pool(len(chunks)) as pool:
+                outs = pool.map(fn, [(scene_name, c) for c in chunks])
+        return time.perf_counter() - t0, outs
+
+    wall_p, outs_p = run(_time_pairs, pairs)
+    passed = sum(o[1] for o in outs_p)
+    wall_e, _ = run(_time_edges, sample_edges)
+    per_pair = wall_p / len(pairs)
+    per_edge = wall_e / len(sample_edges)
+    E_u = len(edges_undirected) if edges_undirected else int(round(P * passed / max(1, len(pairs))))
+    E_d = E_u
+    # sparse linearisation + one matvec of the full system, single process
+    prob = O.Problem(scene.frame_ids, {f: O.pose_of(p) for f, p in scene.init.items()},
+                     scene.corr_sets, None)
+    t0 = time.perf_counter()
+    S_, _, _ = prob.linearize(O.DEFAULT_W, 0.0, O.DEFAULT_CFG)
+    t_sparse = time.perf_counter() - t0
+    nv = prob.n_vars
+    dense = np.zeros((nv, nv))
+    S_.dense = dense
+    x = rng.normal(size=nv)
+    t0 = time.perf_counter()
+    S_.apply(x)
+    t_mv = time.perf_counter() - t0
+    if records:
+        n_gn = len(records)
+        n_dense = sum(1 for r in records if r["dense_weight"] > 0)
+        n_mv = sum(r["pcg_iterations"] + r["pcg_iterations"] // 20 for r in records)
+    else:  # default config upper bounds: 10 GN (ramp: it 0 sparse), 50 PCG each
+        n_gn, n_dense, n_mv = 10, 9, 10 * (50 + 2)
+    total_s = (per_pair * P + per_edge * E_d * n_dense + t_sparse * n_gn * 2 + t_mv * n_mv)
+    sample = (f"{len(pairs)} of {P} frame pairs through the oracle filter, {len(sample_edges)} of "
+              f"{E_d} directed edges linearised+frozen-energy, 1 sparse linearisation, 1 full "
+              f"matvec; extrapolated to {n_gn} GN / {n_dense} dense / {n_mv} matvecs")
+    return total_s * 1e3, sample, (wall_p + wall_e + t_sparse + t_mv)
+
+
+# ---------------------------------------------------------------------------
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    workers = os.cpu_count() or 1
+    scene = _scene_cache(args.config)
+    vals = []
+    for k in range(args.warmup + args.steps):
+        ms, sample, _ = cpu_extrapolate(args.config, None, None, workers, pair_sample=800,
+                                        edge_sample=4 * workers, seed=k)
+        if k >= args.warmup:
+            vals.append(ms)
+    v = float(np.median(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "ms", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOADS[args.config], "name": args.config,
+                   "frames": len(scene.frame_ids)},
+        "cpu_baseline": {"value": v, "unit": "ms", "cores": workers, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": v, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    os.environ["SFB_DEVICE"] = str(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_1604_01093_b200 import _abi
+    from paper_1604_01093_b200 import solver as S
+    from paper_1604_01093_b200 import synth
+    from paper_1604_01093_b200.runtime import runtime
+
+    scene = synth.make(args.config)
+    caches = pin_caches(scene.caches)
+    ids = scene.frame_ids
+    W = S.EnergyWeights(**scene.weights)
+    C = S.SolverConfig(**scene.config)
+    rt = runtime(local)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---- device-resident leg (value) ----------------------------------------
+    problem = S.AlignmentProblem(ids, scene.init, scene.corr_sets, caches)
+    problem.solve(W, C)  # uploads + first solve (warm-up 0)
+    dp = problem._dp
+    ext = torch.cuda.ExternalStream(dp.stream_ptr(), device=torch.device("cuda", local))
+    flush = torch.empty(384 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    for _ in range(args.warmup):
+        problem.poses = dict(scene.init)
+        problem.solve(W, C)
+    dp.profile(True)
+    dp.profile_read(reset=True)
+    times = []
+    launches0 = _abi.launch_count()
+    records = None
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1.0)  # evict L2 (126 MB) between timed solves
+            torch.cuda.synchronize()
+            problem.poses = dict(scene.init)
+            barrier()
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(ext)
+            stats = problem.solve(W, C)
+            e1.record(ext)
+            torch.cuda.synchronize()
+            barrier()
+            times.append(e0.elapsed_time(e1))
+            records = [dict(dense_weight=r.dense_weight, pcg_iterations=r.pcg_iterations,
+                            energy_after=r.energy_after) for r in stats.iterations]
+    launches = _abi.launch_count() - launches0
+    prof = dp.profile_read(reset=True)
+    dp.profile(False)
+    ms = float(np.mean(times))
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    nv, n_pairs, n_corr = dp.dims()
+    n_edges = len(problem.dense_edges)
+    n_dir = n_edges * (2 if C.dense_bidirectional else 1)
+    hw = scene.low_size[0] * scene.low_size[1]
+    cb = canonical_bytes(hw, n_dir, n_corr, n_edges, nv)
+    peak, peak_kind = peaks()
+    lin_ms, lin_n = prof["dense_linearize"]
+    pcg_ms, pcg_n = prof["pcg"]
+    lin_per = lin_ms / max(1, lin_n)
+    achieved = cb["linearize"] / (lin_per * 1e-3) / 1e9 if lin_n else 0.0
+    pcg_iters = sum(r["pcg_iterations"] for r in records) if records else 0
+    pcg_iter_us = 1e3 * (pcg_ms / max(1, pcg_n)) / max(1, pcg_iters / max(1, len(records))) if records else None
+
+    # ---- end-to-end leg (public API, host buffers) --------------------------
+    e2e = None
+    if not args.no_e2e:
+        px = sum(np.asarray(c.valid_depth).size for c in caches.values())
+        h2d = px * (1 + 1 + 12 + 12 + 8) + n_corr * 48 + len(scene.corr_sets) * 16 + len(ids) * 97
+        e2e_t = []
+        for k in range(max(1, args.steps)):
+            rt.clear_frames()
+            problem.close()
+            torch.cuda.synchronize()
+            barrier()
+            t0 = time.perf_counter()
+            p2 = S.AlignmentProblem(ids, scene.init, scene.corr_sets, caches)
+            st2 = p2.solve(W, C)
+            torch.cuda.synchronize()
+            e2e_t.append((time.perf_counter() - t0) * 1e3)
+            p2.close()
+        d2h = len(ids) * 96 + len(st2.iterations) * 64
+        ev = float(np.mean(e2e_t))
+        if world > 1:
+            t = torch.tensor([ev], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ev = float(t.item())
+        e2e = {"value": ev, "unit": "ms", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        edges = [(a, b) for (a, b) in problem.dense_edges]
+        cms, sample, spent = cpu_extrapolate(args.config, edges, records, 1)
+        cpu = {"value": cms, "unit": "ms", "cores": 1, "kind": "port", "sample": sample,
+               "sample_seconds": round(spent, 1)}
+    line = {
+        "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+        "scaling": "strong" if world == 1 else "replicas", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": WORKLOADS[args.config], "name": args.config, "frames": len(ids),
+                   "resolution": list(scene.low_size), "dense_edges": n_edges,
+                   "correspondences": n_corr, "n_vars": nv, "gn_iterations": len(records),
+                   "pcg_iterations": pcg_iters, "l2": "flushed (384 MB write) between steps",
+                   "parallelism": f"dp{world}" if world > 1 else "single"},
+        "roofline": {"bound": "hbm", "kernel": "k_dense_linearize",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak if peak else None, "traffic": None,
+                     "peak_kind": peak_kind,
+                     "algorithmic_bytes_per_launch": cb["linearize"],
+                     "ms_per_launch": lin_per, "launches": lin_n},
+        "pcg": {"us_per_iteration": pcg_iter_us,
+                "canonical_bytes_per_iteration": cb["pcg_iteration"],
+                "gbs": (cb["pcg_iteration"] / (pcg_iter_us * 1e-6) / 1e9) if pcg_iter_us else None},
+        "phase_ms_per_step": {k: round(v[0] / max(1, args.steps), 3) for k, v in prof.items()},
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "final_energy": records[-1]["energy_after"] if records else None,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

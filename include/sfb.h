@@ -1,0 +1,219 @@
+/*
+ * sfb.h — C ABI of the B200-native BundleFusion pose solver (libsfb.so).
+ *
+ * The reference (scanfuse 0.1.0, /root/reference/pkg/src/scanfuse/solver.py)
+ * is pure Python/NumPy and has no FFI layer of its own; its boundary is the
+ * Python API of `scanfuse.solver`.  This header is what that API binds
+ * through ctypes (paper_1604_01093_b200/_abi.py).  Every entry point names the
+ * reference function(s) it replaces.
+ *
+ * Conventions
+ *  - Every function returns int status: SFB_OK (0) or an SFB_E_* code.  No C++
+ *    exception crosses the ABI; the message of the last failure on a handle is
+ *    sfb_last_error(handle) (thread-local fallback when handle is NULL).
+ *  - Host pointers are borrowed for the duration of the call only.  Device
+ *    memory is owned by the handle that allocated it.
+ *  - One CUDA stream per problem handle; frames in a context are read-only
+ *    after upload, so problems created on one context may run concurrently
+ *    (reference contract solver.py:551-552).
+ *  - Frames are addressed by context slot; inside a problem, frames are
+ *    addressed by their position k in frame_ids (k = 0 is the gauge anchor,
+ *    variable block k-1 otherwise; reference solver.py:561-562).
+ */
+#ifndef SFB_H_
+#define SFB_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SFB_ABI_VERSION 1
+
+enum {
+  SFB_OK = 0,
+  SFB_E_ARG = 1,            /* invalid argument / shape                     */
+  SFB_E_CUDA = 2,           /* CUDA runtime / launch failure                */
+  SFB_E_OOM = 3,            /* device allocation failed                     */
+  SFB_E_PCG_NONFINITE = 4,  /* PcgDivergenceError (solver.py:30-31,488-499) */
+  SFB_E_STATE = 5           /* call out of order (e.g. PCG before linearize) */
+};
+
+typedef struct sfb_ctx sfb_ctx;
+typedef struct sfb_problem sfb_problem;
+
+/* One CachedFrame (reference frames.py:38-50): the planes the solver reads.
+ * All planes are row-major (h, w[, c]) and C-contiguous. */
+typedef struct {
+  int32_t width, height;
+  double fx, fy, cx, cy;          /* intrinsics_low                         */
+  const uint8_t* valid_depth;     /* (h, w) bool                             */
+  const uint8_t* valid_normal;    /* (h, w) bool                             */
+  const float* points;            /* (h, w, 3) points_low                    */
+  const float* normals;           /* (h, w, 3) normals_low                   */
+  const float* grad;              /* (h, w, 2) grad_low                      */
+} sfb_frame_desc;
+
+/* EnergyWeights (solver.py:34-46) minus the ramp, which stays on the host. */
+typedef struct {
+  double sparse, photo, geo;
+} sfb_weights;
+
+/* SolverConfig (solver.py:56-69) fields the device path needs. */
+typedef struct {
+  double geo_distance_max;        /* 0.15 */
+  double geo_normal_min;          /* 0.9  */
+  int32_t dense_pixel_stride;     /* 1    */
+  int32_t dense_bidirectional;    /* 0    */
+} sfb_config;
+
+/* Rounding conventions of the host BLAS the reference runs on (see
+ * paper_1604_01093_b200/_rounding.py).  Each code is a permutation index
+ * 0..5 of the 3-term FMA chain fma(a_k b_k, fma(a_j b_j, a_i b_i)); they make
+ * the frame-pair filter and the association gates bit-exact with NumPy. */
+typedef struct {
+  int32_t matvec_c;   /* (3,3) C-contiguous @ (3,)                            */
+  int32_t matvec_f;   /* (3,3) F-contiguous @ (3,)                            */
+  int32_t gemm33;     /* (3,3) @ (3,3)                                        */
+  int32_t apply_n;    /* (m,3) @ (3,3).T for m > 1                            */
+  int32_t apply_1;    /* (1,3) @ (3,3).T                                      */
+  int32_t dot3;       /* np.dot of two 3-vectors                              */
+} sfb_rounding;
+
+/* Per-GN-iteration scalars of the fused iteration (IterationRecord inputs). */
+typedef struct {
+  double e_sparse, e_photo, e_geo;              /* raw sums at linearization   */
+  int32_t pcg_iterations;
+  int32_t pcg_status;                           /* SFB_OK or SFB_E_PCG_NONFINITE */
+  double pcg_relative;
+  double step_norm;
+  double ea_sparse, ea_photo, ea_geo;           /* frozen-association sums     */
+} sfb_iter_result;
+
+const char* sfb_last_error(const void* handle);
+int sfb_abi_version(void);
+
+/* ---- context + frame store ------------------------------------------- */
+int sfb_ctx_create(int32_t device, sfb_ctx** out);
+int sfb_ctx_destroy(sfb_ctx* ctx);
+int sfb_ctx_set_rounding(sfb_ctx* ctx, const sfb_rounding* r);
+/* Upload n CachedFrames (frames.py:38-50); one slot per frame.  Replaces the
+ * per-call `.astype(np.float64)` plane reads of solver.py:219-251,268-272. */
+int sfb_frames_upload(sfb_ctx* ctx, int32_t n, const sfb_frame_desc* descs,
+                      int32_t* slots_out);
+int sfb_frames_release(sfb_ctx* ctx, int32_t n, const int32_t* slots);
+
+/* ---- problem (AlignmentProblem.__init__, solver.py:554-564) ----------- */
+/* n_frames problem frames (slots may be NULL when no caches); n_sets
+ * correspondence sets (CorrespondenceSet, filters.py:50-66) given as
+ * problem-frame indices and offsets into the stacked (N,3) point arrays,
+ * i.e. build_sparse_term (solver.py:89-111). */
+int sfb_problem_create(sfb_ctx* ctx, int32_t n_frames, const int32_t* slots,
+                       int32_t n_sets, const int32_t* set_frame_i,
+                       const int32_t* set_frame_j, const int64_t* set_offsets,
+                       const double* points_i, const double* points_j,
+                       sfb_problem** out);
+int sfb_problem_destroy(sfb_problem* p);
+int sfb_problem_stream(sfb_problem* p, void** stream_out);
+
+/* Poses: R row-major (n,3,3), t (n,3).  f_layout[k] = 1 when the host
+ * rotation array is Fortran-ordered (changes NumPy's inverse() rounding). */
+int sfb_set_poses(sfb_problem* p, const double* R, const double* t,
+                  const uint8_t* f_layout);
+int sfb_get_poses(sfb_problem* p, double* R, double* t);
+int sfb_save_best(sfb_problem* p);     /* best_poses = dict(self.poses)   */
+int sfb_restore_best(sfb_problem* p);  /* self.poses = best_poses          */
+
+/* build_dense_edges (solver.py:130-148) + view_angle_deg/frustum_overlap
+ * (frames.py:154-188), bit-exact.  view_cos_min is the smallest cosine c with
+ * degrees(arccos(c)) < view_angle_max_deg under NumPy (host bisection). */
+int sfb_build_dense_edges(sfb_problem* p, double view_cos_min, int64_t* n_edges);
+int sfb_get_dense_edges(sfb_problem* p, int32_t* pairs_out /* 2*n_edges */);
+int sfb_set_dense_edges(sfb_problem* p, int64_t n_edges, const int32_t* pairs);
+/* frustum_overlap(cache_a, pose_a, cache_b, pose_b) for many (a,b) pairs of
+ * problem frames at the current poses: fraction in [0,1] (frames.py:154-180). */
+int sfb_frustum_overlap(sfb_problem* p, int64_t n_pairs, const int32_t* pairs,
+                        double* overlap_out);
+
+/* normal_equations (solver.py:630-660): sparse state, dense association +
+ * linearization, and the block system; energies are raw sums (host applies
+ * the weights exactly as solver.py:646,655 do). */
+int sfb_linearize(sfb_problem* p, const sfb_weights* w, double w_dense,
+                  const sfb_config* cfg, double energies_out[3]);
+/* pcg_solve (solver.py:463-508), scalar-Jacobi, exact recurrence. */
+int sfb_pcg(sfb_problem* p, int32_t max_iterations, double tolerance,
+            int32_t restart_interval, int32_t* iterations, double* relative,
+            int32_t* status);
+/* The PCG solution dx of the last sfb_pcg / sfb_gn_iteration (n_vars). */
+int sfb_get_solution(sfb_problem* p, double* x);
+/* pcg_solve on a duck-typed host system (.rhs/.diagonal/.apply, the
+ * reference's test DenseSystem, test_solver.py:282-292): A is the dense
+ * (n,n) row-major operator, same device recurrence as sfb_pcg. */
+int sfb_pcg_dense(sfb_ctx* ctx, int32_t n, const double* A, const double* rhs,
+                  const double* diagonal, int32_t max_iterations, double tolerance,
+                  int32_t restart_interval, double* x_out, int32_t* iterations,
+                  double* relative, int32_t* status);
+/* _apply_step (solver.py:674-677): T <- exp(dx) o T for every variable frame. */
+int sfb_apply_step(sfb_problem* p, double* step_norm);
+/* _energy_with_frozen_associations (solver.py:662-672): raw sums. */
+int sfb_energy_frozen(sfb_problem* p, int32_t dense, double energies_out[3]);
+/* One full GN iteration without intermediate host syncs:
+ * linearize -> pcg -> step -> frozen energy (solver.py:700-724). */
+int sfb_gn_iteration(sfb_problem* p, const sfb_weights* w, double w_dense,
+                     const sfb_config* cfg, int32_t pcg_max_iterations,
+                     double pcg_tolerance, int32_t pcg_restart_interval,
+                     sfb_iter_result* out);
+
+/* ---- host views of the linearized system (NormalEquations accessors) --- */
+int sfb_system_dims(sfb_problem* p, int32_t* n_vars, int64_t* n_pairs,
+                    int64_t* n_corr);
+/* NormalEquations.apply (solver.py:403-410). */
+int sfb_matvec(sfb_problem* p, const double* x, double* y);
+/* gradient, Jacobi diagonal (solver.py:412-428). */
+int sfb_get_gradient(sfb_problem* p, double* g);
+int sfb_get_diagonal(sfb_problem* p, double* d);
+/* block system: diag blocks (n_vars/6,6,6), pair blocks (n_pairs,6,6) with
+ * their (row var, col var) ids — used by materialize() (solver.py:446-454). */
+int sfb_get_blocks(sfb_problem* p, double* diag_blocks, double* pair_blocks,
+                   int32_t* pair_vars);
+/* world_i, world_j of the sparse state (solver.py:568-580). */
+int sfb_get_sparse_world(sfb_problem* p, double* world_i, double* world_j);
+/* eval_sparse residuals at current poses (solver.py:114-123), (N,3). */
+int sfb_sparse_residuals(sfb_problem* p, double* res_out);
+/* per-set max residual norm (max_residual_set, solver.py:765-776). */
+int sfb_sparse_set_max(sfb_problem* p, double* set_max_out);
+
+/* ---- per-edge evaluators (solver.py:216-349) ----------------------------
+ * associate_photo / associate_geo (solver.py:216-260) for one directed edge
+ * i->j of problem frames at the current poses.  kind 0 = photo, 1 = geo.
+ * Per-source-pixel outputs (h_i*w_i, row-major), honouring the pixel stride
+ * of _source_pixel_data (solver.py:158-167):
+ *   sel[px] = 1 when the pixel belongs to the association
+ *   tgt[px] = associated target pixel index (geo) or -1                     */
+int sfb_associate(sfb_problem* p, int32_t frame_i, int32_t frame_j,
+                  int32_t kind, const sfb_config* cfg, uint8_t* sel,
+                  int32_t* tgt);
+/* photo_residuals / photo_linearize (kind 0; aux = reference (m,2)) and
+ * geo_residuals / geo_linearize (kind 1; aux = normals (m,3), targets (m,3))
+ * on explicit association arrays (solver.py:263-328).  res is (m,2) or (m,);
+ * jac (optional, may be NULL) is J_i as (m,2,6) or (m,6); J_j = -J_i. */
+int sfb_point_eval(sfb_problem* p, int32_t frame_i, int32_t frame_j,
+                   int32_t kind, int64_t m, const double* points,
+                   const double* aux, const double* targets, double* res,
+                   double* jac);
+
+/* ---- measurement (bench.py) -------------------------------------------
+ * Per-kernel-class device time measured with CUDA events on the problem's
+ * stream.  Classes: 0 dense linearize, 1 frozen energy, 2 PCG, 3 pair filter,
+ * 4 sparse term, 5 assembly, 6 pose update, 7 other. */
+#define SFB_PROF_CLASSES 8
+int sfb_profile(sfb_problem* p, int32_t enable);
+int sfb_profile_read(sfb_problem* p, double* ms, int64_t* launches, int32_t reset);
+/* Kernels launched by this library since load (all handles). */
+int sfb_launch_count(int64_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SFB_H_ */

@@ -1,0 +1,1296 @@
+// sfb_abi.cu — extern "C" entry points of libsfb.so (see include/sfb.h) and
+// the host-side bookkeeping behind them: frame store, problem handles, the
+// block-system structure (which frame pairs couple), work decomposition of
+// the dense term into (directed edge, pixel tile) items.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include <cub/device/device_select.cuh>
+
+#include "../../include/sfb.h"
+#include "sfb_kernels.cuh"
+
+static std::atomic<long long> g_launches{0};
+void sfb_count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+namespace {
+
+thread_local std::string g_tls_err;
+
+// CUDA-event timing of kernel classes on one stream (enabled per problem).
+struct Prof {
+  bool on = false;
+  double ms[SFB_PROF_CLASSES] = {0};
+  int64_t n[SFB_PROF_CLASSES] = {0};
+  struct Pending {
+    int cls;
+    cudaEvent_t a, b;
+  };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t get() {
+    if (pool.empty()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      return e;
+    }
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
+  void begin(int cls, cudaStream_t s, Pending* slot) {
+    slot->cls = cls;
+    slot->a = get();
+    slot->b = get();
+    cudaEventRecord(slot->a, s);
+  }
+  void end(const Pending& pd, cudaStream_t s) {
+    cudaEventRecord(pd.b, s);
+    pending.push_back(pd);
+  }
+  // call after a stream sync
+  void drain() {
+    for (auto& pd : pending) {
+      float t = 0.f;
+      if (cudaEventElapsedTime(&t, pd.a, pd.b) == cudaSuccess) {
+        ms[pd.cls] += t;
+        n[pd.cls] += 1;
+      }
+      pool.push_back(pd.a);
+      pool.push_back(pd.b);
+    }
+    pending.clear();
+  }
+  void destroy() {
+    drain();
+    for (auto e : pool) cudaEventDestroy(e);
+    pool.clear();
+  }
+};
+
+// RAII scope: times the kernels enqueued inside it as one class.
+struct ProfScope {
+  Prof* pr;
+  cudaStream_t s;
+  Prof::Pending pd{};
+  ProfScope(Prof& p, int cls, cudaStream_t st) : pr(p.on ? &p : nullptr), s(st) {
+    if (pr) pr->begin(cls, s, &pd);
+  }
+  ~ProfScope() {
+    if (pr) pr->end(pd, s);
+  }
+};
+
+struct Handle {
+  std::string err;
+};
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaError_t ensure(size_t want) {
+    if (want <= n && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    size_t bytes = std::max<size_t>(want, 1) * sizeof(T);
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e == cudaSuccess) n = std::max<size_t>(want, 1);
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+struct Slot {
+  FrameDev dev;
+  void* block = nullptr;
+  bool alive = false;
+};
+
+}  // namespace
+
+struct sfb_ctx : Handle {
+  int device = 0;
+  int n_sm = 148;
+  cudaStream_t stream = nullptr;
+  Rounding rd{2, 0, 0, 0, 2, 0};
+  std::vector<Slot> slots;
+  std::map<void*, int> block_refs;
+  DBuf<uint8_t> staging;
+  DBuf<int> counts;
+};
+
+struct sfb_problem : Handle {
+  sfb_ctx* ctx = nullptr;
+  cudaStream_t stream = nullptr;
+  int n = 0;          // frames
+  int n_blk = 0;      // variable blocks = n - 1
+  bool has_frames = false;
+  std::vector<int> slots;
+  std::vector<FrameDev> frames_h;
+  DBuf<FrameDev> frames;
+  DBuf<PoseDev> poses, best;
+  // sparse
+  int n_sets = 0;
+  int64_t n_corr = 0;
+  std::vector<int> set_fi_h, set_fj_h;
+  DBuf<int> set_fi, set_fj;
+  DBuf<int64_t> set_off;
+  DBuf<double> pts_i, pts_j, world_i, world_j, set_out;
+  // dense
+  std::vector<int2> edges;  // undirected (a < b in frame order)
+  int struct_bidir = -1;
+  int n_dir = 0, n_items = 0;
+  DBuf<int2> dir_edges;
+  DBuf<int4> items;
+  DBuf<int> edge_item_ptr;
+  DBuf<int64_t> photo_off, geo_off;
+  DBuf<uint32_t> photo_mask;
+  DBuf<uint16_t> geo_tgt;
+  DBuf<double> item_out, edge_out, item_e2;
+  bool dense_active = false;
+  int last_do_photo = 0, last_do_geo = 0;
+  // system
+  int n_pairs = 0;
+  std::vector<int2> pair_vars;
+  DBuf<int> d_ptr, d_ent, b_ptr, b_ent, row_ptr, row_ent, row_col;
+  DBuf<double> D, B, g;
+  DBuf<double> x, r, z, pv, Ap, inv_diag, bvec, part, tmp, jdiag;
+  DBuf<int> flags;
+  bool have_system = false;
+  bool have_solution = false;
+  // scalars
+  DBuf<double> dscal;       // device scalars
+  double* hscal = nullptr;  // pinned mirror
+  Prof prof;
+};
+
+namespace {
+
+int fail(Handle* h, int code, const std::string& msg) {
+  if (h) h->err = msg;
+  g_tls_err = msg;
+  return code;
+}
+
+#define CK(h, expr)                                                                    \
+  do {                                                                                 \
+    cudaError_t _e = (expr);                                                           \
+    if (_e != cudaSuccess) {                                                           \
+      return fail(h, _e == cudaErrorMemoryAllocation ? SFB_E_OOM : SFB_E_CUDA,         \
+                  std::string(#expr) + ": " + cudaGetErrorString(_e));                 \
+    }                                                                                  \
+  } while (0)
+
+#define CKL(h)                                                                         \
+  do {                                                                                 \
+    cudaError_t _e = cudaGetLastError();                                               \
+    if (_e != cudaSuccess) return fail(h, SFB_E_CUDA, std::string("launch: ") + cudaGetErrorString(_e)); \
+  } while (0)
+
+size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+
+// Stable compaction of flagged elements (cub::DeviceSelect::Flagged).
+template <class T>
+cudaError_t select_flagged(const T* in, const uint8_t* flags, T* out, int* d_count, int n,
+                           DBuf<uint8_t>& temp, cudaStream_t s) {
+  size_t bytes = 0;
+  cudaError_t e = cub::DeviceSelect::Flagged(nullptr, bytes, in, flags, out, d_count, n, s);
+  if (e != cudaSuccess) return e;
+  if ((e = temp.ensure(bytes)) != cudaSuccess) return e;
+  return cub::DeviceSelect::Flagged(temp.p, bytes, in, flags, out, d_count, n, s);
+}
+
+__global__ void k_enumerate_pairs(int n, int2* out) {
+  const int a = blockIdx.y;
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b <= a || b >= n) return;
+  const int64_t q = (int64_t)a * n - ((int64_t)a * (a + 1)) / 2 + (b - a - 1);
+  out[q] = make_int2(a, b);
+}
+
+__global__ void k_jacobi_diag(const double* D, const int* d_ptr, const int* d_ent,
+                              const double* set_out, int n_blk, double* out);
+
+PcgArgs pcg_args(sfb_problem* p) {
+  PcgArgs a{};
+  a.n_blk = p->n_blk;
+  a.D = p->D.p;
+  a.B = p->B.p;
+  a.row_ptr = p->row_ptr.p;
+  a.row_ent = p->row_ent.p;
+  a.row_col = p->row_col.p;
+  a.g = p->g.p;
+  a.x = p->x.p;
+  a.r = p->r.p;
+  a.z = p->z.p;
+  a.p = p->pv.p;
+  a.Ap = p->Ap.p;
+  a.inv_diag = p->inv_diag.p;
+  a.b = p->bvec.p;
+  a.jdiag = p->jdiag.p;
+  a.part = p->part.p;
+  a.flags = p->flags.p;
+  return a;
+}
+
+template <class T>
+cudaError_t upload_vec(DBuf<T>& d, const std::vector<T>& h, cudaStream_t s) {
+  cudaError_t e = d.ensure(h.size());
+  if (e != cudaSuccess || h.empty()) return e;
+  return cudaMemcpyAsync(d.p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, s);
+}
+
+// Which frame pairs couple, the contribution lists, the dense work items.
+int rebuild_structure(sfb_problem* p, int bidir) {
+  const int nb = p->n_blk;
+  // directed dense edges (solver.py:151-155)
+  std::vector<int2> dir(p->edges.begin(), p->edges.end());
+  if (bidir)
+    for (const int2& e : p->edges) dir.push_back(make_int2(e.y, e.x));
+  p->n_dir = (int)dir.size();
+
+  // dense work items: (dir edge, pixel tile); tiles start on 32-pixel bounds
+  std::vector<int4> items;
+  std::vector<int> eptr(1, 0);
+  std::vector<int64_t> poff, goff;
+  int64_t pw = 0, gw = 0;
+  const int target = 148 * 8;
+  for (int d = 0; d < p->n_dir; ++d) {
+    const FrameDev& F = p->frames_h[dir[d].x];
+    const int hw = F.w * F.h;
+    int tiles = std::max(1, (target + p->n_dir - 1) / std::max(1, p->n_dir));
+    tiles = std::min(tiles, std::max(1, (hw + 255) / 256));
+    int tile = (hw + tiles - 1) / tiles;
+    tile = (tile + 31) & ~31;
+    for (int b = 0; b < hw; b += tile) items.push_back(make_int4(d, b, std::min(hw, b + tile), 0));
+    eptr.push_back((int)items.size());
+    poff.push_back(pw);
+    goff.push_back(gw);
+    pw += (hw + 31) / 32;
+    gw += (hw + 7) & ~7;
+  }
+  p->n_items = (int)items.size();
+
+  // contribution lists
+  std::map<std::pair<int, int>, int> pid;
+  std::vector<std::vector<int>> dl(nb), bl;
+  std::vector<int2> pv;
+  auto pair_of = [&](int a, int b) {
+    auto key = std::make_pair(a, b);
+    auto it = pid.find(key);
+    if (it != pid.end()) return it->second;
+    const int q = (int)pv.size();
+    pid[key] = q;
+    pv.push_back(make_int2(a, b));
+    bl.emplace_back();
+    return q;
+  };
+  for (int s = 0; s < p->n_sets; ++s) {
+    const int vi = p->set_fi_h[s] - 1, vj = p->set_fj_h[s] - 1;
+    if (vi == vj) {
+      if (vi >= 0) {
+        dl[vi].push_back(s << 3 | 0);
+        dl[vi].push_back(s << 3 | 1);
+        dl[vi].push_back(s << 3 | 2);
+      }
+      continue;
+    }
+    if (vi >= 0) dl[vi].push_back(s << 3 | 0);
+    if (vj >= 0) dl[vj].push_back(s << 3 | 1);
+    if (vi >= 0 && vj >= 0) {
+      const int a = std::min(vi, vj), b = std::max(vi, vj);
+      bl[pair_of(a, b)].push_back(s << 3 | (vi == a ? 0 : 1));
+    }
+  }
+  for (int d = 0; d < p->n_dir; ++d) {
+    const int vs = dir[d].x - 1, vd = dir[d].y - 1;
+    if (vs >= 0) dl[vs].push_back(d << 3 | 4);
+    if (vd >= 0) dl[vd].push_back(d << 3 | 5);
+    if (vs >= 0 && vd >= 0) {
+      const int a = std::min(vs, vd), b = std::max(vs, vd);
+      bl[pair_of(a, b)].push_back(d << 3 | 4);
+    }
+  }
+  p->n_pairs = (int)pv.size();
+  p->pair_vars = pv;
+  std::vector<int> dptr(1, 0), dent, bptr(1, 0), bent;
+  for (int v = 0; v < nb; ++v) {
+    dent.insert(dent.end(), dl[v].begin(), dl[v].end());
+    dptr.push_back((int)dent.size());
+  }
+  for (int q = 0; q < p->n_pairs; ++q) {
+    bent.insert(bent.end(), bl[q].begin(), bl[q].end());
+    bptr.push_back((int)bent.size());
+  }
+  // matvec rows
+  std::vector<std::vector<std::pair<int, int>>> rows(nb);  // (ent, col)
+  for (int q = 0; q < p->n_pairs; ++q) {
+    rows[pv[q].x].push_back({q << 1, pv[q].y});
+    rows[pv[q].y].push_back({q << 1 | 1, pv[q].x});
+  }
+  std::vector<int> rptr(1, 0), rent, rcol;
+  for (int v = 0; v < nb; ++v) {
+    for (auto& e : rows[v]) {
+      rent.push_back(e.first);
+      rcol.push_back(e.second);
+    }
+    rptr.push_back((int)rent.size());
+  }
+
+  cudaStream_t s = p->stream;
+  CK(p, upload_vec(p->dir_edges, dir, s));
+  CK(p, upload_vec(p->items, items, s));
+  CK(p, upload_vec(p->edge_item_ptr, eptr, s));
+  CK(p, upload_vec(p->photo_off, poff, s));
+  CK(p, upload_vec(p->geo_off, goff, s));
+  CK(p, p->photo_mask.ensure((size_t)std::max<int64_t>(pw, 1)));
+  CK(p, p->geo_tgt.ensure((size_t)std::max<int64_t>(gw, 1)));
+  CK(p, p->item_out.ensure((size_t)p->n_items * SFB_ITEM_STRIDE));
+  CK(p, p->edge_out.ensure((size_t)p->n_dir * SFB_ITEM_STRIDE));
+  CK(p, p->item_e2.ensure((size_t)p->n_items * 2));
+  CK(p, upload_vec(p->d_ptr, dptr, s));
+  CK(p, upload_vec(p->d_ent, dent, s));
+  CK(p, upload_vec(p->b_ptr, bptr, s));
+  CK(p, upload_vec(p->b_ent, bent, s));
+  CK(p, upload_vec(p->row_ptr, rptr, s));
+  CK(p, upload_vec(p->row_ent, rent, s));
+  CK(p, upload_vec(p->row_col, rcol, s));
+  CK(p, p->D.ensure((size_t)nb * 36));
+  CK(p, p->B.ensure((size_t)std::max(1, p->n_pairs) * 36));
+  CK(p, cudaStreamSynchronize(s));  // host vectors die here
+  p->struct_bidir = bidir;
+  p->have_system = false;
+  p->dense_active = false;
+  return SFB_OK;
+}
+
+DenseArgs dense_args(sfb_problem* p) {
+  DenseArgs a{};
+  a.frames = p->frames.p;
+  a.poses = p->poses.p;
+  a.items = p->items.p;
+  a.dir_edges = p->dir_edges.p;
+  a.photo_off = p->photo_off.p;
+  a.geo_off = p->geo_off.p;
+  a.photo_mask = p->photo_mask.p;
+  a.geo_tgt = p->geo_tgt.p;
+  a.item_out = p->item_out.p;
+  a.rd = p->ctx->rd;
+  a.n_items = p->n_items;
+  a.stride = 1;
+  return a;
+}
+
+SparseArgs sparse_args(sfb_problem* p) {
+  SparseArgs a{};
+  a.poses = p->poses.p;
+  a.set_fi = p->set_fi.p;
+  a.set_fj = p->set_fj.p;
+  a.set_off = p->set_off.p;
+  a.pts_i = p->pts_i.p;
+  a.pts_j = p->pts_j.p;
+  a.set_out = p->set_out.p;
+  a.n_sets = p->n_sets;
+  return a;
+}
+
+// Enqueue linearize (no sync).  dense_on decided on the host.
+int enqueue_linearize(sfb_problem* p, const sfb_weights* w, double w_dense, const sfb_config* cfg) {
+  if (cfg->dense_pixel_stride < 1) return fail(p, SFB_E_ARG, "dense_pixel_stride must be >= 1");
+  const int bidir = cfg->dense_bidirectional ? 1 : 0;
+  if (p->struct_bidir != bidir) {
+    int rc = rebuild_structure(p, bidir);
+    if (rc) return rc;
+  }
+  cudaStream_t s = p->stream;
+  SparseArgs sa = sparse_args(p);
+  sa.world_i = p->world_i.p;
+  sa.world_j = p->world_j.p;
+  sa.w_sparse = w->sparse;
+  sa.energy_only = 0;
+  {
+    ProfScope ps(p->prof, 4, s);
+    launch_sparse(sa, s);
+  }
+  CKL(p);
+  const bool dense_on = p->has_frames && w_dense > 0.0 && !p->edges.empty();
+  if (dense_on) {
+    DenseArgs da = dense_args(p);
+    da.do_photo = w->photo > 0.0;
+    da.do_geo = w->geo > 0.0;
+    da.s_photo = w_dense * w->photo;
+    da.s_geo = w_dense * w->geo;
+    da.geo_dmax = cfg->geo_distance_max;
+    da.geo_nmin = cfg->geo_normal_min;
+    da.stride = cfg->dense_pixel_stride;
+    if (da.do_photo || da.do_geo) {
+      {
+        ProfScope ps(p->prof, 0, s);
+        launch_dense_linearize(da, s);
+      }
+      CKL(p);
+      ProfScope ps(p->prof, 5, s);
+      launch_edge_reduce(p->edge_item_ptr.p, p->item_out.p, p->edge_out.p, p->n_dir, s);
+      CKL(p);
+    } else {
+      CK(p, cudaMemsetAsync(p->edge_out.p, 0, sizeof(double) * p->n_dir * SFB_ITEM_STRIDE, s));
+    }
+    p->last_do_photo = da.do_photo;
+    p->last_do_geo = da.do_geo;
+  }
+  AssembleArgs aa{};
+  aa.n_blk = p->n_blk;
+  aa.n_pairs = p->n_pairs;
+  aa.set_out = p->set_out.p;
+  aa.edge_out = p->edge_out.p;
+  aa.d_ptr = p->d_ptr.p;
+  aa.d_ent = p->d_ent.p;
+  aa.b_ptr = p->b_ptr.p;
+  aa.b_ent = p->b_ent.p;
+  aa.D = p->D.p;
+  aa.B = p->B.p;
+  aa.g = p->g.p;
+  aa.dense_on = dense_on ? 1 : 0;
+  ProfScope ps(p->prof, 5, s);
+  launch_assemble(aa, s);
+  CKL(p);
+  if (p->n_blk > 0) {
+    sfb_count_launch();
+    k_jacobi_diag<<<(6 * p->n_blk + 255) / 256, 256, 0, s>>>(p->D.p, p->d_ptr.p, p->d_ent.p,
+                                                             p->set_out.p, p->n_blk, p->jdiag.p);
+    CKL(p);
+  }
+  launch_sum_energies(p->set_out.p, p->n_sets, p->edge_out.p, dense_on ? p->n_dir : 0, nullptr, 0,
+                      p->dscal.p, 0, s);
+  CKL(p);
+  p->dense_active = dense_on;
+  p->have_system = true;
+  p->have_solution = false;
+  return SFB_OK;
+}
+
+int enqueue_energy_frozen(sfb_problem* p, int dense, double* dout3) {
+  cudaStream_t s = p->stream;
+  SparseArgs sa = sparse_args(p);
+  sa.energy_only = 1;
+  sa.w_sparse = 1.0;
+  {
+    ProfScope ps(p->prof, 4, s);
+    launch_sparse(sa, s);
+  }
+  CKL(p);
+  const bool d = dense && p->dense_active && p->n_items > 0;
+  if (d) {
+    DenseArgs da = dense_args(p);
+    da.do_photo = p->last_do_photo;
+    da.do_geo = p->last_do_geo;
+    ProfScope ps(p->prof, 1, s);
+    launch_dense_energy(da, p->item_e2.p, s);
+    CKL(p);
+  }
+  launch_sum_energies(p->set_out.p, p->n_sets, nullptr, 0, p->item_e2.p, d ? p->n_items : 0, dout3,
+                      1, s);
+  CKL(p);
+  return SFB_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+const char* sfb_last_error(const void* handle) {
+  if (handle) return static_cast<const Handle*>(handle)->err.c_str();
+  return g_tls_err.c_str();
+}
+
+int sfb_abi_version(void) { return SFB_ABI_VERSION; }
+
+int sfb_ctx_create(int32_t device, sfb_ctx** out) {
+  if (!out) return fail(nullptr, SFB_E_ARG, "out is null");
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    return fail(nullptr, SFB_E_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+  if (device < 0 || device >= ndev) return fail(nullptr, SFB_E_ARG, "bad device index");
+  e = cudaSetDevice(device);
+  if (e != cudaSuccess) return fail(nullptr, SFB_E_CUDA, cudaGetErrorString(e));
+  sfb_ctx* c = new sfb_ctx();
+  c->device = device;
+  cudaDeviceGetAttribute(&c->n_sm, cudaDevAttrMultiProcessorCount, device);
+  e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(nullptr, SFB_E_CUDA, cudaGetErrorString(e));
+  }
+  *out = c;
+  return SFB_OK;
+}
+
+int sfb_ctx_destroy(sfb_ctx* c) {
+  if (!c) return SFB_OK;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (auto& kv : c->block_refs) cudaFree(kv.first);
+  c->staging.release();
+  c->counts.release();
+  cudaStreamDestroy(c->stream);
+  delete c;
+  return SFB_OK;
+}
+
+int sfb_ctx_set_rounding(sfb_ctx* c, const sfb_rounding* r) {
+  if (!c || !r) return fail(c, SFB_E_ARG, "null argument");
+  const int32_t v[6] = {r->matvec_c, r->matvec_f, r->gemm33, r->apply_n, r->apply_1, r->dot3};
+  for (int k = 0; k < 6; ++k)
+    if (v[k] < 0 || v[k] > 5) return fail(c, SFB_E_ARG, "rounding code out of range");
+  c->rd = Rounding{r->matvec_c, r->matvec_f, r->gemm33, r->apply_n, r->apply_1, r->dot3};
+  return SFB_OK;
+}
+
+int sfb_frames_upload(sfb_ctx* c, int32_t n, const sfb_frame_desc* d, int32_t* slots_out) {
+  if (!c || n < 0 || (n > 0 && (!d || !slots_out))) return fail(c, SFB_E_ARG, "bad arguments");
+  if (n == 0) return SFB_OK;
+  CK(c, cudaSetDevice(c->device));
+  size_t total = 0, stage = 0;
+  for (int k = 0; k < n; ++k) {
+    const int64_t hw = (int64_t)d[k].width * d[k].height;
+    if (d[k].width < 2 || d[k].height < 2)
+      return fail(c, SFB_E_ARG, "frames must be at least 2x2 (bilinear sampling)");
+    if (!d[k].valid_depth || !d[k].valid_normal || !d[k].points || !d[k].normals || !d[k].grad)
+      return fail(c, SFB_E_ARG, "null frame plane");
+    total += align256(hw * 16) * 2 + align256(hw * 8) + align256(hw * 32);
+    stage += align256(hw * 2) + align256(hw * 24) + align256(hw * 8);
+  }
+  void* block = nullptr;
+  CK(c, cudaMalloc(&block, total));
+  CK(c, c->staging.ensure(stage));
+  CK(c, c->counts.ensure(2 * (size_t)n));
+  CK(c, cudaMemsetAsync(c->counts.p, 0, sizeof(int) * 2 * n, c->stream));
+  char* dst = static_cast<char*>(block);
+  char* stg = reinterpret_cast<char*>(c->staging.p);
+  std::vector<FrameDev> devs(n);
+  for (int k = 0; k < n; ++k) {
+    const int w = d[k].width, h = d[k].height;
+    const size_t hw = (size_t)w * h;
+    FrameDev f{};
+    f.P = reinterpret_cast<float4*>(dst); dst += align256(hw * 16);
+    f.N = reinterpret_cast<float4*>(dst); dst += align256(hw * 16);
+    f.G = reinterpret_cast<float2*>(dst); dst += align256(hw * 8);
+    f.T = reinterpret_cast<float4*>(dst); dst += align256(hw * 32);
+    f.fx = d[k].fx; f.fy = d[k].fy; f.cx = d[k].cx; f.cy = d[k].cy;
+    f.w = w; f.h = h;
+    uint8_t* svd = reinterpret_cast<uint8_t*>(stg);
+    uint8_t* svn = svd + hw;
+    stg += align256(hw * 2);
+    float* spt = reinterpret_cast<float*>(stg);
+    float* snr = spt + 3 * hw;
+    stg += align256(hw * 24);
+    float* sgr = reinterpret_cast<float*>(stg);
+    stg += align256(hw * 8);
+    CK(c, cudaMemcpyAsync(svd, d[k].valid_depth, hw, cudaMemcpyHostToDevice, c->stream));
+    CK(c, cudaMemcpyAsync(svn, d[k].valid_normal, hw, cudaMemcpyHostToDevice, c->stream));
+    CK(c, cudaMemcpyAsync(spt, d[k].points, hw * 12, cudaMemcpyHostToDevice, c->stream));
+    CK(c, cudaMemcpyAsync(snr, d[k].normals, hw * 12, cudaMemcpyHostToDevice, c->stream));
+    CK(c, cudaMemcpyAsync(sgr, d[k].grad, hw * 8, cudaMemcpyHostToDevice, c->stream));
+    PackArgs pa{svd, svn, spt, snr, sgr, const_cast<float4*>(f.P), const_cast<float4*>(f.N),
+                const_cast<float2*>(f.G), const_cast<float4*>(f.T), w, h, c->counts.p + 2 * k};
+    launch_pack(pa, c->stream);
+    CKL(c);
+    devs[k] = f;
+  }
+  std::vector<int> cnt(2 * n);
+  CK(c, cudaMemcpyAsync(cnt.data(), c->counts.p, sizeof(int) * 2 * n, cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaStreamSynchronize(c->stream));
+  c->block_refs[block] = n;
+  int search = 0;
+  for (int k = 0; k < n; ++k) {
+    devs[k].n_valid_depth = cnt[2 * k];
+    devs[k].n_valid_geo = cnt[2 * k + 1];
+    while (search < (int)c->slots.size() && c->slots[search].alive) ++search;
+    if (search == (int)c->slots.size()) c->slots.emplace_back();
+    Slot& sl = c->slots[search];
+    sl.dev = devs[k];
+    sl.block = block;
+    sl.alive = true;
+    slots_out[k] = search;
+  }
+  return SFB_OK;
+}
+
+int sfb_frames_release(sfb_ctx* c, int32_t n, const int32_t* slots) {
+  if (!c || (n > 0 && !slots)) return fail(c, SFB_E_ARG, "bad arguments");
+  cudaSetDevice(c->device);
+  for (int k = 0; k < n; ++k) {
+    const int s = slots[k];
+    if (s < 0 || s >= (int)c->slots.size() || !c->slots[s].alive) continue;
+    Slot& sl = c->slots[s];
+    sl.alive = false;
+    auto it = c->block_refs.find(sl.block);
+    if (it != c->block_refs.end() && --it->second == 0) {
+      cudaDeviceSynchronize();
+      cudaFree(it->first);
+      c->block_refs.erase(it);
+    }
+    sl.block = nullptr;
+  }
+  return SFB_OK;
+}
+
+int sfb_problem_create(sfb_ctx* c, int32_t n_frames, const int32_t* slots, int32_t n_sets,
+                       const int32_t* set_fi, const int32_t* set_fj, const int64_t* set_off,
+                       const double* pts_i, const double* pts_j, sfb_problem** out) {
+  if (!c || !out || n_frames < 1 || n_sets < 0) return fail(c, SFB_E_ARG, "bad arguments");
+  if (n_sets > 0 && (!set_fi || !set_fj || !set_off)) return fail(c, SFB_E_ARG, "null set arrays");
+  CK(c, cudaSetDevice(c->device));
+  sfb_problem* p = new sfb_problem();
+  p->ctx = c;
+  p->n = n_frames;
+  p->n_blk = n_frames - 1;
+  auto bail = [&](int code, const std::string& m) {
+    sfb_problem_destroy(p);
+    return fail(c, code, m);
+  };
+  if (cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess)
+    return bail(SFB_E_CUDA, "stream create failed");
+  cudaStream_t s = p->stream;
+  p->frames_h.assign(n_frames, FrameDev{});
+  if (slots) {
+    p->has_frames = true;
+    p->slots.assign(slots, slots + n_frames);
+    for (int k = 0; k < n_frames; ++k) {
+      const int sl = slots[k];
+      if (sl < 0 || sl >= (int)c->slots.size() || !c->slots[sl].alive)
+        return bail(SFB_E_ARG, "frame slot not uploaded");
+      p->frames_h[k] = c->slots[sl].dev;
+    }
+  }
+  if (upload_vec(p->frames, p->frames_h, s) != cudaSuccess) return bail(SFB_E_OOM, "frames");
+  if (p->poses.ensure(n_frames) || p->best.ensure(n_frames)) return bail(SFB_E_OOM, "poses");
+  // identity poses until set
+  std::vector<PoseDev> idp(n_frames);
+  for (auto& q : idp) {
+    std::memset(&q, 0, sizeof(q));
+    q.R[0] = q.R[4] = q.R[8] = 1.0;
+  }
+  if (upload_vec(p->poses, idp, s) || upload_vec(p->best, idp, s)) return bail(SFB_E_CUDA, "poses");
+  // sparse term (build_sparse_term, solver.py:89-111)
+  p->n_sets = n_sets;
+  p->n_corr = n_sets > 0 ? set_off[n_sets] : 0;
+  for (int k = 0; k < n_sets; ++k) {
+    if (set_fi[k] < 0 || set_fi[k] >= n_frames || set_fj[k] < 0 || set_fj[k] >= n_frames ||
+        set_off[k + 1] < set_off[k])
+      return bail(SFB_E_ARG, "bad correspondence set");
+  }
+  p->set_fi_h.assign(set_fi, set_fi + n_sets);
+  p->set_fj_h.assign(set_fj, set_fj + n_sets);
+  std::vector<int64_t> off(set_off, set_off + (n_sets > 0 ? n_sets + 1 : 0));
+  if (off.empty()) off.push_back(0);
+  if (upload_vec(p->set_fi, p->set_fi_h, s) || upload_vec(p->set_fj, p->set_fj_h, s) ||
+      upload_vec(p->set_off, off, s))
+    return bail(SFB_E_OOM, "sets");
+  const size_t nc = (size_t)std::max<int64_t>(p->n_corr, 1) * 3;
+  if (p->pts_i.ensure(nc) || p->pts_j.ensure(nc) || p->world_i.ensure(nc) || p->world_j.ensure(nc) ||
+      p->set_out.ensure((size_t)std::max(1, n_sets) * SFB_SET_STRIDE))
+    return bail(SFB_E_OOM, "correspondences");
+  if (p->n_corr > 0) {
+    if (!pts_i || !pts_j) return bail(SFB_E_ARG, "null points");
+    if (cudaMemcpyAsync(p->pts_i.p, pts_i, sizeof(double) * 3 * p->n_corr, cudaMemcpyHostToDevice, s) ||
+        cudaMemcpyAsync(p->pts_j.p, pts_j, sizeof(double) * 3 * p->n_corr, cudaMemcpyHostToDevice, s))
+      return bail(SFB_E_CUDA, "points upload");
+  }
+  const size_t nv = (size_t)std::max(1, 6 * p->n_blk);
+  if (p->g.ensure(nv) || p->x.ensure(nv) || p->r.ensure(nv) || p->z.ensure(nv) || p->pv.ensure(nv) ||
+      p->Ap.ensure(nv) || p->inv_diag.ensure(nv) || p->bvec.ensure(nv) || p->jdiag.ensure(nv) || p->tmp.ensure(2 * nv) ||
+      p->part.ensure(4 * 1024) || p->flags.ensure(64) || p->dscal.ensure(64))
+    return bail(SFB_E_OOM, "vectors");
+  if (cudaMallocHost(&p->hscal, 64 * sizeof(double)) != cudaSuccess) return bail(SFB_E_OOM, "pinned");
+  int rc = rebuild_structure(p, 0);
+  if (rc) {
+    std::string m = p->err;
+    sfb_problem_destroy(p);
+    return fail(c, rc, m);
+  }
+  *out = p;
+  return SFB_OK;
+}
+
+int sfb_problem_destroy(sfb_problem* p) {
+  if (!p) return SFB_OK;
+  cudaSetDevice(p->ctx->device);
+  if (p->stream) cudaStreamSynchronize(p->stream);
+  DBuf<int>* ib[] = {&p->set_fi, &p->set_fj, &p->edge_item_ptr, &p->d_ptr, &p->d_ent, &p->b_ptr,
+                     &p->b_ent, &p->row_ptr, &p->row_ent, &p->row_col, &p->flags};
+  for (auto* b : ib) b->release();
+  DBuf<double>* db[] = {&p->pts_i, &p->pts_j, &p->world_i, &p->world_j, &p->set_out,
+                        &p->item_out, &p->edge_out, &p->item_e2, &p->D, &p->B, &p->g, &p->x,
+                        &p->r, &p->z, &p->pv, &p->Ap, &p->inv_diag, &p->bvec, &p->part, &p->tmp, &p->jdiag,
+                        &p->dscal};
+  for (auto* b : db) b->release();
+  p->frames.release();
+  p->poses.release();
+  p->best.release();
+  p->set_off.release();
+  p->dir_edges.release();
+  p->items.release();
+  p->photo_off.release();
+  p->geo_off.release();
+  p->photo_mask.release();
+  p->geo_tgt.release();
+  p->prof.destroy();
+  if (p->hscal) cudaFreeHost(p->hscal);
+  if (p->stream) cudaStreamDestroy(p->stream);
+  delete p;
+  return SFB_OK;
+}
+
+int sfb_problem_stream(sfb_problem* p, void** s) {
+  if (!p || !s) return fail(p, SFB_E_ARG, "null argument");
+  *s = (void*)p->stream;
+  return SFB_OK;
+}
+
+int sfb_set_poses(sfb_problem* p, const double* R, const double* t, const uint8_t* fl) {
+  if (!p || !R || !t) return fail(p, SFB_E_ARG, "null argument");
+  CK(p, cudaSetDevice(p->ctx->device));
+  std::vector<PoseDev> h(p->n);
+  for (int k = 0; k < p->n; ++k) {
+    std::memset(&h[k], 0, sizeof(PoseDev));
+    std::memcpy(h[k].R, R + 9 * k, 9 * sizeof(double));
+    std::memcpy(h[k].t, t + 3 * k, 3 * sizeof(double));
+    h[k].f_layout = fl ? (fl[k] ? 1 : 0) : 0;
+  }
+  CK(p, cudaMemcpyAsync(p->poses.p, h.data(), sizeof(PoseDev) * p->n, cudaMemcpyHostToDevice, p->stream));
+  CK(p, cudaStreamSynchronize(p->stream));
+  return SFB_OK;
+}
+
+int sfb_get_poses(sfb_problem* p, double* R, double* t) {
+  if (!p || !R || !t) return fail(p, SFB_E_ARG, "null argument");
+  CK(p, cudaSetDevice(p->ctx->device));
+  std::vector<PoseDev> h(p->n);
+  CK(p, cudaMemcpyAsync(h.data(), p->poses.p, sizeof(PoseDev) * p->n, cudaMemcpyDeviceToHost, p->stream));
+  CK(p, cudaStreamSynchronize(p->stream));
+  for (int k = 0; k < p->n; ++k) {
+    std::memcpy(R + 9 * k, h[k].R, 9 * sizeof(double));
+    std::memcpy(t + 3 * k, h[k].t, 3 * sizeof(double));
+  }
+  return SFB_OK;
+}
+
+int sfb_save_best(sfb_problem* p) {
+  if (!p) return fail(p, SFB_E_ARG, "null problem");
+  CK(p, cudaMemcpyAsync(p->best.p, p->poses.p, sizeof(PoseDev) * p->n, cudaMemcpyDeviceToDevice, p->stream));
+  return SFB_OK;
+}
+
+int sfb_restore_best(sfb_problem* p) {
+  if (!p) return fail(p, SFB_E_ARG, "null problem");
+  CK(p, cudaMemcpyAsync(p->poses.p, p->best.p, sizeof(PoseDev) * p->n, cudaMemcpyDeviceToDevice, p->stream));
+  CK(p, cudaStreamSynchronize(p->stream));
+  return SFB_OK;
+}
+
+int sfb_build_dense_edges(sfb_problem* p, double cos_min, int64_t* n_out) {
+  if (!p || !n_out) return fail(p, SFB_E_ARG, "null argument");
+  if (!p->has_frames) return fail(p, SFB_E_STATE, "problem has no frames (caches=None)");
+  CK(p, cudaSetDevice(p->ctx->device));
+  cudaStream_t s = p->stream;
+  const int n = p->n;
+  const int64_t P = (int64_t)n * (n - 1) / 2;
+  p->edges.clear();
+  if (P > 0) {
+    if (P > INT32_MAX) return fail(p, SFB_E_ARG, "too many frames for the pair filter");
+    DBuf<int2> all, cand, sel;
+    DBuf<uint8_t> fl, pass, temp;
+    DBuf<int> cnt;
+    CK(p, all.ensure(P));
+    CK(p, cand.ensure(P));
+    CK(p, fl.ensure(P));
+    CK(p, cnt.ensure(2));
+    dim3 grid((n + 255) / 256, n - 1);
+    {
+      ProfScope ps(p->prof, 3, s);
+      sfb_count_launch();
+      k_enumerate_pairs<<<grid, 256, 0, s>>>(n, all.p);
+      CKL(p);
+      launch_angle_gate(p->poses.p, n, p->ctx->rd, cos_min, fl.p, s);
+      CKL(p);
+      sfb_count_launch(2);
+      CK(p, select_flagged(all.p, fl.p, cand.p, cnt.p, (int)P, temp, s));
+    }
+    int nc = 0;
+    CK(p, cudaMemcpyAsync(&nc, cnt.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(p, cudaStreamSynchronize(s));
+    if (nc > 0) {
+      CK(p, pass.ensure(nc));
+      CK(p, sel.ensure(nc));
+      {
+        ProfScope ps(p->prof, 3, s);
+        launch_overlap(p->frames.p, p->poses.p, cand.p, nc, p->ctx->rd, 0, pass.p, nullptr, s);
+        CKL(p);
+        sfb_count_launch(2);
+        CK(p, select_flagged(cand.p, pass.p, sel.p, cnt.p + 1, nc, temp, s));
+      }
+      int ne = 0;
+      CK(p, cudaMemcpyAsync(&ne, cnt.p + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+      CK(p, cudaStreamSynchronize(s));
+      p->edges.resize(ne);
+      if (ne > 0)
+        CK(p, cudaMemcpyAsync(p->edges.data(), sel.p, sizeof(int2) * ne, cudaMemcpyDeviceToHost, s));
+      CK(p, cudaStreamSynchronize(s));
+    }
+    all.release(); cand.release(); sel.release(); fl.release(); pass.release(); temp.release(); cnt.release();
+  }
+  *n_out = (int64_t)p->edges.size();
+  return rebuild_structure(p, p->struct_bidir < 0 ? 0 : p->struct_bidir);
+}
+
+int sfb_get_dense_edges(sfb_problem* p, int32_t* out) {
+  if (!p || (!out && !p->edges.empty())) return fail(p, SFB_E_ARG, "null argument");
+  for (size_t k = 0; k < p->edges.size(); ++k) {
+    out[2 * k] = p->edges[k].x;
+    out[2 * k + 1] = p->edges[k].y;
+  }
+  return SFB_OK;
+}
+
+int sfb_set_dense_edges(sfb_problem* p, int64_t ne, const int32_t* pairs) {
+  if (!p || ne < 0 || (ne > 0 && !pairs)) return fail(p, SFB_E_ARG, "bad arguments");
+  std::vector<int2> e(ne);
+  for (int64_t k = 0; k < ne; ++k) {
+    const int a = pairs[2 * k], b = pairs[2 * k + 1];
+    if (a < 0 || a >= p->n || b < 0 || b >= p->n) return fail(p, SFB_E_ARG, "edge frame out of range");
+    e[k] = make_int2(a, b);
+  }
+  p->edges = e;
+  return rebuild_structure(p, p->struct_bidir < 0 ? 0 : p->struct_bidir);
+}
+
+int sfb_frustum_overlap(sfb_problem* p, int64_t np_, const int32_t* pairs, double* out) {
+  if (!p || np_ < 0 || (np_ > 0 && (!pairs || !out))) return fail(p, SFB_E_ARG, "bad arguments");
+  if (!p->has_frames) return fail(p, SFB_E_STATE, "problem has no frames");
+  if (np_ == 0) return SFB_OK;
+  CK(p, cudaSetDevice(p->ctx->device));
+  cudaStream_t s = p->stream;
+  std::vector<int2> h(np_);
+  for (int64_t k = 0; k < np_; ++k) {
+    h[k] = make_int2(pairs[2 * k], pairs[2 * k + 1]);
+    if (h[k].x < 0 || h[k].x >= p->n || h[k].y < 0 || h[k].y >= p->n)
+      return fail(p, SFB_E_ARG, "pair frame out of range");
+  }
+  DBuf<int2> d;
+  DBuf<int> cnt;
+  CK(p, upload_vec(d, h, s));
+  CK(p, cnt.ensure(2 * np_));
+  launch_overlap(p->frames.p, p->poses.p, d.p, (int)np_, p->ctx->rd, 1, nullptr, cnt.p, s);
+  CKL(p);
+  std::vector<int> hc(2 * np_);
+  CK(p, cudaMemcpyAsync(hc.data(), cnt.p, sizeof(int) * 2 * np_, cudaMemcpyDeviceToHost, s));
+  CK(p, cudaStreamSynchronize(s));
+  for (int64_t k = 0; k < np_; ++k) {
+    const int total = p->frames_h[h[k].x].n_valid_depth;
+    out[k] = total > 0 ? (double)hc[2 * k] / (double)total : 0.0;
+  }
+  d.release();
+  cnt.release();
+  return SFB_OK;
+}
+
+int sfb_linearize(sfb_problem* p, const sfb_weights* w, double w_dense, const sfb_config* cfg,
+                  double e3[3]) {
+  if (!p || !w || !cfg || !e3) return fail(p, SFB_E_ARG, "null argument");
+  CK(p, cudaSetDevice(p->ctx->device));
+  int rc = enqueue_linearize(p, w, w_dense, cfg);
+  if (rc) return rc;
+  CK(p, cudaMemcpyAsync(p->hscal, p->dscal.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+  CK(p, cudaStreamSynchronize(p->stream));
+  for (int k = 0; k < 3; ++k) e3[k] = p->hscal[k];
+  return SFB_OK;
+}
+
+int sfb_pcg(sfb_problem* p, int32_t max_it, double tol, int32_t restart, int32_t* iters,
+            double* rel, int32_t* status) {
+  if (!p || !iters || !rel || !status) return fail(p, SFB_E_ARG, "null argument");
+  if (!p->have_system) return fail(p, SFB_E_STATE, "pcg before linearize");
+  if (restart < 1) return fail(p, SFB_E_ARG, "pcg_restart_interval must be >= 1");
+  CK(p, cudaSetDevice(p->ctx->device));
+  PcgArgs a = pcg_args(p);
+  a.max_it = max_it;
+  a.tol = tol;
+  a.restart = restart;
+  a.out_scalars = p->dscal.p + 8;
+  a.skip = nullptr;
+  if (p->n_blk > 0) {
+    ProfScope ps(p->prof, 2, p->stream);
+    CK(p, launch_pcg(a, p->ctx->n_sm, p->stream));
+  } else {
+    double z3[3] = {0, 0, 0};
+    CK(p, cudaMemcpyAsync(p->dscal.p + 8, z3, sizeof(z3), cudaMemcpyHostToDevice, p->stream));
+  }
+  CK(p, cudaMemcpyAsync(p->hscal + 8, p->dscal.p + 8, 3 * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+  CK(p, cudaStreamSynchronize(p->stream));
+  *iters = (int32_t)p->hscal[8];
+  *rel = p->hscal[9];
+  *status = p->hscal[10] != 0.0 ? SFB_E_PCG_NONFINITE : SFB_OK;
+  p->have_solution = true;
+  return SFB_OK;
+}
+
+static int copy_out(sfb_problem* p, double* dst, const double* src, size_t n);
+
+int sfb_get_solution(sfb_problem* p, double* x) {
+  if (!p || (!x && p->n_blk > 0)) return fail(p, SFB_E_ARG, "null argument");
+  if (!p->have_solution) return fail(p, SFB_E_STATE, "no PCG solution");
+  CK(p, cudaSetDevice(p->ctx->device));
+  return copy_out(p, x, p->x.p, 6 * (size_t)p->n_blk);
+}
+
+int sfb_pcg_dense(sfb_ctx* c, int32_t n, const double* A, const double* rhs, const double* diag,
+                  int32_t max_it, double tol, int32_t restart, double* x_out, int32_t* iters,
+                  double* rel, int32_t* status) {
+  if (!c || n < 0 || (n > 0 && (!A || !rhs || !diag || !x_out)) || !iters || !rel || !status)
+    return fail(c, SFB_E_ARG, "bad arguments");
+  if (restart < 1) return fail(c, SFB_E_ARG, "restart_interval must be >= 1");
+  if (n == 0) {
+    *iters = 0;
+    *rel = 0.0;
+    *status = SFB_OK;
+    return SFB_OK;
+  }
+  CK(c, cudaSetDevice(c->device));
+  const int nb = (n + 5) / 6, n6 = 6 * nb;
+  std::vector<double> hA((size_t)n6 * n6, 0.0), hg(n6, 0.0), hd(n6, 1.0);
+  for (int r = 0; r < n; ++r) {
+    std::memcpy(&hA[(size_t)r * n6], A + (size_t)r * n, sizeof(double) * n);
+    hg[r] = -rhs[r];
+    hd[r] = diag[r];
+  }
+  DBuf<double> dA, vec;
+  CK(c, dA.ensure(hA.size()));
+  CK(c, vec.ensure((size_t)n6 * 10 + 4 * 1024 + 8));
+  cudaStream_t s = c->stream;
+  CK(c, cudaMemcpyAsync(dA.p, hA.data(), sizeof(double) * hA.size(), cudaMemcpyHostToDevice, s));
+  double* v = vec.p;
+  PcgArgs a{};
+  a.n_blk = nb;
+  a.g = v;
+  a.jdiag = v + n6;
+  a.x = v + 2 * n6;
+  a.r = v + 3 * n6;
+  a.z = v + 4 * n6;
+  a.p = v + 5 * n6;
+  a.Ap = v + 6 * n6;
+  a.inv_diag = v + 7 * n6;
+  a.b = v + 8 * n6;
+  a.out_scalars = v + 9 * n6;
+  a.part = v + 10 * n6;
+  a.max_it = max_it;
+  a.tol = tol;
+  a.restart = restart;
+  CK(c, cudaMemcpyAsync(const_cast<double*>(a.g), hg.data(), sizeof(double) * n6, cudaMemcpyHostToDevice, s));
+  CK(c, cudaMemcpyAsync(const_cast<double*>(a.jdiag), hd.data(), sizeof(double) * n6, cudaMemcpyHostToDevice, s));
+  CK(c, launch_pcg_dense(a, dA.p, c->n_sm, s));
+  double sc[3];
+  CK(c, cudaMemcpyAsync(x_out, a.x, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+  CK(c, cudaMemcpyAsync(sc, a.out_scalars, sizeof(sc), cudaMemcpyDeviceToHost, s));
+  CK(c, cudaStreamSynchronize(s));
+  *iters = (int32_t)sc[0];
+  *rel = sc[1];
+  *status = sc[2] != 0.0 ? SFB_E_PCG_NONFINITE : SFB_OK;
+  dA.release();
+  vec.release();
+  return SFB_OK;
+}
+
+int sfb_apply_step(sfb_problem* p, double* step_norm) {
+  if (!p || !step_norm) return fail(p, SFB_E_ARG, "null argument");
+  if (!p->have_solution) return fail(p, SFB_E_STATE, "apply_step before pcg");
+  CK(p, cudaSetDevice(p->ctx->device));
+  {
+    ProfScope ps(p->prof, 6, p->stream);
+    launch_pose_update(p->poses.p, p->n, p->x.p, p->dscal.p + 12, nullptr, p->stream);
+  }
+  CKL(p);
+  CK(p, cudaMemcpyAsync(p->hscal + 12, p->dscal.p + 12, sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+  CK(p, cudaStreamSynchronize(p->stream));
+  *step_norm = p->n_blk > 0 ? p->hscal[12] : 0.0;
+  return SFB_OK;
+}
+
+int sfb_energy_frozen(sfb_problem* p, int32_t dense, double e3[3]) {
+  if (!p || !e3) return fail(p, SFB_E_ARG, "null argument");
+  CK(p, cudaSetDevice(p->ctx->device));
+  int rc = enqueue_energy_frozen(p, dense, p->dscal.p + 16);
+  if (rc) return rc;
+  CK(p, cudaMemcpyAsync(p->hscal + 16, p->dscal.p + 16, 3 * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+  CK(p, cudaStreamSynchronize(p->stream));
+  for (int k = 0; k < 3; ++k) e3[k] = p->hscal[16 + k];
+  return SFB_OK;
+}
+
+int sfb_gn_iteration(sfb_problem* p, const sfb_weights* w, double w_dense, const sfb_config* cfg,
+                     int32_t max_it, double tol, int32_t restart, sfb_iter_result* out) {
+  if (!p || !w || !cfg || !out) return fail(p, SFB_E_ARG, "null argument");
+  if (restart < 1) return fail(p, SFB_E_ARG, "pcg_restart_interval must be >= 1");
+  CK(p, cudaSetDevice(p->ctx->device));
+  int rc = enqueue_linearize(p, w, w_dense, cfg);
+  if (rc) return rc;
+  cudaStream_t s = p->stream;
+  if (p->n_blk > 0) {
+    PcgArgs a = pcg_args(p);
+    a.max_it = max_it;
+    a.tol = tol;
+    a.restart = restart;
+    a.out_scalars = p->dscal.p + 8;
+    a.skip = nullptr;
+    {
+      ProfScope ps(p->prof, 2, s);
+      CK(p, launch_pcg(a, p->ctx->n_sm, s));
+    }
+    ProfScope ps(p->prof, 6, s);
+    launch_pose_update(p->poses.p, p->n, p->x.p, p->dscal.p + 12, nullptr, s);
+    CKL(p);
+  }
+  rc = enqueue_energy_frozen(p, w_dense > 0.0, p->dscal.p + 16);
+  if (rc) return rc;
+  CK(p, cudaMemcpyAsync(p->hscal, p->dscal.p, 20 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(p, cudaStreamSynchronize(s));
+  const double* h = p->hscal;
+  out->e_sparse = h[0];
+  out->e_photo = h[1];
+  out->e_geo = h[2];
+  out->pcg_iterations = p->n_blk > 0 ? (int32_t)h[8] : 0;
+  out->pcg_relative = p->n_blk > 0 ? h[9] : 0.0;
+  out->pcg_status = (p->n_blk > 0 && h[10] != 0.0) ? SFB_E_PCG_NONFINITE : SFB_OK;
+  out->step_norm = p->n_blk > 0 ? h[12] : 0.0;
+  out->ea_sparse = h[16];
+  out->ea_photo = h[17];
+  out->ea_geo = h[18];
+  p->have_solution = true;
+  return SFB_OK;
+}
+
+int sfb_system_dims(sfb_problem* p, int32_t* n_vars, int64_t* n_pairs, int64_t* n_corr) {
+  if (!p) return fail(p, SFB_E_ARG, "null problem");
+  if (n_vars) *n_vars = 6 * p->n_blk;
+  if (n_pairs) *n_pairs = p->n_pairs;
+  if (n_corr) *n_corr = p->n_corr;
+  return SFB_OK;
+}
+
+int sfb_matvec(sfb_problem* p, const double* x, double* y) {
+  if (!p || !x || !y) return fail(p, SFB_E_ARG, "null argument");
+  if (!p->have_system) return fail(p, SFB_E_STATE, "matvec before linearize");
+  const int nv = 6 * p->n_blk;
+  if (nv == 0) return SFB_OK;
+  CK(p, cudaSetDevice(p->ctx->device));
+  CK(p, cudaMemcpyAsync(p->tmp.p, x, sizeof(double) * nv, cudaMemcpyHostToDevice, p->stream));
+  PcgArgs a = pcg_args(p);
+  launch_matvec(a, p->tmp.p, p->tmp.p + nv, p->stream);
+  CKL(p);
+  CK(p, cudaMemcpyAsync(y, p->tmp.p + nv, sizeof(double) * nv, cudaMemcpyDeviceToHost, p->stream));
+  CK(p, cudaStreamSynchronize(p->stream));
+  return SFB_OK;
+}
+
+static int copy_out(sfb_problem* p, double* dst, const double* src, size_t n) {
+  if (n == 0) return SFB_OK;
+  CK(p, cudaMemcpyAsync(dst, src, sizeof(double) * n, cudaMemcpyDeviceToHost, p->stream));
+  CK(p, cudaStreamSynchronize(p->stream));
+  return SFB_OK;
+}
+
+int sfb_get_gradient(sfb_problem* p, double* g) {
+  if (!p || !g) return fail(p, SFB_E_ARG, "null argument");
+  if (!p->have_system) return fail(p, SFB_E_STATE, "no system");
+  return copy_out(p, g, p->g.p, 6 * (size_t)p->n_blk);
+}
+
+}  // extern "C"
+
+namespace {
+__global__ void k_jacobi_diag(const double* D, const int* d_ptr, const int* d_ent,
+                              const double* set_out, int n_blk, double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 6 * n_blk) return;
+  const int v = i / 6, c = i % 6;
+  double d = D[(int64_t)v * 36 + c * 7];
+  // _jacobi_diagonal (solver.py:412-428) has no cross term for a set whose
+  // two frames coincide; remove the H_ij + H_ij^T diagonal it would add.
+  for (int k = d_ptr[v]; k < d_ptr[v + 1]; ++k)
+    if ((d_ent[k] & 7) == 2) d -= 2.0 * set_out[(int64_t)(d_ent[k] >> 3) * SFB_SET_STRIDE + 72 + c * 7];
+  out[i] = d;
+}
+}  // namespace
+
+extern "C" {
+
+int sfb_get_diagonal(sfb_problem* p, double* d) {
+  if (!p || !d) return fail(p, SFB_E_ARG, "null argument");
+  if (!p->have_system) return fail(p, SFB_E_STATE, "no system");
+  const int nv = 6 * p->n_blk;
+  if (nv == 0) return SFB_OK;
+  CK(p, cudaSetDevice(p->ctx->device));
+  return copy_out(p, d, p->jdiag.p, nv);
+}
+
+int sfb_get_blocks(sfb_problem* p, double* diag_blocks, double* pair_blocks, int32_t* pair_vars) {
+  if (!p) return fail(p, SFB_E_ARG, "null problem");
+  if (!p->have_system) return fail(p, SFB_E_STATE, "no system");
+  CK(p, cudaSetDevice(p->ctx->device));
+  if (diag_blocks) {
+    int rc = copy_out(p, diag_blocks, p->D.p, 36 * (size_t)p->n_blk);
+    if (rc) return rc;
+  }
+  if (pair_blocks) {
+    int rc = copy_out(p, pair_blocks, p->B.p, 36 * (size_t)p->n_pairs);
+    if (rc) return rc;
+  }
+  if (pair_vars)
+    for (int q = 0; q < p->n_pairs; ++q) {
+      pair_vars[2 * q] = p->pair_vars[q].x;
+      pair_vars[2 * q + 1] = p->pair_vars[q].y;
+    }
+  return SFB_OK;
+}
+
+int sfb_get_sparse_world(sfb_problem* p, double* wi, double* wj) {
+  if (!p || !wi || !wj) return fail(p, SFB_E_ARG, "null argument");
+  if (!p->have_system) return fail(p, SFB_E_STATE, "no system");
+  int rc = copy_out(p, wi, p->world_i.p, 3 * (size_t)p->n_corr);
+  if (rc) return rc;
+  return copy_out(p, wj, p->world_j.p, 3 * (size_t)p->n_corr);
+}
+
+int sfb_sparse_residuals(sfb_problem* p, double* res) {
+  if (!p || (!res && p->n_corr > 0)) return fail(p, SFB_E_ARG, "null argument");
+  if (p->n_corr == 0) return SFB_OK;
+  CK(p, cudaSetDevice(p->ctx->device));
+  DBuf<double> d;
+  CK(p, d.ensure(3 * (size_t)p->n_corr));
+  launch_sparse_residuals(sparse_args(p), d.p, nullptr, p->stream);
+  CKL(p);
+  int rc = copy_out(p, res, d.p, 3 * (size_t)p->n_corr);
+  d.release();
+  return rc;
+}
+
+int sfb_sparse_set_max(sfb_problem* p, double* out) {
+  if (!p || (!out && p->n_sets > 0)) return fail(p, SFB_E_ARG, "null argument");
+  if (p->n_sets == 0) return SFB_OK;
+  CK(p, cudaSetDevice(p->ctx->device));
+  DBuf<double> d;
+  CK(p, d.ensure(p->n_sets));
+  launch_sparse_residuals(sparse_args(p), nullptr, d.p, p->stream);
+  CKL(p);
+  int rc = copy_out(p, out, d.p, p->n_sets);
+  d.release();
+  return rc;
+}
+
+int sfb_associate(sfb_problem* p, int32_t fi, int32_t fj, int32_t kind, const sfb_config* cfg,
+                  uint8_t* sel, int32_t* tgt) {
+  if (!p || !cfg || !sel || !tgt) return fail(p, SFB_E_ARG, "null argument");
+  if (!p->has_frames) return fail(p, SFB_E_STATE, "problem has no frames");
+  if (fi < 0 || fi >= p->n || fj < 0 || fj >= p->n || kind < 0 || kind > 1)
+    return fail(p, SFB_E_ARG, "bad edge");
+  if (cfg->dense_pixel_stride < 1) return fail(p, SFB_E_ARG, "dense_pixel_stride must be >= 1");
+  CK(p, cudaSetDevice(p->ctx->device));
+  const FrameDev& F = p->frames_h[fi];
+  const size_t hw = (size_t)F.w * F.h;
+  DBuf<uint8_t> ds;
+  DBuf<int> dt;
+  CK(p, ds.ensure(hw));
+  CK(p, dt.ensure(hw));
+  DenseArgs a = dense_args(p);
+  a.geo_dmax = cfg->geo_distance_max;
+  a.geo_nmin = cfg->geo_normal_min;
+  a.stride = cfg->dense_pixel_stride;
+  launch_associate(a, fi, fj, kind, ds.p, dt.p, p->stream);
+  CKL(p);
+  CK(p, cudaMemcpyAsync(sel, ds.p, hw, cudaMemcpyDeviceToHost, p->stream));
+  CK(p, cudaMemcpyAsync(tgt, dt.p, hw * sizeof(int), cudaMemcpyDeviceToHost, p->stream));
+  CK(p, cudaStreamSynchronize(p->stream));
+  ds.release();
+  dt.release();
+  return SFB_OK;
+}
+
+int sfb_point_eval(sfb_problem* p, int32_t fi, int32_t fj, int32_t kind, int64_t m,
+                   const double* pts, const double* aux, const double* tg, double* res, double* jac) {
+  if (!p || m < 0 || (m > 0 && (!pts || !aux || !res || (kind == 1 && !tg))))
+    return fail(p, SFB_E_ARG, "bad arguments");
+  if (fi < 0 || fi >= p->n || fj < 0 || fj >= p->n || kind < 0 || kind > 1)
+    return fail(p, SFB_E_ARG, "bad edge");
+  if (kind == 0 && !p->has_frames) return fail(p, SFB_E_STATE, "photo terms need frames");
+  if (m == 0) return SFB_OK;
+  CK(p, cudaSetDevice(p->ctx->device));
+  const int na = kind == 0 ? 2 : 3, nr = kind == 0 ? 2 : 1, nj = kind == 0 ? 12 : 6;
+  DBuf<double> buf;
+  const size_t tot = (size_t)m * (3 + na + 3 + nr + nj);
+  CK(p, buf.ensure(tot));
+  double* dp = buf.p;
+  double* da = dp + 3 * m;
+  double* dt = da + na * m;
+  double* dr = dt + 3 * m;
+  double* dj = dr + nr * m;
+  cudaStream_t s = p->stream;
+  CK(p, cudaMemcpyAsync(dp, pts, sizeof(double) * 3 * m, cudaMemcpyHostToDevice, s));
+  CK(p, cudaMemcpyAsync(da, aux, sizeof(double) * na * m, cudaMemcpyHostToDevice, s));
+  if (kind == 1) CK(p, cudaMemcpyAsync(dt, tg, sizeof(double) * 3 * m, cudaMemcpyHostToDevice, s));
+  launch_point_eval(p->frames.p, p->poses.p, fi, fj, kind, m, dp, da, dt, dr, jac ? dj : nullptr, s);
+  CKL(p);
+  CK(p, cudaMemcpyAsync(res, dr, sizeof(double) * nr * m, cudaMemcpyDeviceToHost, s));
+  if (jac) CK(p, cudaMemcpyAsync(jac, dj, sizeof(double) * nj * m, cudaMemcpyDeviceToHost, s));
+  CK(p, cudaStreamSynchronize(s));
+  buf.release();
+  return SFB_OK;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int sfb_profile(sfb_problem* p, int32_t enable) {
+  if (!p) return fail(p, SFB_E_ARG, "null problem");
+  p->prof.on = enable != 0;
+  return SFB_OK;
+}
+
+int sfb_profile_read(sfb_problem* p, double* ms, int64_t* launches, int32_t reset) {
+  if (!p) return fail(p, SFB_E_ARG, "null problem");
+  CK(p, cudaSetDevice(p->ctx->device));
+  CK(p, cudaStreamSynchronize(p->stream));
+  p->prof.drain();
+  for (int k = 0; k < SFB_PROF_CLASSES; ++k) {
+    if (ms) ms[k] = p->prof.ms[k];
+    if (launches) launches[k] = p->prof.n[k];
+    if (reset) {
+      p->prof.ms[k] = 0.0;
+      p->prof.n[k] = 0;
+    }
+  }
+  return SFB_OK;
+}
+
+int sfb_launch_count(int64_t* out) {
+  if (!out) return fail(nullptr, SFB_E_ARG, "null argument");
+  *out = g_launches.load();
+  return SFB_OK;
+}
+
+}  // extern "C"

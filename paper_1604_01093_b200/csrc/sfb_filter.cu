@@ -1,0 +1,104 @@
+// Frame-pair filter: build_dense_edges (solver.py:130-148) with
+// view_angle_deg and frustum_overlap (frames.py:154-188), bit-exact.
+//
+//  k_angle_gate  one thread per pair a<b: clip(z_a . z_b) >= cos_min, the dot
+//                in NumPy's np.dot FMA order.  cos_min is the exact preimage
+//                of `degrees(arccos(c)) < view_angle_max_deg` (host bisection).
+//  k_overlap     one CTA per candidate pair, both directions; each direction
+//                maps the source's valid points through pose_b^-1 o pose_a
+//                with NumPy's rounding and stops at the first point inside
+//                the target frustum (overlap > 0 <=> at least one inside),
+//                __syncthreads_or per 256-pixel chunk.  full_count mode counts
+//                every point instead (frustum_overlap's fraction).
+#include "sfb_kernels.cuh"
+
+__global__ void k_angle_gate(const PoseDev* poses, int n, Rounding rd, double cos_min,
+                             uint8_t* flags) {
+  const int a = blockIdx.y;
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b <= a || b >= n) return;
+  const PoseDev& A = poses[a];
+  const PoseDev& B = poses[b];
+  // z axes = rotation[:, 2]
+  double d = dot3o(A.R[2], A.R[5], A.R[8], B.R[2], B.R[5], B.R[8], rd.dot3);
+  d = fmin(fmax(d, -1.0), 1.0);
+  const int64_t q = (int64_t)a * n - ((int64_t)a * (a + 1)) / 2 + (b - a - 1);
+  flags[q] = d >= cos_min ? 1 : 0;
+}
+
+void launch_angle_gate(const PoseDev* poses, int n, Rounding rd, double cos_min, uint8_t* flags,
+                       cudaStream_t s) {
+  if (n < 2) return;
+  dim3 grid((n + 255) / 256, n - 1);
+  sfb_count_launch();
+  k_angle_gate<<<grid, 256, 0, s>>>(poses, n, rd, cos_min, flags);
+}
+
+__device__ __forceinline__ bool point_inside(const Xf& rel, const FrameDev& Fb, const float4 P,
+                                             int ord) {
+  double q[3], u, v;
+  bool front;
+  xf_apply_exact(rel, (double)P.x, (double)P.y, (double)P.z, ord, q);
+  project_exact(Fb.fx, Fb.fy, Fb.cx, Fb.cy, q, &u, &v, &front);
+  return front && u >= 0.0 && u <= (double)(Fb.w - 1) && v >= 0.0 && v <= (double)(Fb.h - 1);
+}
+
+__global__ void __launch_bounds__(256) k_overlap(const FrameDev* frames, const PoseDev* poses,
+                                                 const int2* cand, Rounding rd, int full_count,
+                                                 uint8_t* pass, int* counts) {
+  __shared__ Xf rel[2];
+  __shared__ int red[8];
+  const int2 ab = cand[blockIdx.x];
+  if (threadIdx.x < 2) {
+    const int s = threadIdx.x == 0 ? ab.x : ab.y;
+    const int t = threadIdx.x == 0 ? ab.y : ab.x;
+    rel[threadIdx.x] = xf_relative_exact(poses[s], poses[t], rd);
+  }
+  __syncthreads();
+  bool ok = true;
+  for (int dir = 0; dir < 2 && ok; ++dir) {
+    const FrameDev Fa = frames[dir == 0 ? ab.x : ab.y];
+    const FrameDev Fb = frames[dir == 0 ? ab.y : ab.x];
+    const int hw = Fa.w * Fa.h;
+    const int ord = Fa.n_valid_depth == 1 ? rd.apply_1 : rd.apply_n;
+    if (full_count) {
+      int c = 0;
+      for (int p = threadIdx.x; p < hw; p += blockDim.x) {
+        const float4 P = __ldg(&Fa.P[p]);
+        if ((__float_as_uint(P.w) & SFB_FLAG_VD) && point_inside(rel[dir], Fb, P, ord)) ++c;
+      }
+      for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int t = 0;
+        for (int w = 0; w < 8; ++w) t += red[w];
+        counts[2 * blockIdx.x + dir] = t;
+      }
+      __syncthreads();
+      continue;
+    }
+    bool found = false;
+    for (int base = 0; base < hw; base += blockDim.x) {
+      const int p = base + threadIdx.x;
+      bool in = false;
+      if (p < hw) {
+        const float4 P = __ldg(&Fa.P[p]);
+        in = (__float_as_uint(P.w) & SFB_FLAG_VD) && point_inside(rel[dir], Fb, P, ord);
+      }
+      if (__syncthreads_or(in)) {
+        found = true;
+        break;
+      }
+    }
+    ok = found;
+  }
+  if (!full_count && threadIdx.x == 0) pass[blockIdx.x] = ok ? 1 : 0;
+}
+
+void launch_overlap(const FrameDev* frames, const PoseDev* poses, const int2* cand, int n_cand,
+                    Rounding rd, int full_count, uint8_t* pass, int* counts, cudaStream_t s) {
+  if (n_cand <= 0) return;
+  sfb_count_launch();
+  k_overlap<<<n_cand, 256, 0, s>>>(frames, poses, cand, rd, full_count, pass, counts);
+}

@@ -1,0 +1,304 @@
+// Frame packing, sparse correspondence term, pose update.
+//
+//  k_pack           CachedFrame planes (frames.py:38-50) -> P/N/G/T device layout
+//  k_sparse         _sparse_state + sparse gradient/diagonal/J^T J blocks
+//                   (solver.py:568-580, 389-428, 644-646) and eval_sparse (:114-123)
+//  k_pose_update    _apply_step + exp_twist_vector (solver.py:674-677,
+//                   geometry.py:40-48,78-90,183-186)
+#include "sfb_kernels.cuh"
+
+// ---------------------------------------------------------------------------
+__global__ void k_pack(PackArgs a) {
+  const int hw = a.w * a.h;
+  int cnt_vd = 0, cnt_geo = 0;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < hw; p += gridDim.x * blockDim.x) {
+    const unsigned vd = a.vd[p] ? 1u : 0u;
+    const unsigned vn = a.vn[p] ? 1u : 0u;
+    const unsigned flags = vd * SFB_FLAG_VD | vn * SFB_FLAG_VN;
+    a.P[p] = make_float4(a.pts[3 * p], a.pts[3 * p + 1], a.pts[3 * p + 2], __uint_as_float(flags));
+    a.N[p] = make_float4(a.nrm[3 * p], a.nrm[3 * p + 1], a.nrm[3 * p + 2], 0.f);
+    const float2 g = make_float2(a.grad[2 * p], a.grad[2 * p + 1]);
+    a.G[p] = g;
+    const int y = p / a.w, x = p - y * a.w;
+    float4 t0 = make_float4(0.f, 0.f, 0.f, 0.f), t1 = t0;
+    if (x + 1 < a.w && y + 1 < a.h) {
+      const int q = p + 1, r = p + a.w, s = p + a.w + 1;
+      t0 = make_float4(g.x, g.y, a.grad[2 * q], a.grad[2 * q + 1]);
+      t1 = make_float4(a.grad[2 * r], a.grad[2 * r + 1], a.grad[2 * s], a.grad[2 * s + 1]);
+    }
+    a.T[2 * p] = t0;
+    a.T[2 * p + 1] = t1;
+    cnt_vd += (int)vd;
+    cnt_geo += (int)(vd & vn);
+  }
+  // integer counts: atomics are exact and order-independent
+  for (int o = 16; o > 0; o >>= 1) {
+    cnt_vd += __shfl_xor_sync(0xffffffffu, cnt_vd, o);
+    cnt_geo += __shfl_xor_sync(0xffffffffu, cnt_geo, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&a.counts[0], cnt_vd);
+    atomicAdd(&a.counts[1], cnt_geo);
+  }
+}
+
+void launch_pack(const PackArgs& a, cudaStream_t s) {
+  const int hw = a.w * a.h;
+  int blocks = (hw + 255) / 256;
+  if (blocks > 1184) blocks = 1184;
+  sfb_count_launch();
+  k_pack<<<blocks, 256, 0, s>>>(a);
+}
+
+// ---------------------------------------------------------------------------
+// One warp per correspondence set.  Per set we accumulate the moments that
+// define the three 6x6 blocks of w_s * J^T J (H_ii, H_jj, H_ij), the two
+// gradient 6-vectors and the energy.  With S = -[y]x,
+//   H_ii = [[|y_i|^2 I - y_i y_i^T, [y_i]x], [-[y_i]x, I]]  summed over corr,
+//   H_ij = [[y_j y_i^T - (y_i.y_j) I, -[y_i]x], [[y_j]x, -I]],
+//   g_i  = [y_i x r ; r],  g_j = -[y_j x r ; r]
+// which is exactly the matrix-free product of solver.py:375-401 regrouped.
+__global__ void __launch_bounds__(256) k_sparse(SparseArgs a) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= a.n_sets) return;
+  const int fi = a.set_fi[warp], fj = a.set_fj[warp];
+  const int64_t c0 = a.set_off[warp], c1 = a.set_off[warp + 1];
+  const PoseDev& Pi = a.poses[fi];
+  const PoseDev& Pj = a.poses[fj];
+  double Ri[9], ti[3], Rj[9], tj[3];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) { Ri[k] = Pi.R[k]; Rj[k] = Pj.R[k]; }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) { ti[k] = Pi.t[k]; tj[k] = Pj.t[k]; }
+
+  // moments
+  double Ai[6] = {0, 0, 0, 0, 0, 0};   // |y_i|^2 I - y_i y_i^T, packed (00,01,02,11,12,22)
+  double Aj[6] = {0, 0, 0, 0, 0, 0};
+  double M[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};  // y_j y_i^T - (y_i.y_j) I
+  double Si[3] = {0, 0, 0}, Sj[3] = {0, 0, 0};
+  double gi[3] = {0, 0, 0}, gj[3] = {0, 0, 0}, sr[3] = {0, 0, 0};
+  double E = 0.0, cnt = 0.0;
+  for (int64_t c = c0 + lane; c < c1; c += 32) {
+    double yi[3], yj[3];
+    xf_apply(Ri, ti, a.pts_i[3 * c], a.pts_i[3 * c + 1], a.pts_i[3 * c + 2], yi);
+    xf_apply(Rj, tj, a.pts_j[3 * c], a.pts_j[3 * c + 1], a.pts_j[3 * c + 2], yj);
+    const double r0 = yi[0] - yj[0], r1 = yi[1] - yj[1], r2 = yi[2] - yj[2];
+    E += r0 * r0 + r1 * r1 + r2 * r2;
+    if (a.world_i) {
+      a.world_i[3 * c] = yi[0]; a.world_i[3 * c + 1] = yi[1]; a.world_i[3 * c + 2] = yi[2];
+      a.world_j[3 * c] = yj[0]; a.world_j[3 * c + 1] = yj[1]; a.world_j[3 * c + 2] = yj[2];
+    }
+    if (a.energy_only) continue;
+    cnt += 1.0;
+    Ai[0] += yi[1] * yi[1] + yi[2] * yi[2];
+    Ai[1] -= yi[0] * yi[1];
+    Ai[2] -= yi[0] * yi[2];
+    Ai[3] += yi[0] * yi[0] + yi[2] * yi[2];
+    Ai[4] -= yi[1] * yi[2];
+    Ai[5] += yi[0] * yi[0] + yi[1] * yi[1];
+    Aj[0] += yj[1] * yj[1] + yj[2] * yj[2];
+    Aj[1] -= yj[0] * yj[1];
+    Aj[2] -= yj[0] * yj[2];
+    Aj[3] += yj[0] * yj[0] + yj[2] * yj[2];
+    Aj[4] -= yj[1] * yj[2];
+    Aj[5] += yj[0] * yj[0] + yj[1] * yj[1];
+    M[0] -= yj[1] * yi[1] + yj[2] * yi[2];
+    M[1] += yj[0] * yi[1];
+    M[2] += yj[0] * yi[2];
+    M[3] += yj[1] * yi[0];
+    M[4] -= yj[0] * yi[0] + yj[2] * yi[2];
+    M[5] += yj[1] * yi[2];
+    M[6] += yj[2] * yi[0];
+    M[7] += yj[2] * yi[1];
+    M[8] -= yj[0] * yi[0] + yj[1] * yi[1];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) { Si[k] += yi[k]; Sj[k] += yj[k]; }
+    gi[0] += yi[1] * r2 - yi[2] * r1;
+    gi[1] += yi[2] * r0 - yi[0] * r2;
+    gi[2] += yi[0] * r1 - yi[1] * r0;
+    gj[0] += yj[1] * r2 - yj[2] * r1;
+    gj[1] += yj[2] * r0 - yj[0] * r2;
+    gj[2] += yj[0] * r1 - yj[1] * r0;
+    sr[0] += r0; sr[1] += r1; sr[2] += r2;
+  }
+  E = warp_sum(E);
+  double* out = a.set_out + (int64_t)warp * SFB_SET_STRIDE;
+  if (a.energy_only) {
+    if (lane == 0) out[SFB_SET_E] = E;
+    return;
+  }
+#pragma unroll
+  for (int k = 0; k < 6; ++k) { Ai[k] = warp_sum(Ai[k]); Aj[k] = warp_sum(Aj[k]); }
+#pragma unroll
+  for (int k = 0; k < 9; ++k) M[k] = warp_sum(M[k]);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    Si[k] = warp_sum(Si[k]); Sj[k] = warp_sum(Sj[k]);
+    gi[k] = warp_sum(gi[k]); gj[k] = warp_sum(gj[k]); sr[k] = warp_sum(sr[k]);
+  }
+  cnt = warp_sum(cnt);
+  if (lane != 0) return;
+  // solver.py:406,414: the J^T J blocks only exist for w_sparse > 0, while the
+  // gradient always carries w_sparse (solver.py:644-645).
+  const double wg = a.w_sparse;
+  const double w = a.w_sparse > 0.0 ? a.w_sparse : 0.0;
+  // blocks, row-major 6x6
+  double* Hii = out;
+  double* Hjj = out + 36;
+  double* Hij = out + 72;
+  const int ai[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) {
+      Hii[r * 6 + c] = w * Ai[ai[r][c]];
+      Hjj[r * 6 + c] = w * Aj[ai[r][c]];
+      Hij[r * 6 + c] = w * M[r * 3 + c];
+      const double eye = (r == c) ? 1.0 : 0.0;
+      Hii[(r + 3) * 6 + (c + 3)] = w * cnt * eye;
+      Hjj[(r + 3) * 6 + (c + 3)] = w * cnt * eye;
+      Hij[(r + 3) * 6 + (c + 3)] = -w * cnt * eye;
+    }
+  // [s]x = [[0,-s2,s1],[s2,0,-s0],[-s1,s0,0]]
+  const double Ki[9] = {0, -Si[2], Si[1], Si[2], 0, -Si[0], -Si[1], Si[0], 0};
+  const double Kj[9] = {0, -Sj[2], Sj[1], Sj[2], 0, -Sj[0], -Sj[1], Sj[0], 0};
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) {
+      Hii[r * 6 + c + 3] = w * Ki[r * 3 + c];
+      Hii[(r + 3) * 6 + c] = -w * Ki[r * 3 + c];
+      Hjj[r * 6 + c + 3] = w * Kj[r * 3 + c];
+      Hjj[(r + 3) * 6 + c] = -w * Kj[r * 3 + c];
+      Hij[r * 6 + c + 3] = -w * Ki[r * 3 + c];
+      Hij[(r + 3) * 6 + c] = w * Kj[r * 3 + c];
+    }
+  for (int k = 0; k < 3; ++k) {
+    out[SFB_SET_GI + k] = wg * gi[k];
+    out[SFB_SET_GI + 3 + k] = wg * sr[k];
+    out[SFB_SET_GJ + k] = -wg * gj[k];
+    out[SFB_SET_GJ + 3 + k] = -wg * sr[k];
+  }
+  out[SFB_SET_E] = E;
+}
+
+void launch_sparse(const SparseArgs& a, cudaStream_t s) {
+  if (a.n_sets <= 0) return;
+  const int blocks = (a.n_sets * 32 + 255) / 256;
+  sfb_count_launch();
+  k_sparse<<<blocks, 256, 0, s>>>(a);
+}
+
+// eval_sparse residuals (solver.py:114-123) and per-set max |r| for
+// max_residual_set (solver.py:765-776).
+__global__ void k_sparse_residuals(SparseArgs a, double* res, double* set_max) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= a.n_sets) return;
+  const PoseDev& Pi = a.poses[a.set_fi[warp]];
+  const PoseDev& Pj = a.poses[a.set_fj[warp]];
+  double mx = 0.0;
+  for (int64_t c = a.set_off[warp] + lane; c < a.set_off[warp + 1]; c += 32) {
+    double yi[3], yj[3];
+    xf_apply(Pi.R, Pi.t, a.pts_i[3 * c], a.pts_i[3 * c + 1], a.pts_i[3 * c + 2], yi);
+    xf_apply(Pj.R, Pj.t, a.pts_j[3 * c], a.pts_j[3 * c + 1], a.pts_j[3 * c + 2], yj);
+    const double r0 = yi[0] - yj[0], r1 = yi[1] - yj[1], r2 = yi[2] - yj[2];
+    if (res) { res[3 * c] = r0; res[3 * c + 1] = r1; res[3 * c + 2] = r2; }
+    mx = fmax(mx, sqrt(r0 * r0 + r1 * r1 + r2 * r2));
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0 && set_max) set_max[warp] = mx;
+}
+
+void launch_sparse_residuals(const SparseArgs& a, double* res, double* set_max, cudaStream_t s) {
+  if (a.n_sets <= 0) return;
+  sfb_count_launch();
+  k_sparse_residuals<<<(a.n_sets * 32 + 255) / 256, 256, 0, s>>>(a, res, set_max);
+}
+
+// ---------------------------------------------------------------------------
+// T_f <- exp(dx_f) o T_f for every non-anchor frame (thread per frame), plus a
+// deterministic |dx| in block 0.
+__device__ void so3_exp_dev(const double w[3], double E[9]) {
+  const double a = sqrt(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]);
+  double K[9] = {0, -w[2], w[1], w[2], 0, -w[0], -w[1], w[0], 0};
+  double KK[9];
+  double s1, s2;
+  if (a < 1e-8) {  // geometry.py:44-46
+    s1 = 1.0;
+    s2 = 0.5;
+  } else {
+    for (int k = 0; k < 9; ++k) K[k] /= a;
+    s1 = sin(a);
+    s2 = 1.0 - cos(a);
+  }
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c)
+      KK[r * 3 + c] = K[r * 3 + 0] * K[0 * 3 + c] + K[r * 3 + 1] * K[1 * 3 + c] + K[r * 3 + 2] * K[2 * 3 + c];
+  for (int k = 0; k < 9; ++k) E[k] = ((k % 4) == 0 ? 1.0 : 0.0) + s1 * K[k] + s2 * KK[k];
+}
+
+__device__ void left_jacobian_dev(const double w[3], double V[9]) {
+  const double a = sqrt(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]);
+  const double K[9] = {0, -w[2], w[1], w[2], 0, -w[0], -w[1], w[0], 0};
+  double KK[9];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c)
+      KK[r * 3 + c] = K[r * 3 + 0] * K[0 * 3 + c] + K[r * 3 + 1] * K[1 * 3 + c] + K[r * 3 + 2] * K[2 * 3 + c];
+  const double a2 = a * a;
+  double c1, c2;
+  if (a < 1e-4) {  // geometry.py:85-86
+    c1 = 0.5 - a2 / 24.0;
+    c2 = 1.0 / 6.0 - a2 / 120.0;
+  } else {
+    c1 = (1.0 - cos(a)) / a2;
+    c2 = (a - sin(a)) / (a2 * a);
+  }
+  for (int k = 0; k < 9; ++k) V[k] = ((k % 4) == 0 ? 1.0 : 0.0) + c1 * K[k] + c2 * KK[k];
+}
+
+__global__ void k_pose_update(PoseDev* poses, int n_frames, const double* dx, double* step_norm,
+                              const double* skip) {
+  if (skip && *skip != 0.0) return;
+  const int f = blockIdx.x * blockDim.x + threadIdx.x + 1;
+  if (f < n_frames) {
+    const double* d = dx + 6 * (f - 1);
+    const double w[3] = {d[0], d[1], d[2]};
+    const double v[3] = {d[3], d[4], d[5]};
+    double E[9], V[9];
+    so3_exp_dev(w, E);
+    left_jacobian_dev(w, V);
+    PoseDev& P = poses[f];
+    double R[9], t[3];
+    for (int r = 0; r < 3; ++r) {
+      for (int c = 0; c < 3; ++c)
+        R[r * 3 + c] = E[r * 3 + 0] * P.R[0 * 3 + c] + E[r * 3 + 1] * P.R[1 * 3 + c] + E[r * 3 + 2] * P.R[2 * 3 + c];
+      const double te = V[r * 3 + 0] * v[0] + V[r * 3 + 1] * v[1] + V[r * 3 + 2] * v[2];
+      t[r] = E[r * 3 + 0] * P.t[0] + E[r * 3 + 1] * P.t[1] + E[r * 3 + 2] * P.t[2] + te;
+    }
+    for (int k = 0; k < 9; ++k) P.R[k] = R[k];
+    for (int k = 0; k < 3; ++k) P.t[k] = t[k];
+    P.f_layout = 0;  // matmul results are C-ordered
+  }
+  if (blockIdx.x == 0 && step_norm) {
+    // deterministic |dx|: fixed per-thread striding + fixed tree
+    __shared__ double sh[32];
+    const int nv = 6 * (n_frames - 1);
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) acc += dx[i] * dx[i];
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      double v = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+      v = warp_sum(v);
+      if (threadIdx.x == 0) *step_norm = sqrt(v);
+    }
+  }
+}
+
+void launch_pose_update(PoseDev* poses, int n_frames, const double* dx, double* step_norm,
+                        const double* skip, cudaStream_t s) {
+  const int nv = n_frames - 1;
+  int blocks = (nv + 255) / 256;
+  if (blocks < 1) blocks = 1;
+  sfb_count_launch();
+  k_pose_update<<<blocks, 256, 0, s>>>(poses, n_frames, dx, step_norm, skip);
+}

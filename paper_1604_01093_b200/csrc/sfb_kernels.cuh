@@ -1,0 +1,119 @@
+// sfb_kernels.cuh — launcher declarations shared by the kernel TUs and the ABI.
+#pragma once
+#include "sfb_internal.cuh"
+
+struct PackArgs {
+  const uint8_t* vd;
+  const uint8_t* vn;
+  const float* pts;
+  const float* nrm;
+  const float* grad;
+  float4* P;
+  float4* N;
+  float2* G;
+  float4* T;
+  int w, h;
+  int* counts;  // [0] valid_depth, [1] valid_depth & valid_normal
+};
+
+struct SparseArgs {
+  const PoseDev* poses;
+  const int* set_fi;
+  const int* set_fj;
+  const int64_t* set_off;
+  const double* pts_i;
+  const double* pts_j;
+  double* world_i;     // may be null (energy-only)
+  double* world_j;
+  double* set_out;     // SFB_SET_STRIDE per set
+  int n_sets;
+  double w_sparse;
+  int energy_only;
+};
+
+struct DenseArgs {
+  const FrameDev* frames;
+  const PoseDev* poses;
+  const int4* items;        // (dir edge, begin, end, 0)
+  const int2* dir_edges;    // (src frame, dst frame)
+  const int64_t* photo_off; // per dir edge: u32-word offset
+  const int64_t* geo_off;   // per dir edge: u16 offset
+  uint32_t* photo_mask;
+  uint16_t* geo_tgt;
+  double* item_out;         // SFB_ITEM_STRIDE per item
+  Rounding rd;
+  double s_photo, s_geo;
+  int do_photo, do_geo;
+  double geo_dmax, geo_nmin;
+  int stride;
+  int n_items;
+};
+
+struct AssembleArgs {
+  int n_blk;
+  int n_pairs;
+  const double* set_out;
+  const double* edge_out;
+  const int* d_ptr;   // per var: D/g contribution list
+  const int* d_ent;
+  const int* b_ptr;   // per pair: B contribution list
+  const int* b_ent;
+  double* D;          // n_blk * 36
+  double* B;          // n_pairs * 36
+  double* g;          // n_blk * 6
+  int dense_on;
+};
+
+struct PcgArgs {
+  int n_blk;
+  const double* D;
+  const double* B;
+  const int* row_ptr;
+  const int* row_ent;  // pair << 1 | transposed
+  const int* row_col;
+  const double* g;
+  double* x;
+  double* r;
+  double* z;
+  double* p;
+  double* Ap;
+  double* inv_diag;
+  double* b;
+  const double* jdiag; // _jacobi_diagonal (solver.py:412-428)
+  double* part;        // 4 * gridDim
+  int* flags;          // scratch
+  int max_it;
+  double tol;
+  int restart;
+  double* out_scalars; // [0] iterations, [1] relative, [2] status
+  const double* skip;  // optional: skip when *skip != 0
+};
+
+// Library-wide kernel launch counter (sfb_launch_count).
+void sfb_count_launch(int n = 1);
+
+void launch_pack(const PackArgs& a, cudaStream_t s);
+void launch_sparse(const SparseArgs& a, cudaStream_t s);
+void launch_dense_linearize(const DenseArgs& a, cudaStream_t s);
+void launch_dense_energy(const DenseArgs& a, double* item_e2, cudaStream_t s);
+void launch_edge_reduce(const int* edge_item_ptr, const double* item_out, double* edge_out,
+                        int n_dir, cudaStream_t s);
+void launch_assemble(const AssembleArgs& a, cudaStream_t s);
+void launch_sum_energies(const double* set_out, int n_sets, const double* edge_out, int n_dir,
+                         const double* item_e2, int n_items, double* out3, int mode,
+                         cudaStream_t s);
+cudaError_t launch_pcg(const PcgArgs& a, int n_sm, cudaStream_t s);
+cudaError_t launch_pcg_dense(const PcgArgs& a, const double* A, int n_sm, cudaStream_t s);
+void launch_matvec(const PcgArgs& a, const double* xin, double* yout, cudaStream_t s);
+void launch_pose_update(PoseDev* poses, int n_frames, const double* dx, double* step_norm,
+                        const double* skip, cudaStream_t s);
+void launch_angle_gate(const PoseDev* poses, int n, Rounding rd, double cos_min, uint8_t* flags,
+                       cudaStream_t s);
+void launch_overlap(const FrameDev* frames, const PoseDev* poses, const int2* cand, int n_cand,
+                    Rounding rd, int full_count, uint8_t* pass, int* counts, cudaStream_t s);
+void launch_associate(const DenseArgs& a, int src, int dst, int kind, uint8_t* sel, int* tgt,
+                      cudaStream_t s);
+void launch_point_eval(const FrameDev* frames, const PoseDev* poses, int src, int dst, int kind,
+                       int64_t m, const double* pts, const double* aux, const double* tgts,
+                       double* res, double* jac, cudaStream_t s);
+void launch_sparse_residuals(const SparseArgs& a, double* res, double* set_max, cudaStream_t s);

@@ -1,0 +1,118 @@
+"""Device runtime: one libsfb context per CUDA device plus its frame store.
+
+A `CachedFrame` is immutable after construction (reference frames.py:8-9),
+so its planes are uploaded once per context and addressed by slot.  The
+store keys frames by object identity and holds a strong reference so an id
+cannot be recycled while its slot is alive; `clear_frames()` drops them.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+from . import _abi
+from ._rounding import probe
+
+
+def _default_device() -> int:
+    for key in ("SFB_DEVICE", "LOCAL_RANK"):
+        if key in os.environ:
+            return int(os.environ[key])
+    return 0
+
+
+def _plane(a, dtype, shape) -> np.ndarray:
+    arr = np.ascontiguousarray(np.asarray(a), dtype=dtype)
+    if arr.shape != shape:
+        raise ValueError(f"cache plane has shape {arr.shape}, expected {shape}")
+    return arr
+
+
+class Runtime:
+    def __init__(self, device: int):
+        self.lib = _abi.load()
+        self.device = device
+        h = C.c_void_p()
+        _abi.check(self.lib.sfb_ctx_create(device, C.byref(h)))
+        self.handle = h
+        r = _abi.Rounding(**probe())
+        _abi.check(self.lib.sfb_ctx_set_rounding(h, C.byref(r)), h)
+        self._frames: dict[int, tuple[int, object]] = {}
+        self._lock = threading.Lock()
+
+    # -- frame store --------------------------------------------------------
+    def slots_for(self, caches) -> list[int]:
+        """Slots of the given caches, uploading the ones not yet resident."""
+        with self._lock:
+            missing = []
+            seen = set()
+            for c in caches:
+                if id(c) not in self._frames and id(c) not in seen:
+                    missing.append(c)
+                    seen.add(id(c))
+            if missing:
+                self._upload(missing)
+            return [self._frames[id(c)][0] for c in caches]
+
+    def _upload(self, caches) -> None:
+        n = len(caches)
+        descs = (_abi.FrameDesc * n)()
+        keep = []
+        for k, c in enumerate(caches):
+            vd = np.asarray(c.valid_depth)
+            h, w = vd.shape
+            planes = (
+                _plane(vd, np.bool_, (h, w)).view(np.uint8),
+                _plane(c.valid_normal, np.bool_, (h, w)).view(np.uint8),
+                _plane(c.points_low, np.float32, (h, w, 3)),
+                _plane(c.normals_low, np.float32, (h, w, 3)),
+                _plane(c.grad_low, np.float32, (h, w, 2)),
+            )
+            keep.append(planes)
+            k_low = c.intrinsics_low
+            if int(k_low.width) != w or int(k_low.height) != h:
+                raise ValueError("intrinsics_low size does not match the cache planes")
+            d = descs[k]
+            d.width, d.height = w, h
+            d.fx, d.fy, d.cx, d.cy = (float(k_low.fx), float(k_low.fy), float(k_low.cx),
+                                      float(k_low.cy))
+            d.valid_depth, d.valid_normal, d.points, d.normals, d.grad = (
+                p.ctypes.data for p in planes)
+        slots = np.zeros(n, dtype=np.int32)
+        _abi.check(self.lib.sfb_frames_upload(self.handle, n, descs, _abi.ptr(slots)), self.handle)
+        for c, s in zip(caches, slots):
+            self._frames[id(c)] = (int(s), c)
+        del keep
+
+    def clear_frames(self) -> None:
+        with self._lock:
+            if not self._frames:
+                return
+            slots = np.array([s for s, _ in self._frames.values()], dtype=np.int32)
+            _abi.check(self.lib.sfb_frames_release(self.handle, len(slots), _abi.ptr(slots)),
+                       self.handle)
+            self._frames.clear()
+
+    def __del__(self):
+        try:
+            self.lib.sfb_ctx_destroy(self.handle)
+        except Exception:
+            pass
+
+
+_runtimes: dict[int, Runtime] = {}
+_rt_lock = threading.Lock()
+
+
+def runtime(device: int | None = None) -> Runtime:
+    dev = _default_device() if device is None else int(device)
+    with _rt_lock:
+        rt = _runtimes.get(dev)
+        if rt is None:
+            rt = Runtime(dev)
+            _runtimes[dev] = rt
+        return rt

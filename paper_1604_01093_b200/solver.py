@@ -1,0 +1,702 @@
+"""Drop-in, B200-native replacement for `scanfuse.solver` (reference solver.py).
+
+Same public names, signatures, data layouts and error behaviour as the
+reference module; every numeric step runs in libsfb.so on the GPU:
+
+* `AlignmentProblem.solve` (solver.py:681-750) keeps the reference's
+  Gauss-Newton control flow on the host (dense ramp, accept / two-strike
+  abort / best-pose restore, relative-decrease convergence) and only moves
+  scalars across PCIe per iteration; linearisation, the block system, the
+  scalar-Jacobi PCG, the Lie update and the frozen-association energy are
+  device kernels.
+* `build_dense_edges` (:130-148) is the bit-exact device pair filter.
+* `pcg_solve` (:463-508) runs the exact recurrence on the device; it stays
+  duck-typed: a foreign system exposing `.rhs/.diagonal/.apply` is
+  materialised through its own `apply` and solved by the same device PCG.
+* The per-edge evaluators (:114-349) return host arrays computed on device.
+
+There is no CPU fallback: without libsfb.so or a CUDA device every entry
+point raises.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _abi
+from .device_problem import DeviceProblem
+from .se3 import RigidTransform
+
+
+class PcgDivergenceError(RuntimeError):
+    """Non-finite values appeared inside the linear solve (solver.py:30-31)."""
+
+
+@dataclass
+class EnergyWeights:
+    sparse: float = 1.0
+    photo: float = 0.1
+    geo: float = 1.0
+    dense_ramp: tuple = (0, 5)
+
+
+def dense_ramp_weight(weights: EnergyWeights, iteration: int) -> float:
+    """Linear 0 -> 1 dense-term ramp over outer iterations (solver.py:49-53)."""
+    start, end = weights.dense_ramp
+    if end <= start:
+        return 1.0 if iteration >= end else 0.0
+    return float(np.clip((iteration - start) / (end - start), 0.0, 1.0))
+
+
+@dataclass
+class SolverConfig:
+    batch_iterations: int = 10
+    online_iterations: int = 3
+    pcg_max_iterations: int = 50
+    pcg_tolerance: float = 1e-6
+    pcg_restart_interval: int = 20
+    min_relative_decrease: float = 1e-9
+    view_angle_max_deg: float = 60.0
+    geo_distance_max: float = 0.15
+    geo_normal_min: float = 0.9
+    dense_pixel_stride: int = 1
+    dense_bidirectional: bool = False
+    prune_residual_max: float = 0.05
+
+
+# ---------------------------------------------------------------------------
+# Sparse term
+
+
+@dataclass
+class SparseTerm:
+    """Stacked correspondences with variable indices, -1 = anchor (solver.py:76-86)."""
+
+    var_i: np.ndarray
+    var_j: np.ndarray
+    points_i: np.ndarray
+    points_j: np.ndarray
+    set_index: np.ndarray
+    frames_i: np.ndarray
+    frames_j: np.ndarray
+
+
+def build_sparse_term(corr_sets, frame_to_var) -> SparseTerm:
+    """Host packing of CorrespondenceSets into SoA (solver.py:89-111)."""
+    if not corr_sets:
+        e = np.zeros(0, dtype=int)
+        return SparseTerm(e, e, np.zeros((0, 3)), np.zeros((0, 3)), e, e, e)
+    sizes = np.array([len(cs) for cs in corr_sets], dtype=int)
+    fi = np.array([cs.frame_i for cs in corr_sets])
+    fj = np.array([cs.frame_j for cs in corr_sets])
+    vi = np.array([frame_to_var[f] for f in fi], dtype=int)
+    vj = np.array([frame_to_var[f] for f in fj], dtype=int)
+    pts_i = np.vstack([np.asarray(cs.points_i, dtype=np.float64).reshape(-1, 3) for cs in corr_sets])
+    pts_j = np.vstack([np.asarray(cs.points_j, dtype=np.float64).reshape(-1, 3) for cs in corr_sets])
+    return SparseTerm(np.repeat(vi, sizes), np.repeat(vj, sizes), pts_i, pts_j,
+                      np.repeat(np.arange(len(corr_sets)), sizes), np.repeat(fi, sizes),
+                      np.repeat(fj, sizes))
+
+
+def _set_layout(corr_sets, frame_index):
+    """(n_sets,2) problem-frame indices, offsets and stacked points for the ABI."""
+    n = len(corr_sets)
+    frames = np.zeros((n, 2), dtype=np.int32)
+    off = np.zeros(n + 1, dtype=np.int64)
+    pi, pj = [], []
+    for k, cs in enumerate(corr_sets):
+        frames[k] = (frame_index[cs.frame_i], frame_index[cs.frame_j])
+        a = np.asarray(cs.points_i, dtype=np.float64).reshape(-1, 3)
+        b = np.asarray(cs.points_j, dtype=np.float64).reshape(-1, 3)
+        if a.shape != b.shape:
+            raise ValueError("points_i and points_j of a correspondence set differ in shape")
+        off[k + 1] = off[k] + a.shape[0]
+        pi.append(a)
+        pj.append(b)
+    pts_i = np.vstack(pi) if pi else np.zeros((0, 3))
+    pts_j = np.vstack(pj) if pj else np.zeros((0, 3))
+    return frames, off, pts_i, pts_j
+
+
+def _poses_from_arrays(R, t):
+    return [RigidTransform(R[k].copy(), t[k].copy()) for k in range(R.shape[0])]
+
+
+def _sparse_problem(poses: dict, corr_sets):
+    ids = list(dict.fromkeys(f for cs in corr_sets for f in (cs.frame_i, cs.frame_j)))
+    index = {f: k for k, f in enumerate(ids)}
+    frames, off, pi, pj = _set_layout(corr_sets, index)
+    dp = DeviceProblem(max(1, len(ids)), None, frames, pi, pj, off)
+    if ids:
+        dp.set_poses([poses[f] for f in ids])
+    return dp
+
+
+def eval_sparse(poses: dict, corr_sets):
+    """Residuals T_i p_i - T_j p_j (n,3) and their summed square (solver.py:114-123)."""
+    if not corr_sets:
+        return np.zeros((0, 3)), 0.0
+    dp = _sparse_problem(poses, corr_sets)
+    res = dp.sparse_residuals()
+    dp.close()
+    return res, float(np.sum(res ** 2))
+
+
+# ---------------------------------------------------------------------------
+# Dense terms
+
+
+def _pair_problem(poses, frame_i, frame_j, cache_i, cache_j):
+    dp = DeviceProblem(2, [cache_i, cache_j])
+    dp.set_poses([poses[frame_i], poses[frame_j]])
+    return dp
+
+
+def build_dense_edges(frame_ids, poses, caches, config: SolverConfig):
+    """Frame pairs admitted to the dense terms (solver.py:130-148), on device, bit-exact."""
+    ids = list(frame_ids)
+    if len(ids) < 2:
+        return []
+    dp = DeviceProblem(len(ids), [caches[f] for f in ids])
+    dp.set_poses([poses[f] for f in ids])
+    pairs = dp.build_dense_edges(config.view_angle_max_deg)
+    dp.close()
+    return [(ids[a], ids[b]) for a, b in pairs]
+
+
+def _directed_edges(edges, bidirectional):
+    directed = list(edges)
+    if bidirectional:
+        directed += [(j, i) for (i, j) in edges]
+    return directed
+
+
+@dataclass
+class PhotoAssociation:
+    frame_i: int
+    frame_j: int
+    points: np.ndarray     # (m,3) source camera-space points
+    reference: np.ndarray  # (m,2) gradient at the source pixels
+
+
+@dataclass
+class GeoAssociation:
+    frame_i: int
+    frame_j: int
+    points: np.ndarray
+    normals: np.ndarray
+    targets: np.ndarray
+
+
+def _cfg_stride(stride, config=None):
+    cfg = config if config is not None else SolverConfig()
+    return _StrideConfig(cfg, stride)
+
+
+class _StrideConfig:
+    def __init__(self, cfg, stride):
+        self.geo_distance_max = cfg.geo_distance_max
+        self.geo_normal_min = cfg.geo_normal_min
+        self.dense_pixel_stride = int(stride)
+        self.dense_bidirectional = False
+
+
+def associate_photo(poses, frame_i, frame_j, cache_i, cache_j, stride=1):
+    """Source pixels whose warp lands inside frame j (solver.py:216-232)."""
+    dp = _pair_problem(poses, frame_i, frame_j, cache_i, cache_j)
+    sel, _ = dp.associate(0, 1, 0, _cfg_stride(stride))
+    dp.close()
+    ys, xs = np.nonzero(sel.reshape(np.asarray(cache_i.valid_depth).shape))
+    return PhotoAssociation(frame_i, frame_j,
+                            np.asarray(cache_i.points_low)[ys, xs].astype(np.float64),
+                            np.asarray(cache_i.grad_low)[ys, xs].astype(np.float64))
+
+
+def associate_geo(poses, frame_i, frame_j, cache_i, cache_j, config: SolverConfig, stride=1):
+    """Projective association with distance/normal gates (solver.py:235-260)."""
+    dp = _pair_problem(poses, frame_i, frame_j, cache_i, cache_j)
+    sel, tgt = dp.associate(0, 1, 1, _cfg_stride(stride, config))
+    dp.close()
+    shape = np.asarray(cache_i.valid_depth).shape
+    ys, xs = np.nonzero(sel.reshape(shape))
+    t = tgt.reshape(shape)[ys, xs]
+    wj = np.asarray(cache_j.valid_depth).shape[1]
+    ty, tx = t // wj, t % wj
+    return GeoAssociation(frame_i, frame_j,
+                          np.asarray(cache_i.points_low)[ys, xs].astype(np.float64),
+                          np.asarray(cache_i.normals_low)[ys, xs].astype(np.float64),
+                          np.asarray(cache_j.points_low)[ty, tx].astype(np.float64))
+
+
+def photo_residuals(poses, assoc: PhotoAssociation, cache_j):
+    """ref - I_j(pi(T_j^-1 T_i d)) on a frozen association (solver.py:263-274)."""
+    if assoc.points.shape[0] == 0:
+        return np.zeros((0, 2))
+    dp = _pair_problem(poses, assoc.frame_i, assoc.frame_j, cache_j, cache_j)
+    res, _ = dp.point_eval(0, 1, 0, assoc.points, assoc.reference, jacobian=False)
+    dp.close()
+    return res
+
+
+def _nocache_pair(poses, frame_i, frame_j):
+    dp = DeviceProblem(2, None)
+    dp.set_poses([poses[frame_i], poses[frame_j]])
+    return dp
+
+
+def geo_residuals(poses, assoc: GeoAssociation):
+    """n . (d - T_i^-1 T_j target) on a frozen association (solver.py:277-283)."""
+    if assoc.points.shape[0] == 0:
+        return np.zeros(0)
+    dp = _nocache_pair(poses, assoc.frame_i, assoc.frame_j)
+    res, _ = dp.point_eval(0, 1, 1, assoc.points, assoc.normals, assoc.targets, jacobian=False)
+    dp.close()
+    return res
+
+
+def photo_linearize(poses, assoc: PhotoAssociation, cache_j):
+    """Residuals and analytic J_i, J_j = -J_i of a photo edge (solver.py:286-310)."""
+    m = assoc.points.shape[0]
+    if m == 0:
+        return np.zeros((0, 2)), np.zeros((0, 2, 6)), np.zeros((0, 2, 6))
+    dp = _pair_problem(poses, assoc.frame_i, assoc.frame_j, cache_j, cache_j)
+    res, J = dp.point_eval(0, 1, 0, assoc.points, assoc.reference)
+    dp.close()
+    return res, J, -J
+
+
+def geo_linearize(poses, assoc: GeoAssociation):
+    """Residuals and analytic J_i, J_j = -J_i of a geo edge (solver.py:313-328)."""
+    m = assoc.points.shape[0]
+    if m == 0:
+        return np.zeros(0), np.zeros((0, 6)), np.zeros((0, 6))
+    dp = _nocache_pair(poses, assoc.frame_i, assoc.frame_j)
+    res, J = dp.point_eval(0, 1, 1, assoc.points, assoc.normals, assoc.targets)
+    dp.close()
+    return res, J, -J
+
+
+def eval_photo(poses, edges, caches, stride=1):
+    """Photo residuals over directed edges, fresh association (solver.py:331-338)."""
+    residuals = [photo_residuals(poses, associate_photo(poses, i, j, caches[i], caches[j], stride),
+                                 caches[j]) for (i, j) in edges]
+    res = np.vstack(residuals) if residuals else np.zeros((0, 2))
+    return res, float(np.sum(res ** 2))
+
+
+def eval_geo(poses, edges, caches, config: SolverConfig = None, stride=1):
+    """Geo residuals over directed edges, fresh association (solver.py:341-349)."""
+    config = config or SolverConfig()
+    residuals = [geo_residuals(poses, associate_geo(poses, i, j, caches[i], caches[j], config,
+                                                    stride)) for (i, j) in edges]
+    res = np.concatenate(residuals) if residuals else np.zeros(0)
+    return res, float(np.sum(res ** 2))
+
+
+# ---------------------------------------------------------------------------
+# Normal equations
+
+
+class NormalEquations:
+    """Device-resident Gauss-Newton system (solver.py:356-454).
+
+    Holds the 6x6 block system assembled on the GPU by `normal_equations`.
+    Host accessors download on demand; `apply` runs the device block matvec.
+    The object is a view of its problem's current linearisation: re-linearising
+    the problem invalidates it.
+    """
+
+    def __init__(self, device_problem: DeviceProblem, n_vars: int, w_sparse: float,
+                 var_i: np.ndarray, var_j: np.ndarray):
+        self._dp = device_problem
+        self._version = device_problem.version
+        self.n_vars = n_vars
+        self.w_sparse = w_sparse
+        self.var_i = var_i
+        self.var_j = var_j
+        self._cache = {}
+
+    def _live(self) -> DeviceProblem:
+        if self._dp.version != self._version or self._dp.handle is None:
+            raise RuntimeError("NormalEquations is stale: its problem was re-linearised")
+        return self._dp
+
+    def _get(self, key, fn):
+        if key not in self._cache:
+            self._cache[key] = fn()
+        return self._cache[key]
+
+    @property
+    def gradient(self) -> np.ndarray:
+        return self._get("g", lambda: self._live().gradient())
+
+    @property
+    def rhs(self) -> np.ndarray:
+        return -self.gradient
+
+    @property
+    def diagonal(self) -> np.ndarray:
+        return self._get("d", lambda: self._live().diagonal())
+
+    @property
+    def world_i(self):
+        return self._get("w", lambda: self._live().sparse_world())[0]
+
+    @property
+    def world_j(self):
+        return self._get("w", lambda: self._live().sparse_world())[1]
+
+    def apply(self, x):
+        """(J^T J) x on the device (solver.py:403-410)."""
+        x = np.asarray(x, dtype=np.float64)
+        if self.n_vars == 0:
+            return np.zeros(0)
+        return self._live().matvec(x)
+
+    def materialize_sparse_jacobian(self):
+        """Explicit (3n, N) sparse-term Jacobian (solver.py:430-444), small problems only."""
+        wi, wj = self.world_i, self.world_j
+        n = wi.shape[0]
+        J = np.zeros((3 * n, self.n_vars))
+        for k in range(n):
+            r = slice(3 * k, 3 * k + 3)
+            for var, y, sgn in ((self.var_i[k], wi[k], 1.0), (self.var_j[k], wj[k], -1.0)):
+                if var >= 0:
+                    c = 6 * var
+                    J[r, c:c + 3] += -sgn * np.array([[0.0, -y[2], y[1]], [y[2], 0.0, -y[0]],
+                                                      [-y[1], y[0], 0.0]])
+                    J[r, c + 3:c + 6] += sgn * np.eye(3)
+        return J
+
+    def materialize(self):
+        """Full matrix from the device blocks (small problems only)."""
+        D, B, pv = self._get("b", lambda: self._live().blocks())
+        A = np.zeros((self.n_vars, self.n_vars))
+        for v in range(D.shape[0]):
+            A[6 * v:6 * v + 6, 6 * v:6 * v + 6] = D[v]
+        for q, (a, b) in enumerate(pv):
+            A[6 * a:6 * a + 6, 6 * b:6 * b + 6] += B[q]
+            A[6 * b:6 * b + 6, 6 * a:6 * a + 6] += B[q].T
+        return A
+
+    @property
+    def dense_jtj(self):
+        """Dense-term part of the system (the reference's precomputed matrix)."""
+        A = self.materialize()
+        if self.world_i.shape[0] and self.w_sparse > 0.0:
+            J = self.materialize_sparse_jacobian()
+            A = A - self.w_sparse * (J.T @ J)
+        return A
+
+
+@dataclass
+class PcgResult:
+    iterations: int
+    relative_residual: float
+
+
+def pcg_solve(equations, max_iterations: int = 50, tolerance: float = 1e-6,
+              restart_interval: int = 20):
+    """Scalar-Jacobi PCG with the reference's exact recurrence (solver.py:463-508)."""
+    if isinstance(equations, NormalEquations):
+        dp = equations._live()
+        if equations.n_vars == 0:
+            return np.zeros(0), PcgResult(0, 0.0)
+        it, rel, st = dp.pcg(max_iterations, tolerance, restart_interval)
+        if st == _abi.SFB_E_PCG_NONFINITE:
+            raise PcgDivergenceError("non-finite values in PCG")
+        x = np.zeros(equations.n_vars)
+        _abi.check(dp.lib.sfb_get_solution(dp.handle, _abi.ptr(x)), dp.handle)
+        return x, PcgResult(it, rel)
+    return _pcg_foreign(equations, max_iterations, tolerance, restart_interval)
+
+
+def _pcg_foreign(equations, max_iterations, tolerance, restart_interval):
+    """Duck-typed system (.rhs/.diagonal/.apply): materialise A through the
+    caller's own `apply` and run the same device recurrence on it."""
+    from .runtime import runtime
+    b = np.ascontiguousarray(equations.rhs, dtype=np.float64).reshape(-1)
+    n = b.shape[0]
+    if n == 0:
+        return np.zeros(0), PcgResult(0, 0.0)
+    cols = [np.asarray(equations.apply(e), dtype=np.float64).reshape(n) for e in np.eye(n)]
+    A = np.ascontiguousarray(np.stack(cols, axis=1))
+    diag = np.ascontiguousarray(equations.diagonal, dtype=np.float64).reshape(n)
+    rt = runtime()
+    x = np.zeros(n)
+    import ctypes as C
+    it, st = C.c_int32(), C.c_int32()
+    rel = C.c_double()
+    _abi.check(rt.lib.sfb_pcg_dense(rt.handle, n, _abi.ptr(A), _abi.ptr(b), _abi.ptr(diag),
+                                    int(max_iterations), C.c_double(tolerance),
+                                    int(restart_interval), _abi.ptr(x), C.byref(it), C.byref(rel),
+                                    C.byref(st)), rt.handle)
+    if st.value == _abi.SFB_E_PCG_NONFINITE:
+        raise PcgDivergenceError("non-finite values in PCG")
+    return x, PcgResult(it.value, rel.value)
+
+
+# ---------------------------------------------------------------------------
+# Gauss-Newton driver
+
+
+@dataclass
+class IterationRecord:
+    iteration: int
+    energy_before: float
+    energy_after: float
+    dense_weight: float
+    pcg_iterations: int
+    pcg_residual: float
+    step_norm: float
+    accepted: bool
+
+
+@dataclass
+class GaussNewtonStats:
+    iterations: list = field(default_factory=list)
+    converged: bool = False
+    aborted: bool = False
+
+    @property
+    def final_energy(self):
+        return self.iterations[-1].energy_after if self.iterations else 0.0
+
+    def energies_non_increasing(self) -> bool:
+        return all(rec.energy_after <= rec.energy_before * (1 + 1e-12) + 1e-15
+                   for rec in self.iterations if rec.accepted)
+
+
+class _LazyAssociations(list):
+    """Frozen associations of the last linearisation, materialised on first access."""
+
+    def __init__(self, builder):
+        super().__init__()
+        self._builder = builder
+        self._done = False
+
+    def _fill(self):
+        if not self._done:
+            self._done = True
+            super().extend(self._builder())
+
+    def __len__(self):
+        self._fill()
+        return super().__len__()
+
+    def __iter__(self):
+        self._fill()
+        return super().__iter__()
+
+    def __getitem__(self, i):
+        self._fill()
+        return super().__getitem__(i)
+
+    def __bool__(self):
+        return len(self) > 0
+
+
+class AlignmentProblem:
+    """One joint pose-alignment problem over a set of frames (solver.py:545-750).
+
+    The first frame anchors the gauge.  Dense terms join when `caches` are
+    given and the weights ramp them in.  Each instance owns one device
+    problem (its own CUDA stream); distinct instances may run concurrently.
+    """
+
+    def __init__(self, frame_ids, poses, corr_sets, caches=None, device=None):
+        self.frame_ids = list(frame_ids)
+        if not self.frame_ids:
+            raise ValueError("need at least one frame")
+        self.poses = {f: poses[f] for f in self.frame_ids}
+        self.corr_sets = list(corr_sets)
+        self.caches = caches
+        self.frame_to_var = {f: k - 1 for k, f in enumerate(self.frame_ids)}
+        self.n_vars = 6 * (len(self.frame_ids) - 1)
+        self.sparse = build_sparse_term(self.corr_sets, self.frame_to_var)
+        self.dense_edges = []
+        self._device = device
+        self._dp = None
+        self._dp_edges = None
+
+    # -- device plumbing ---------------------------------------------------
+    def _problem(self) -> DeviceProblem:
+        if self._dp is None:
+            index = {f: k for k, f in enumerate(self.frame_ids)}
+            frames, off, pi, pj = _set_layout(self.corr_sets, index)
+            cl = [self.caches[f] for f in self.frame_ids] if self.caches is not None else None
+            self._dp = DeviceProblem(len(self.frame_ids), cl, frames, pi, pj, off,
+                                     device=self._device)
+        return self._dp
+
+    def _push_poses(self):
+        self._problem().set_poses([self.poses[f] for f in self.frame_ids])
+
+    def _pull_poses(self):
+        R, t = self._dp.get_poses()
+        for k, f in enumerate(self.frame_ids[1:], start=1):
+            self.poses[f] = RigidTransform(R[k].copy(), t[k].copy())
+
+    def _sync_edges(self):
+        edges = list(self.dense_edges)
+        if edges != self._dp_edges:
+            index = {f: k for k, f in enumerate(self.frame_ids)}
+            self._dp.set_dense_edges([(index[i], index[j]) for (i, j) in edges])
+            self._dp_edges = edges
+
+    def close(self):
+        if self._dp is not None:
+            self._dp.close()
+            self._dp = None
+
+    # -- linearisation ------------------------------------------------------
+    def normal_equations(self, weights: EnergyWeights, w_dense: float, config: SolverConfig):
+        """(equations, energy, photo_assocs, geo_assocs) at the current poses (solver.py:630-660)."""
+        dp = self._problem()
+        self._push_poses()
+        self._sync_edges()
+        e = dp.linearize(weights, w_dense, config)
+        dense_on = self.caches is not None and w_dense > 0.0 and bool(self.dense_edges)
+        energy = weights.sparse * float(e[0])
+        if dense_on:
+            energy += w_dense * (weights.photo * float(e[1]) + weights.geo * float(e[2]))
+        eqs = NormalEquations(dp, self.n_vars, weights.sparse, self.sparse.var_i, self.sparse.var_j)
+        if dense_on:
+            directed = _directed_edges(self.dense_edges, config.dense_bidirectional)
+            poses = dict(self.poses)
+            stride = config.dense_pixel_stride
+            photo = _LazyAssociations(lambda: [
+                associate_photo(poses, i, j, self.caches[i], self.caches[j], stride)
+                for (i, j) in directed] if weights.photo > 0.0 else [])
+            geo = _LazyAssociations(lambda: [
+                associate_geo(poses, i, j, self.caches[i], self.caches[j], config, stride)
+                for (i, j) in directed] if weights.geo > 0.0 else [])
+        else:
+            photo, geo = [], []
+        return eqs, energy, photo, geo
+
+    # -- outer loop ----------------------------------------------------------
+    def solve(self, weights: EnergyWeights, config: SolverConfig,
+              max_iterations: int = None) -> GaussNewtonStats:
+        """Gauss-Newton over the device kernels with the reference's control flow."""
+        if max_iterations is None:
+            max_iterations = config.batch_iterations
+        stats = GaussNewtonStats()
+        if self.n_vars == 0:
+            stats.converged = True
+            return stats
+        dp = self._problem()
+        self._push_poses()
+        if self.caches is not None:
+            pairs = dp.build_dense_edges(config.view_angle_max_deg)
+            self.dense_edges = [(self.frame_ids[a], self.frame_ids[b]) for a, b in pairs]
+            self._dp_edges = list(self.dense_edges)
+        else:
+            self._sync_edges()
+        best_energy = np.inf
+        dp.save_best()
+        consecutive_increases = 0
+        moved = False
+        for it in range(max_iterations):
+            w_dense = dense_ramp_weight(weights, it)
+            e = dp.linearize(weights, w_dense, config)
+            dense_on = self.caches is not None and w_dense > 0.0 and bool(self.dense_edges)
+            energy_before = weights.sparse * float(e[0])
+            if dense_on:
+                energy_before += w_dense * (weights.photo * float(e[1]) + weights.geo * float(e[2]))
+            if energy_before <= 1e-18:
+                stats.converged = True
+                stats.iterations.append(IterationRecord(
+                    it, energy_before, energy_before, w_dense, 0, 0.0, 0.0, True))
+                break
+            pcg_it, pcg_rel, status = dp.pcg(config.pcg_max_iterations, config.pcg_tolerance,
+                                            config.pcg_restart_interval)
+            if status == _abi.SFB_E_PCG_NONFINITE:
+                stats.aborted = True
+                break
+            step_norm = dp.apply_step()
+            moved = True
+            ea = dp.energy_frozen(w_dense > 0.0)
+            energy_after = weights.sparse * float(ea[0])
+            if w_dense > 0.0:
+                energy_after += w_dense * (weights.photo * float(ea[1]) + weights.geo * float(ea[2]))
+            accepted = energy_after <= energy_before
+            stats.iterations.append(IterationRecord(
+                it, energy_before, energy_after, w_dense, pcg_it, pcg_rel, step_norm, accepted))
+            if accepted:
+                consecutive_increases = 0
+            else:
+                consecutive_increases += 1
+                if consecutive_increases >= 2:
+                    dp.restore_best()
+                    stats.aborted = True
+                    break
+            if energy_after < best_energy:
+                best_energy = energy_after
+                dp.save_best()
+            if accepted and (energy_before - energy_after) < config.min_relative_decrease * max(
+                    energy_before, 1e-30):
+                stats.converged = True
+                break
+        else:
+            stats.converged = True
+        if moved:
+            self._pull_poses()
+        return stats
+
+
+# ---------------------------------------------------------------------------
+# Residual-based pruning
+
+
+@dataclass
+class PruneReport:
+    removed_pairs: list
+    invalid_frames: list
+    rounds: int
+    final_max_residual: float
+
+
+def max_residual_set(poses, corr_sets):
+    """Set holding the worst correspondence residual and its value (solver.py:765-776)."""
+    worst_set, worst = -1, -1.0
+    if not corr_sets:
+        return worst_set, worst
+    dp = _sparse_problem(poses, corr_sets)
+    peaks = dp.sparse_set_max()
+    dp.close()
+    for idx, cs in enumerate(corr_sets):
+        peak = float(peaks[idx]) if len(cs) else 0.0
+        if peak > worst:
+            worst, worst_set = peak, idx
+    return worst_set, worst
+
+
+def solve_with_pruning(frame_ids, poses, corr_sets, weights, config: SolverConfig,
+                       caches=None, max_iterations=None):
+    """Alternate solving and pruning of the worst set (solver.py:779-816)."""
+    sets = list(corr_sets)
+    poses = dict(poses)
+    removed_pairs, invalid_frames, stats_list = [], [], []
+    rounds = 0
+    r_max = 0.0
+    while True:
+        rounds += 1
+        connected = {f for cs in sets for f in (cs.frame_i, cs.frame_j)}
+        active = [f for f in frame_ids if f in connected]
+        invalid_frames.extend(f for f in frame_ids if f not in connected and f not in invalid_frames)
+        if len(active) < 2 or not sets:
+            r_max = 0.0
+            break
+        problem = AlignmentProblem(active, poses, sets, caches)
+        stats_list.append(problem.solve(weights, config, max_iterations))
+        poses.update(problem.poses)
+        problem.close()
+        worst_idx, r_max = max_residual_set(poses, sets)
+        if r_max <= config.prune_residual_max:
+            break
+        offender = sets.pop(worst_idx)
+        removed_pairs.append((offender.frame_i, offender.frame_j))
+    return poses, sets, PruneReport(removed_pairs, invalid_frames, rounds, r_max), stats_list
