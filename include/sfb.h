@@ -158,6 +158,11 @@ int sfb_pcg_dense(sfb_ctx* ctx, int32_t n, const double* A, const double* rhs,
 int sfb_apply_step(sfb_problem* p, double* step_norm);
 /* _energy_with_frozen_associations (solver.py:662-672): raw sums. */
 int sfb_energy_frozen(sfb_problem* p, int32_t dense, double energies_out[3]);
+/* E_after of the previous GN iteration and the next linearisation at the
+ * same (current) poses in one fused pass (solver.py:662-672 then :630-660):
+ * out = {E_sparse, E_photo_frozen, E_geo_frozen, E_sparse, E_photo, E_geo}. */
+int sfb_energy_and_linearize(sfb_problem* p, const sfb_weights* w, int32_t prev_dense,
+                             double w_dense_next, const sfb_config* cfg, double out6[6]);
 /* One full GN iteration without intermediate host syncs:
  * linearize -> pcg -> step -> frozen energy (solver.py:700-724). */
 int sfb_gn_iteration(sfb_problem* p, const sfb_weights* w, double w_dense,

@@ -107,6 +107,7 @@ SIGNATURES = {
     "sfb_sparse_set_max": [_P, _P],
     "sfb_associate": [_P, _I32, _I32, _I32, C.POINTER(Config), _P, _P],
     "sfb_point_eval": [_P, _I32, _I32, _I32, _I64, _P, _P, _P, _P, _P],
+    "sfb_energy_and_linearize": [_P, C.POINTER(Weights), _I32, _D, C.POINTER(Config), _P],
     "sfb_profile": [_P, _I32],
     "sfb_profile_read": [_P, _P, _P, _I32],
     "sfb_launch_count": [C.POINTER(_I64)],

@@ -157,8 +157,9 @@ struct sfb_problem : Handle {
   DBuf<int4> items;
   DBuf<int> edge_item_ptr;
   DBuf<int64_t> photo_off, geo_off;
-  DBuf<uint32_t> photo_mask;
-  DBuf<uint16_t> geo_tgt;
+  DBuf<uint32_t> photo_mask[2];  // frozen associations, double-buffered so the
+  DBuf<uint16_t> geo_tgt[2];     // next linearisation can evaluate the last one
+  int cur = 0;                   // buffer holding the latest linearisation
   DBuf<double> item_out, edge_out, item_e2;
   bool dense_active = false;
   int last_do_photo = 0, last_do_geo = 0;
@@ -166,7 +167,8 @@ struct sfb_problem : Handle {
   int n_pairs = 0;
   std::vector<int2> pair_vars;
   DBuf<int> d_ptr, d_ent, b_ptr, b_ent, row_ptr, row_ent, row_col;
-  DBuf<double> D, B, g;
+  DBuf<double> D, B, g, Brow;  // Brow: row-major pre-oriented blocks for the matvec
+  DBuf<double> pv2;            // second search-direction buffer (PCG ping-pong)
   DBuf<double> x, r, z, pv, Ap, inv_diag, bvec, part, tmp, jdiag;
   DBuf<int> flags;
   bool have_system = false;
@@ -227,11 +229,10 @@ __global__ void k_jacobi_diag(const double* D, const int* d_ptr, const int* d_en
 PcgArgs pcg_args(sfb_problem* p) {
   PcgArgs a{};
   a.n_blk = p->n_blk;
-  a.D = p->D.p;
-  a.B = p->B.p;
+  a.Brow = p->Brow.p;
   a.row_ptr = p->row_ptr.p;
-  a.row_ent = p->row_ent.p;
   a.row_col = p->row_col.p;
+  a.p2 = p->pv2.p;
   a.g = p->g.p;
   a.x = p->x.p;
   a.r = p->r.p;
@@ -335,20 +336,29 @@ int rebuild_structure(sfb_problem* p, int bidir) {
     bent.insert(bent.end(), bl[q].begin(), bl[q].end());
     bptr.push_back((int)bent.size());
   }
-  // matvec rows
-  std::vector<std::vector<std::pair<int, int>>> rows(nb);  // (ent, col)
+  // matvec rows: slot 0 of row v is its diagonal block, then one pre-oriented
+  // copy of every off-diagonal block touching v (pair_slot[2q] in row a as
+  // is, pair_slot[2q+1] in row b transposed).
+  std::vector<int> rcount(nb, 1);
   for (int q = 0; q < p->n_pairs; ++q) {
-    rows[pv[q].x].push_back({q << 1, pv[q].y});
-    rows[pv[q].y].push_back({q << 1 | 1, pv[q].x});
+    ++rcount[pv[q].x];
+    ++rcount[pv[q].y];
   }
-  std::vector<int> rptr(1, 0), rent, rcol;
+  std::vector<int> rptr(nb + 1, 0);
+  for (int v = 0; v < nb; ++v) rptr[v + 1] = rptr[v] + rcount[v];
+  std::vector<int> rcol(rptr[nb]), fill(nb), pslot(2 * (size_t)std::max(1, p->n_pairs));
   for (int v = 0; v < nb; ++v) {
-    for (auto& e : rows[v]) {
-      rent.push_back(e.first);
-      rcol.push_back(e.second);
-    }
-    rptr.push_back((int)rent.size());
+    rcol[rptr[v]] = v;
+    fill[v] = rptr[v] + 1;
   }
+  for (int q = 0; q < p->n_pairs; ++q) {
+    const int a = pv[q].x, b = pv[q].y;
+    pslot[2 * q] = fill[a];
+    rcol[fill[a]++] = b;
+    pslot[2 * q + 1] = fill[b];
+    rcol[fill[b]++] = a;
+  }
+  std::vector<int>& rent = pslot;
 
   cudaStream_t s = p->stream;
   CK(p, upload_vec(p->dir_edges, dir, s));
@@ -356,8 +366,10 @@ int rebuild_structure(sfb_problem* p, int bidir) {
   CK(p, upload_vec(p->edge_item_ptr, eptr, s));
   CK(p, upload_vec(p->photo_off, poff, s));
   CK(p, upload_vec(p->geo_off, goff, s));
-  CK(p, p->photo_mask.ensure((size_t)std::max<int64_t>(pw, 1)));
-  CK(p, p->geo_tgt.ensure((size_t)std::max<int64_t>(gw, 1)));
+  for (int b = 0; b < 2; ++b) {
+    CK(p, p->photo_mask[b].ensure((size_t)std::max<int64_t>(pw, 1)));
+    CK(p, p->geo_tgt[b].ensure((size_t)std::max<int64_t>(gw, 1)));
+  }
   CK(p, p->item_out.ensure((size_t)p->n_items * SFB_ITEM_STRIDE));
   CK(p, p->edge_out.ensure((size_t)p->n_dir * SFB_ITEM_STRIDE));
   CK(p, p->item_e2.ensure((size_t)p->n_items * 2));
@@ -370,6 +382,7 @@ int rebuild_structure(sfb_problem* p, int bidir) {
   CK(p, upload_vec(p->row_col, rcol, s));
   CK(p, p->D.ensure((size_t)nb * 36));
   CK(p, p->B.ensure((size_t)std::max(1, p->n_pairs) * 36));
+  CK(p, p->Brow.ensure((size_t)std::max(1, rptr[nb]) * 36));
   CK(p, cudaStreamSynchronize(s));  // host vectors die here
   p->struct_bidir = bidir;
   p->have_system = false;
@@ -385,8 +398,8 @@ DenseArgs dense_args(sfb_problem* p) {
   a.dir_edges = p->dir_edges.p;
   a.photo_off = p->photo_off.p;
   a.geo_off = p->geo_off.p;
-  a.photo_mask = p->photo_mask.p;
-  a.geo_tgt = p->geo_tgt.p;
+  a.photo_mask = p->photo_mask[p->cur].p;
+  a.geo_tgt = p->geo_tgt[p->cur].p;
   a.item_out = p->item_out.p;
   a.rd = p->ctx->rd;
   a.n_items = p->n_items;
@@ -408,7 +421,14 @@ SparseArgs sparse_args(sfb_problem* p) {
 }
 
 // Enqueue linearize (no sync).  dense_on decided on the host.
-int enqueue_linearize(sfb_problem* p, const sfb_weights* w, double w_dense, const sfb_config* cfg) {
+int enqueue_energy_frozen(sfb_problem* p, int dense, double* dout3, int dense_only = 0);
+
+// Linearisation at the current poses.  With fuse_prev, the previous
+// linearisation's frozen dense energy is evaluated in the same pass when one
+// exists (*prev_mode = 1: sums in dscal[3..4]; 2: separate pass, dscal[17..18];
+// 0: none).
+int enqueue_linearize(sfb_problem* p, const sfb_weights* w, double w_dense, const sfb_config* cfg,
+                      int fuse_prev = 0, int* prev_mode = nullptr) {
   if (cfg->dense_pixel_stride < 1) return fail(p, SFB_E_ARG, "dense_pixel_stride must be >= 1");
   const int bidir = cfg->dense_bidirectional ? 1 : 0;
   if (p->struct_bidir != bidir) {
@@ -427,6 +447,14 @@ int enqueue_linearize(sfb_problem* p, const sfb_weights* w, double w_dense, cons
   }
   CKL(p);
   const bool dense_on = p->has_frames && w_dense > 0.0 && !p->edges.empty();
+  const bool prev_avail = fuse_prev && p->dense_active && p->n_items > 0;
+  if (prev_mode) *prev_mode = 0;
+  const bool lin = dense_on && (w->photo > 0.0 || w->geo > 0.0);
+  if (prev_avail && !lin) {
+    int rc = enqueue_energy_frozen(p, 1, p->dscal.p + 16, /*dense_only=*/1);
+    if (rc) return rc;
+    if (prev_mode) *prev_mode = 2;
+  }
   if (dense_on) {
     DenseArgs da = dense_args(p);
     da.do_photo = w->photo > 0.0;
@@ -436,12 +464,23 @@ int enqueue_linearize(sfb_problem* p, const sfb_weights* w, double w_dense, cons
     da.geo_dmax = cfg->geo_distance_max;
     da.geo_nmin = cfg->geo_normal_min;
     da.stride = cfg->dense_pixel_stride;
-    if (da.do_photo || da.do_geo) {
+    if (lin) {
+      const int nxt = 1 - p->cur;
+      da.photo_mask = p->photo_mask[nxt].p;
+      da.geo_tgt = p->geo_tgt[nxt].p;
+      if (prev_avail) {
+        da.photo_mask_prev = p->photo_mask[p->cur].p;
+        da.geo_tgt_prev = p->geo_tgt[p->cur].p;
+        da.prev_photo = p->last_do_photo;
+        da.prev_geo = p->last_do_geo;
+        if (prev_mode) *prev_mode = 1;
+      }
       {
         ProfScope ps(p->prof, 0, s);
         launch_dense_linearize(da, s);
       }
       CKL(p);
+      p->cur = nxt;
       ProfScope ps(p->prof, 5, s);
       launch_edge_reduce(p->edge_item_ptr.p, p->item_out.p, p->edge_out.p, p->n_dir, s);
       CKL(p);
@@ -464,6 +503,9 @@ int enqueue_linearize(sfb_problem* p, const sfb_weights* w, double w_dense, cons
   aa.B = p->B.p;
   aa.g = p->g.p;
   aa.dense_on = dense_on ? 1 : 0;
+  aa.row_ptr = p->row_ptr.p;
+  aa.pair_slot = p->row_ent.p;
+  aa.Brow = p->Brow.p;
   ProfScope ps(p->prof, 5, s);
   launch_assemble(aa, s);
   CKL(p);
@@ -482,12 +524,12 @@ int enqueue_linearize(sfb_problem* p, const sfb_weights* w, double w_dense, cons
   return SFB_OK;
 }
 
-int enqueue_energy_frozen(sfb_problem* p, int dense, double* dout3) {
+int enqueue_energy_frozen(sfb_problem* p, int dense, double* dout3, int dense_only) {
   cudaStream_t s = p->stream;
   SparseArgs sa = sparse_args(p);
   sa.energy_only = 1;
   sa.w_sparse = 1.0;
-  {
+  if (!dense_only) {
     ProfScope ps(p->prof, 4, s);
     launch_sparse(sa, s);
   }
@@ -572,7 +614,10 @@ int sfb_frames_upload(sfb_ctx* c, int32_t n, const sfb_frame_desc* d, int32_t* s
       return fail(c, SFB_E_ARG, "frames must be at least 2x2 (bilinear sampling)");
     if (!d[k].valid_depth || !d[k].valid_normal || !d[k].points || !d[k].normals || !d[k].grad)
       return fail(c, SFB_E_ARG, "null frame plane");
-    total += align256(hw * 16) * 2 + align256(hw * 8) + align256(hw * 32);
+    const int64_t nt = (int64_t)((d[k].width + SFB_TILE - 1) / SFB_TILE) *
+                       ((d[k].height + SFB_TILE - 1) / SFB_TILE);
+    total += align256(hw * 16) * 2 + align256(hw * 8) + align256(hw * 32) + align256(nt * 32) +
+             align256(nt * 4);
     stage += align256(hw * 2) + align256(hw * 24) + align256(hw * 8);
   }
   void* block = nullptr;
@@ -591,6 +636,11 @@ int sfb_frames_upload(sfb_ctx* c, int32_t n, const sfb_frame_desc* d, int32_t* s
     f.N = reinterpret_cast<float4*>(dst); dst += align256(hw * 16);
     f.G = reinterpret_cast<float2*>(dst); dst += align256(hw * 8);
     f.T = reinterpret_cast<float4*>(dst); dst += align256(hw * 32);
+    f.tiles_x = (w + SFB_TILE - 1) / SFB_TILE;
+    f.tiles_y = (h + SFB_TILE - 1) / SFB_TILE;
+    const size_t nt = (size_t)f.tiles_x * f.tiles_y;
+    f.tiles = reinterpret_cast<double4*>(dst); dst += align256(nt * 32);
+    f.tile_count = reinterpret_cast<int*>(dst); dst += align256(nt * 4);
     f.fx = d[k].fx; f.fy = d[k].fy; f.cx = d[k].cx; f.cy = d[k].cy;
     f.w = w; f.h = h;
     uint8_t* svd = reinterpret_cast<uint8_t*>(stg);
@@ -609,6 +659,8 @@ int sfb_frames_upload(sfb_ctx* c, int32_t n, const sfb_frame_desc* d, int32_t* s
     PackArgs pa{svd, svn, spt, snr, sgr, const_cast<float4*>(f.P), const_cast<float4*>(f.N),
                 const_cast<float2*>(f.G), const_cast<float4*>(f.T), w, h, c->counts.p + 2 * k};
     launch_pack(pa, c->stream);
+    launch_tiles(f.P, w, h, f.tiles_x, f.tiles_y, const_cast<double4*>(f.tiles),
+                 const_cast<int*>(f.tile_count), c->stream);
     CKL(c);
     devs[k] = f;
   }
@@ -714,7 +766,8 @@ int sfb_problem_create(sfb_ctx* c, int32_t n_frames, const int32_t* slots, int32
   }
   const size_t nv = (size_t)std::max(1, 6 * p->n_blk);
   if (p->g.ensure(nv) || p->x.ensure(nv) || p->r.ensure(nv) || p->z.ensure(nv) || p->pv.ensure(nv) ||
-      p->Ap.ensure(nv) || p->inv_diag.ensure(nv) || p->bvec.ensure(nv) || p->jdiag.ensure(nv) || p->tmp.ensure(2 * nv) ||
+      p->Ap.ensure(nv) || p->inv_diag.ensure(nv) || p->bvec.ensure(nv) || p->jdiag.ensure(nv) ||
+      p->pv2.ensure(nv) || p->tmp.ensure(2 * nv) ||
       p->part.ensure(4 * 1024) || p->flags.ensure(64) || p->dscal.ensure(64))
     return bail(SFB_E_OOM, "vectors");
   if (cudaMallocHost(&p->hscal, 64 * sizeof(double)) != cudaSuccess) return bail(SFB_E_OOM, "pinned");
@@ -738,6 +791,7 @@ int sfb_problem_destroy(sfb_problem* p) {
   DBuf<double>* db[] = {&p->pts_i, &p->pts_j, &p->world_i, &p->world_j, &p->set_out,
                         &p->item_out, &p->edge_out, &p->item_e2, &p->D, &p->B, &p->g, &p->x,
                         &p->r, &p->z, &p->pv, &p->Ap, &p->inv_diag, &p->bvec, &p->part, &p->tmp, &p->jdiag,
+                        &p->pv2, &p->Brow,
                         &p->dscal};
   for (auto* b : db) b->release();
   p->frames.release();
@@ -748,8 +802,10 @@ int sfb_problem_destroy(sfb_problem* p) {
   p->items.release();
   p->photo_off.release();
   p->geo_off.release();
-  p->photo_mask.release();
-  p->geo_tgt.release();
+  for (int b = 0; b < 2; ++b) {
+    p->photo_mask[b].release();
+    p->geo_tgt[b].release();
+  }
   p->prof.destroy();
   if (p->hscal) cudaFreeHost(p->hscal);
   if (p->stream) cudaStreamDestroy(p->stream);
@@ -981,7 +1037,7 @@ int sfb_pcg_dense(sfb_ctx* c, int32_t n, const double* A, const double* rhs, con
   }
   DBuf<double> dA, vec;
   CK(c, dA.ensure(hA.size()));
-  CK(c, vec.ensure((size_t)n6 * 10 + 4 * 1024 + 8));
+  CK(c, vec.ensure((size_t)n6 * 11 + 4 * 1024 + 8));
   cudaStream_t s = c->stream;
   CK(c, cudaMemcpyAsync(dA.p, hA.data(), sizeof(double) * hA.size(), cudaMemcpyHostToDevice, s));
   double* v = vec.p;
@@ -997,7 +1053,9 @@ int sfb_pcg_dense(sfb_ctx* c, int32_t n, const double* A, const double* rhs, con
   a.inv_diag = v + 7 * n6;
   a.b = v + 8 * n6;
   a.out_scalars = v + 9 * n6;
-  a.part = v + 10 * n6;
+  a.p2 = v + 10 * n6;
+  a.part = v + 11 * n6;
+  a.flags = reinterpret_cast<int*>(v + 11 * n6 + 4 * 1024);
   a.max_it = max_it;
   a.tol = tol;
   a.restart = restart;
@@ -1290,6 +1348,33 @@ int sfb_profile_read(sfb_problem* p, double* ms, int64_t* launches, int32_t rese
 int sfb_launch_count(int64_t* out) {
   if (!out) return fail(nullptr, SFB_E_ARG, "null argument");
   *out = g_launches.load();
+  return SFB_OK;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+// E_after of the previous GN iteration and the next linearisation, at the
+// same (current) poses, in one pass over the frame pairs (solver.py:662-672
+// followed by :630-660).  out = {E_sparse, E_photo_frozen, E_geo_frozen,
+// E_sparse, E_photo_new, E_geo_new} (raw sums).
+int sfb_energy_and_linearize(sfb_problem* p, const sfb_weights* w, int32_t prev_dense,
+                             double w_dense_next, const sfb_config* cfg, double out6[6]) {
+  if (!p || !w || !cfg || !out6) return fail(p, SFB_E_ARG, "null argument");
+  CK(p, cudaSetDevice(p->ctx->device));
+  int mode = 0;
+  int rc = enqueue_linearize(p, w, w_dense_next, cfg, prev_dense ? 1 : 0, &mode);
+  if (rc) return rc;
+  CK(p, cudaMemcpyAsync(p->hscal, p->dscal.p, 20 * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+  CK(p, cudaStreamSynchronize(p->stream));
+  const double* h = p->hscal;
+  out6[0] = h[0];
+  out6[1] = mode == 1 ? h[3] : (mode == 2 ? h[17] : 0.0);
+  out6[2] = mode == 1 ? h[4] : (mode == 2 ? h[18] : 0.0);
+  out6[3] = h[0];
+  out6[4] = h[1];
+  out6[5] = h[2];
   return SFB_OK;
 }
 

@@ -184,11 +184,98 @@ __device__ __forceinline__ bool stride_ok(int p, int w, int stride) {
   return (y % stride) == 0 && (x % stride) == 0;
 }
 
-__global__ void __launch_bounds__(DENSE_THREADS, 2) k_dense_linearize(DenseArgs a) {
-  __shared__ EdgeCtx ec;
+// ---------------------------------------------------------------------------
+// Fused dense pass.  For each (directed edge, pixel tile) item, at the current
+// poses, one thread per source pixel:
+//   LIN : associate_photo / associate_geo (solver.py:216-260), bit-exact, and
+//         photo_linearize / geo_linearize + _accumulate (:286-328, :615-628)
+//         into 21 packed H + 6 g + 2 energies;
+//   PREV: the frozen-association energy of the PREVIOUS linearisation
+//         (_energy_with_frozen_associations, :662-672) at these same poses -
+//         the GN loop evaluates E_after(k) and linearises iteration k+1 at the
+//         identical poses, so both share the warp, the bilinear sample and
+//         the loads.
+// Association decisions need NumPy's exact rounding; the division in the
+// projection is replaced by a correctly-rounded reciprocal and the exact
+// IEEE quotient is recomputed only when the approximate pixel lies within
+// 1e-6 px of a decision boundary (bounds, or a .5 for np.round), where the
+// two could disagree (|u_approx - u| is ~1e-13 px).
+
+struct FusedCtx {
+  Xf rel;              // pose_j^-1 o pose_i, NumPy rounding
+  double Ri[9], ti[3]; // pose_i
+  double Rj[9], tj[3]; // pose_j
+  double back[12];     // pose_i^-1 o pose_j (R row-major, t)
+};
+
+__device__ __forceinline__ void load_fused_ctx(FusedCtx* e, const PoseDev& Pi, const PoseDev& Pj,
+                                               const Rounding& rd) {
+  e->rel = xf_relative_exact(Pi, Pj, rd);
+  for (int k = 0; k < 9; ++k) { e->Ri[k] = Pi.R[k]; e->Rj[k] = Pj.R[k]; }
+  for (int k = 0; k < 3; ++k) { e->ti[k] = Pi.t[k]; e->tj[k] = Pj.t[k]; }
+  double iR[9], it[3];
+  xf_inverse_plain(Pi.R, Pi.t, iR, it);
+  for (int r = 0; r < 3; ++r) {
+    for (int c = 0; c < 3; ++c)
+      e->back[r * 3 + c] = iR[r * 3 + 0] * Pj.R[0 * 3 + c] + iR[r * 3 + 1] * Pj.R[1 * 3 + c] +
+                           iR[r * 3 + 2] * Pj.R[2 * 3 + c];
+    e->back[9 + r] = iR[r * 3 + 0] * Pj.t[0] + iR[r * 3 + 1] * Pj.t[1] + iR[r * 3 + 2] * Pj.t[2] + it[r];
+  }
+}
+
+template <bool STD>
+__device__ __forceinline__ double dot3x(double a0, double a1, double a2, double b0, double b1,
+                                        double b2, int o) {
+  if (STD) return __fma_rn(a2, b2, __fma_rn(a1, b1, __dmul_rn(a0, b0)));
+  return dot3o(a0, a1, a2, b0, b1, b2, o);
+}
+
+// round-half-even for |x| < 2^51 on the FP64 pipe
+__device__ __forceinline__ double rint_magic(double x) {
+  const double M = 6755399441055744.0;  // 1.5 * 2^52
+  return __dsub_rn(__dadd_rn(x, M), M);
+}
+
+__device__ __forceinline__ bool near_val(double x, double b) { return fabs(x - b) < 1e-6; }
+
+// |x| < 2^51: is x within 1e-6 of a half-integer (np.round tie region)?
+__device__ __forceinline__ bool near_half(double x) {
+  return fabs(fabs(x - rint_magic(x)) - 0.5) < 1e-6;
+}
+
+// bilinear_sample_with_grad on the taps plane with FP64-pipe floor.
+__device__ __forceinline__ void bilinear_fast(const FrameDev& f, double x, double y, double val[2],
+                                              double ddx[2], double ddy[2]) {
+  const double wm1 = (double)(f.w - 1), hm1 = (double)(f.h - 1);
+  x = fmin(fmax(x, 0.0), wm1);
+  y = fmin(fmax(y, 0.0), hm1);
+  double fxr = rint_magic(x), fyr = rint_magic(y);
+  fxr = fxr > x ? fxr - 1.0 : fxr;  // floor
+  fyr = fyr > y ? fyr - 1.0 : fyr;
+  fxr = fmin(fxr, (double)(f.w - 2));
+  fyr = fmin(fyr, (double)(f.h - 2));
+  const int x0 = __double2loint(__dadd_rn(fxr, 6755399441055744.0));
+  const int y0 = __double2loint(__dadd_rn(fyr, 6755399441055744.0));
+  const double ax = x - fxr, ay = y - fyr;
+  const float4 t0 = __ldg(&f.T[2 * (y0 * f.w + x0)]);
+  const float4 t1 = __ldg(&f.T[2 * (y0 * f.w + x0) + 1]);
+  const double bx = 1.0 - ax, by = 1.0 - ay;
+  const double v00[2] = {t0.x, t0.y}, v01[2] = {t0.z, t0.w};
+  const double v10[2] = {t1.x, t1.y}, v11[2] = {t1.z, t1.w};
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    val[c] = v00[c] * bx * by + v01[c] * ax * by + v10[c] * bx * ay + v11[c] * ax * ay;
+    ddx[c] = (v01[c] - v00[c]) * by + (v11[c] - v10[c]) * ay;
+    ddy[c] = (v10[c] - v00[c]) * bx + (v11[c] - v01[c]) * ax;
+  }
+}
+
+template <bool STD, bool PREV>
+__global__ void __launch_bounds__(DENSE_THREADS, 2) k_dense_fused(DenseArgs a) {
+  __shared__ FusedCtx ec;
   const int4 it = a.items[blockIdx.x];
   const int2 de = a.dir_edges[it.x];
-  if (threadIdx.x == 0) load_edge_ctx(&ec, a.poses[de.x], a.poses[de.y], a.rd);
+  if (threadIdx.x == 0) load_fused_ctx(&ec, a.poses[de.x], a.poses[de.y], a.rd);
   const FrameDev Fi = a.frames[de.x];
   const FrameDev Fj = a.frames[de.y];
   __syncthreads();
@@ -197,15 +284,20 @@ __global__ void __launch_bounds__(DENSE_THREADS, 2) k_dense_linearize(DenseArgs 
   const int lane = threadIdx.x & 31;
   uint32_t* pmask = a.photo_mask + a.photo_off[it.x];
   uint16_t* gtgt = a.geo_tgt + a.geo_off[it.x];
+  const uint32_t* pmask_prev = PREV ? a.photo_mask_prev + a.photo_off[it.x] : nullptr;
+  const uint16_t* gtgt_prev = PREV ? a.geo_tgt_prev + a.geo_off[it.x] : nullptr;
+  const double wm1 = (double)(Fj.w - 1), hm1 = (double)(Fj.h - 1);
+  const double dwj = (double)Fj.w, dhj = (double)Fj.h;
 
   double acc[29];
 #pragma unroll
   for (int k = 0; k < 29; ++k) acc[k] = 0.0;
+  double eprev_p = 0.0, eprev_g = 0.0;
 
   for (int base = it.y; base < it.z; base += DENSE_THREADS) {
     const int p = base + threadIdx.x;
     const bool live = p < it.z;
-    float4 P = make_float4(0.f, 0.f, 0.f, 0.f), N = P;
+    float4 P = make_float4(0.f, 0.f, 0.f, 0.f);
     unsigned fl = 0;
     if (live) {
       P = __ldg(&Fi.P[p]);
@@ -214,37 +306,186 @@ __global__ void __launch_bounds__(DENSE_THREADS, 2) k_dense_linearize(DenseArgs 
     const bool sok = live && stride_ok(p, Fi.w, a.stride);
     const bool ph = a.do_photo && sok && (fl & SFB_FLAG_VD);
     const bool ge = a.do_geo && sok && (fl & SFB_FLAG_VD) && (fl & SFB_FLAG_VN);
-    if (ge) N = __ldg(&Fi.N[p]);
-    const AssocOut ao = associate_pixel(ec, Fj, P, N, ph, ge, ord_ph, ord_ge, a.rd, a.geo_dmax,
-                                        a.geo_nmin);
+    bool pph = false;
+    int ptg = 0xFFFF;
+    if (PREV && live) {
+      if (a.prev_photo) pph = (pmask_prev[p >> 5] >> (p & 31)) & 1u;
+      if (a.prev_geo) ptg = gtgt_prev[p];
+    }
+    bool ph_in = false;
+    int tgt = -1;
+    double q0 = 0.0, q1 = 0.0, q2 = 1.0, rz = 1.0, ua = 0.0, va = 0.0;
+    const double d0 = P.x, d1 = P.y, d2 = P.z;
+    float4 N = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (ph || ge || pph) {
+      const int ord = ph ? ord_ph : ord_ge;
+      const bool generic = !STD || (ord != 0);
+      // warped = relative.apply(points): NumPy rounding
+      if (!generic) {
+        q0 = __dadd_rn(dot3x<true>(d0, d1, d2, ec.rel.R[0], ec.rel.R[1], ec.rel.R[2], 0), ec.rel.t[0]);
+        q1 = __dadd_rn(dot3x<true>(d0, d1, d2, ec.rel.R[3], ec.rel.R[4], ec.rel.R[5], 0), ec.rel.t[1]);
+        q2 = __dadd_rn(dot3x<true>(d0, d1, d2, ec.rel.R[6], ec.rel.R[7], ec.rel.R[8], 0), ec.rel.t[2]);
+      } else {
+        q0 = __dadd_rn(dot3o(d0, d1, d2, ec.rel.R[0], ec.rel.R[1], ec.rel.R[2], ord), ec.rel.t[0]);
+        q1 = __dadd_rn(dot3o(d0, d1, d2, ec.rel.R[3], ec.rel.R[4], ec.rel.R[5], ord), ec.rel.t[1]);
+        q2 = __dadd_rn(dot3o(d0, d1, d2, ec.rel.R[6], ec.rel.R[7], ec.rel.R[8], ord), ec.rel.t[2]);
+      }
+      const bool front = q2 > 0.0;
+      const double z = front ? q2 : 1.0;
+      rz = __drcp_rn(z);
+      const double tu = __dmul_rn(Fj.fx, q0), tv = __dmul_rn(Fj.fy, q1);
+      ua = fma(tu, rz, Fj.cx);
+      va = fma(tv, rz, Fj.cy);
+      if (ph) {
+        double u = ua, v = va;
+        if (near_val(ua, 0.0) || near_val(ua, wm1) || near_val(va, 0.0) || near_val(va, hm1)) {
+          u = __dadd_rn(__ddiv_rn(tu, z), Fj.cx);
+          v = __dadd_rn(__ddiv_rn(tv, z), Fj.cy);
+        }
+        ph_in = front && u >= 0.0 && u <= wm1 && v >= 0.0 && v <= hm1;
+      }
+      if (ge) {
+        double u = ua, v = va;
+        if (ph && ord_ge != ord_ph) {  // m == 1 special case: re-derive the warp
+          q0 = __dadd_rn(dot3o(d0, d1, d2, ec.rel.R[0], ec.rel.R[1], ec.rel.R[2], ord_ge), ec.rel.t[0]);
+          q1 = __dadd_rn(dot3o(d0, d1, d2, ec.rel.R[3], ec.rel.R[4], ec.rel.R[5], ord_ge), ec.rel.t[1]);
+          q2 = __dadd_rn(dot3o(d0, d1, d2, ec.rel.R[6], ec.rel.R[7], ec.rel.R[8], ord_ge), ec.rel.t[2]);
+        }
+        const bool fr = q2 > 0.0;
+        const double zz = fr ? q2 : 1.0;
+        if (fabs(u) < 1e9 && fabs(v) < 1e9 && (near_half(u) || near_half(v) || (ph && ord_ge != ord_ph))) {
+          u = __dadd_rn(__ddiv_rn(__dmul_rn(Fj.fx, q0), zz), Fj.cx);
+          v = __dadd_rn(__ddiv_rn(__dmul_rn(Fj.fy, q1), zz), Fj.cy);
+        }
+        if (fr && fabs(u) < 1e9 && fabs(v) < 1e9) {
+          const double xr = rint_magic(u), yr = rint_magic(v);
+          if (xr >= 0.0 && xr < dwj && yr >= 0.0 && yr < dhj) {
+            const int ti = __double2loint(__dadd_rn(yr, 6755399441055744.0)) * Fj.w +
+                           __double2loint(__dadd_rn(xr, 6755399441055744.0));
+            const float4 PT = __ldg(&Fj.P[ti]);
+            const unsigned tf = __float_as_uint(PT.w);
+            if ((tf & (SFB_FLAG_VD | SFB_FLAG_VN)) == (SFB_FLAG_VD | SFB_FLAG_VN)) {
+              N = __ldg(&Fi.N[p]);
+              const float4 NT = __ldg(&Fj.N[ti]);
+              const double x0 = __dsub_rn(q0, (double)PT.x);
+              const double x1 = __dsub_rn(q1, (double)PT.y);
+              const double x2 = __dsub_rn(q2, (double)PT.z);
+              const double dist = __dsqrt_rn(__dadd_rn(
+                  __dadd_rn(__dmul_rn(x0, x0), __dmul_rn(x1, x1)), __dmul_rn(x2, x2)));
+              const double n0 = N.x, n1 = N.y, n2 = N.z;
+              double nr0, nr1, nr2;
+              if (STD && ord_ge == 0) {
+                nr0 = dot3x<true>(n0, n1, n2, ec.rel.R[0], ec.rel.R[1], ec.rel.R[2], 0);
+                nr1 = dot3x<true>(n0, n1, n2, ec.rel.R[3], ec.rel.R[4], ec.rel.R[5], 0);
+                nr2 = dot3x<true>(n0, n1, n2, ec.rel.R[6], ec.rel.R[7], ec.rel.R[8], 0);
+              } else {
+                nr0 = dot3o(n0, n1, n2, ec.rel.R[0], ec.rel.R[1], ec.rel.R[2], ord_ge);
+                nr1 = dot3o(n0, n1, n2, ec.rel.R[3], ec.rel.R[4], ec.rel.R[5], ord_ge);
+                nr2 = dot3o(n0, n1, n2, ec.rel.R[6], ec.rel.R[7], ec.rel.R[8], ord_ge);
+              }
+              const double nd = __dadd_rn(__dadd_rn(__dmul_rn(nr0, (double)NT.x),
+                                                    __dmul_rn(nr1, (double)NT.y)),
+                                          __dmul_rn(nr2, (double)NT.z));
+              if (dist < a.geo_dmax && nd > a.geo_nmin) tgt = ti;
+            }
+          }
+        }
+      }
+    }
     if (a.do_photo) {
-      const unsigned word = __ballot_sync(0xffffffffu, ao.photo);
+      const unsigned word = __ballot_sync(0xffffffffu, ph_in);
       if (lane == 0 && base + (threadIdx.x & ~31) < it.z) pmask[(p - lane) >> 5] = word;
     }
-    if (a.do_geo && live) gtgt[p] = ao.tgt >= 0 ? (uint16_t)ao.tgt : (uint16_t)0xFFFF;
-    if (ao.photo) {
+    if (a.do_geo && live) gtgt[p] = tgt >= 0 ? (uint16_t)tgt : (uint16_t)0xFFFF;
+
+    // ---- photometric: one bilinear sample serves the frozen energy and J
+    if (ph_in || pph) {
+      double val[2], ddx[2], ddy[2];
+      bilinear_fast(Fj, ua, va, val, ddx, ddy);
       const float2 ref = __ldg(&Fi.G[p]);
-      double res[2], J[2][6];
-      photo_lin_pixel(ec, Fj, P.x, P.y, P.z, ref.x, ref.y, res, J);
-      accum_row(acc, J[0], res[0], a.s_photo);
-      accum_row(acc, J[1], res[1], a.s_photo);
-      acc[27] += res[0] * res[0] + res[1] * res[1];
+      const double r0 = (double)ref.x - val[0], r1 = (double)ref.y - val[1];
+      const double e2 = r0 * r0 + r1 * r1;
+      if (PREV && pph) eprev_p += e2;
+      if (ph_in) {
+        acc[27] += e2;
+        double wld[3];
+        xf_apply(ec.Ri, ec.ti, d0, d1, d2, wld);
+        const double a_ = Fj.fx * rz, b_ = Fj.fy * rz;
+        const double rz2 = rz * rz;
+        const double au = -Fj.fx * q0 * rz2, bv = -Fj.fy * q1 * rz2;
+        const double res[2] = {r0, r1};
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const double dq0 = ddx[c] * a_, dq1 = ddy[c] * b_, dq2 = ddx[c] * au + ddy[c] * bv;
+          double g[3];
+#pragma unroll
+          for (int k = 0; k < 3; ++k) g[k] = dq0 * ec.Rj[k * 3 + 0] + dq1 * ec.Rj[k * 3 + 1] + dq2 * ec.Rj[k * 3 + 2];
+          double J[6];
+          J[0] = g[1] * wld[2] - g[2] * wld[1];
+          J[1] = g[2] * wld[0] - g[0] * wld[2];
+          J[2] = g[0] * wld[1] - g[1] * wld[0];
+          J[3] = -g[0];
+          J[4] = -g[1];
+          J[5] = -g[2];
+          accum_row(acc, J, res[c], a.s_photo);
+        }
+      }
     }
-    if (ao.tgt >= 0) {
-      const float4 PT = __ldg(&Fj.P[ao.tgt]);
-      double res, J[6];
-      geo_lin_pixel(ec, P.x, P.y, P.z, N.x, N.y, N.z, PT.x, PT.y, PT.z, &res, J);
-      accum_row(acc, J, res, a.s_geo);
-      acc[28] += res * res;
+    // ---- point-to-plane: new association and/or frozen target
+    if (tgt >= 0 || (PREV && ptg != 0xFFFF)) {
+      if (tgt < 0) N = __ldg(&Fi.N[p]);
+      const double n0 = N.x, n1 = N.y, n2 = N.z;
+      if (PREV && ptg != 0xFFFF) {
+        const float4 PT = __ldg(&Fj.P[ptg]);
+        const double t0 = PT.x, t1 = PT.y, t2 = PT.z;
+        const double m0 = ec.back[0] * t0 + ec.back[1] * t1 + ec.back[2] * t2 + ec.back[9];
+        const double m1 = ec.back[3] * t0 + ec.back[4] * t1 + ec.back[5] * t2 + ec.back[10];
+        const double m2 = ec.back[6] * t0 + ec.back[7] * t1 + ec.back[8] * t2 + ec.back[11];
+        const double r = n0 * (d0 - m0) + n1 * (d1 - m1) + n2 * (d2 - m2);
+        eprev_g += r * r;
+      }
+      if (tgt >= 0) {
+        const float4 PT = __ldg(&Fj.P[tgt]);
+        const double t0 = PT.x, t1 = PT.y, t2 = PT.z;
+        const double m0 = ec.back[0] * t0 + ec.back[1] * t1 + ec.back[2] * t2 + ec.back[9];
+        const double m1 = ec.back[3] * t0 + ec.back[4] * t1 + ec.back[5] * t2 + ec.back[10];
+        const double m2 = ec.back[6] * t0 + ec.back[7] * t1 + ec.back[8] * t2 + ec.back[11];
+        const double r = n0 * (d0 - m0) + n1 * (d1 - m1) + n2 * (d2 - m2);
+        double wt[3];
+        xf_apply(ec.Rj, ec.tj, t0, t1, t2, wt);
+        double m[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) m[k] = ec.Ri[k * 3 + 0] * n0 + ec.Ri[k * 3 + 1] * n1 + ec.Ri[k * 3 + 2] * n2;
+        const double J[6] = {wt[1] * m[2] - wt[2] * m[1], wt[2] * m[0] - wt[0] * m[2],
+                             wt[0] * m[1] - wt[1] * m[0], m[0], m[1], m[2]};
+        accum_row(acc, J, r, a.s_geo);
+        acc[28] += r * r;
+      }
     }
   }
-  block_reduce_store<29>(acc, a.item_out + (int64_t)blockIdx.x * SFB_ITEM_STRIDE);
+  double* out = a.item_out + (int64_t)blockIdx.x * SFB_ITEM_STRIDE;
+  if (PREV) {
+    double tail[31];
+#pragma unroll
+    for (int k = 0; k < 29; ++k) tail[k] = acc[k];
+    tail[29] = eprev_p;
+    tail[30] = eprev_g;
+    block_reduce_store<31>(tail, out);
+  } else {
+    block_reduce_store<29>(acc, out);
+    if (threadIdx.x == 0) { out[29] = 0.0; out[30] = 0.0; }
+  }
 }
 
 void launch_dense_linearize(const DenseArgs& a, cudaStream_t s) {
   if (a.n_items <= 0) return;
+  const bool std_order = a.rd.apply_n == 0;
+  const bool prev = a.photo_mask_prev != nullptr;
   sfb_count_launch();
-  k_dense_linearize<<<a.n_items, DENSE_THREADS, 0, s>>>(a);
+  if (std_order && prev) k_dense_fused<true, true><<<a.n_items, DENSE_THREADS, 0, s>>>(a);
+  else if (std_order) k_dense_fused<true, false><<<a.n_items, DENSE_THREADS, 0, s>>>(a);
+  else if (prev) k_dense_fused<false, true><<<a.n_items, DENSE_THREADS, 0, s>>>(a);
+  else k_dense_fused<false, false><<<a.n_items, DENSE_THREADS, 0, s>>>(a);
 }
 
 // Frozen-association energy at the current poses.
@@ -369,8 +610,13 @@ __global__ void k_assemble(AssembleArgs a) {
       }
     }
     double* D = a.D + (int64_t)v * 36;
+    double* S = a.Brow + (int64_t)a.row_ptr[v] * 36;
     D[e0] = d0;
-    if (e1 < 36) D[e1] = d1;
+    S[e0] = d0;
+    if (e1 < 36) {
+      D[e1] = d1;
+      S[e1] = d1;
+    }
     if (lane < 6) a.g[v * 6 + lane] = gv;
   } else if (warp < a.n_blk + a.n_pairs) {
     const int q = warp - a.n_blk;
@@ -395,8 +641,16 @@ __global__ void k_assemble(AssembleArgs a) {
       }
     }
     double* B = a.B + (int64_t)q * 36;
+    double* Sa = a.Brow + (int64_t)a.pair_slot[2 * q] * 36;      // row a: as is
+    double* Sb = a.Brow + (int64_t)a.pair_slot[2 * q + 1] * 36;  // row b: transposed
     B[e0] = b0;
-    if (e1 < 36) B[e1] = b1;
+    Sa[e0] = b0;
+    Sb[(e0 % 6) * 6 + e0 / 6] = b0;
+    if (e1 < 36) {
+      B[e1] = b1;
+      Sa[e1] = b1;
+      Sb[(e1 % 6) * 6 + e1 / 6] = b1;
+    }
   }
 }
 
@@ -413,35 +667,38 @@ void launch_assemble(const AssembleArgs& a, cudaStream_t s) {
 __global__ void k_sum_energies(const double* set_out, int n_sets, const double* edge_out,
                                int n_dir, const double* item_e2, int n_items, double* out3,
                                int mode) {
-  __shared__ double sh[3][32];
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-  for (int i = threadIdx.x; i < n_sets; i += blockDim.x) s0 += set_out[(int64_t)i * SFB_SET_STRIDE + SFB_SET_E];
+  // mode 0 writes 5 values: {set E, edge e_photo, edge e_geo, edge prev e_photo, edge prev e_geo}
+  __shared__ double sh[5][32];
+  double s[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int i = threadIdx.x; i < n_sets; i += blockDim.x) s[0] += set_out[(int64_t)i * SFB_SET_STRIDE + SFB_SET_E];
   if (mode == 0) {
     for (int i = threadIdx.x; i < n_dir; i += blockDim.x) {
-      s1 += edge_out[(int64_t)i * SFB_ITEM_STRIDE + SFB_ITEM_EP];
-      s2 += edge_out[(int64_t)i * SFB_ITEM_STRIDE + SFB_ITEM_EG];
+      const double* e = edge_out + (int64_t)i * SFB_ITEM_STRIDE;
+      s[1] += e[SFB_ITEM_EP];
+      s[2] += e[SFB_ITEM_EG];
+      s[3] += e[SFB_ITEM_PP];
+      s[4] += e[SFB_ITEM_PG];
     }
   } else {
     for (int i = threadIdx.x; i < n_items; i += blockDim.x) {
-      s1 += item_e2[2 * (int64_t)i];
-      s2 += item_e2[2 * (int64_t)i + 1];
+      s[1] += item_e2[2 * (int64_t)i];
+      s[2] += item_e2[2 * (int64_t)i + 1];
     }
   }
-  s0 = warp_sum(s0);
-  s1 = warp_sum(s1);
-  s2 = warp_sum(s2);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (lane == 0) { sh[0][warp] = s0; sh[1][warp] = s1; sh[2][warp] = s2; }
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const double v = warp_sum(s[k]);
+    if (lane == 0) sh[k][warp] = v;
+  }
   __syncthreads();
   if (warp == 0) {
     const int nw = blockDim.x >> 5;
-    double a0 = lane < nw ? sh[0][lane] : 0.0;
-    double a1 = lane < nw ? sh[1][lane] : 0.0;
-    double a2 = lane < nw ? sh[2][lane] : 0.0;
-    a0 = warp_sum(a0);
-    a1 = warp_sum(a1);
-    a2 = warp_sum(a2);
-    if (lane == 0) { out3[0] = a0; out3[1] = a1; out3[2] = a2; }
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const double v = warp_sum(lane < nw ? sh[k][lane] : 0.0);
+      if (lane == 0 && (mode == 0 || k < 3)) out3[k] = v;
+    }
   }
 }
 

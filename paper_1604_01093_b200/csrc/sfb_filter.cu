@@ -96,9 +96,90 @@ __global__ void __launch_bounds__(256) k_overlap(const FrameDev* frames, const P
   if (!full_count && threadIdx.x == 0) pass[blockIdx.x] = ok ? 1 : 0;
 }
 
+// Tile culling.  A tile's bounding sphere, moved by the (plainly rounded)
+// relative pose, is classified against the target frustum's five half-spaces
+// n.q >= 0 (n = (fx,0,cx), (-fx,0,w-1-cx), (0,fy,cy), (0,-fy,h-1-cy)) and
+// q_z > 0.  The radius carries a 1e-7 m margin, far above the ~1e-13 m error
+// of the plain transform and of NumPy's own rounding, so "no point inside"
+// and "every point inside" hold for the exactly-rounded per-point test too:
+// culling never changes a decision, it only skips work.
+__device__ __forceinline__ int classify_tile(const Xf& rel, const double4 s, const FrameDev& Fb) {
+  if (s.w < 0.0) return 0;
+  double c[3];
+  xf_apply(rel.R, rel.t, s.x, s.y, s.z, c);
+  const double r = s.w * (1.0 + 1e-7) + 1e-7;
+  const double wm1 = (double)(Fb.w - 1), hm1 = (double)(Fb.h - 1);
+  const double n[4][3] = {{Fb.fx, 0.0, Fb.cx}, {-Fb.fx, 0.0, wm1 - Fb.cx},
+                          {0.0, Fb.fy, Fb.cy}, {0.0, -Fb.fy, hm1 - Fb.cy}};
+  bool all_in = c[2] - r > 0.0;
+  if (c[2] + r <= 0.0) return 0;
+  for (int k = 0; k < 4; ++k) {
+    const double d = n[k][0] * c[0] + n[k][1] * c[1] + n[k][2] * c[2];
+    const double nn = sqrt(n[k][0] * n[k][0] + n[k][1] * n[k][1] + n[k][2] * n[k][2]);
+    if (d + r * nn < 0.0) return 0;
+    if (d - r * nn <= 0.0) all_in = false;
+  }
+  return all_in ? 1 : 2;
+}
+
+__global__ void __launch_bounds__(256) k_overlap_culled(const FrameDev* frames, const PoseDev* poses,
+                                                        const int2* cand, Rounding rd,
+                                                        uint8_t* pass) {
+  __shared__ Xf rel[2];
+  __shared__ int partial[1024];
+  __shared__ int n_partial;
+  const int2 ab = cand[blockIdx.x];
+  if (threadIdx.x < 2) {
+    const int s = threadIdx.x == 0 ? ab.x : ab.y;
+    const int t = threadIdx.x == 0 ? ab.y : ab.x;
+    rel[threadIdx.x] = xf_relative_exact(poses[s], poses[t], rd);
+  }
+  __syncthreads();
+  bool ok = true;
+  for (int dir = 0; dir < 2 && ok; ++dir) {
+    const FrameDev Fa = frames[dir == 0 ? ab.x : ab.y];
+    const FrameDev Fb = frames[dir == 0 ? ab.y : ab.x];
+    const int ord = Fa.n_valid_depth == 1 ? rd.apply_1 : rd.apply_n;
+    const int nt = Fa.tiles_x * Fa.tiles_y;
+    bool found = false;
+    for (int t0 = 0; t0 < nt && !found; t0 += 1024) {
+      if (threadIdx.x == 0) n_partial = 0;
+      __syncthreads();
+      bool any_in = false;
+      for (int t = t0 + threadIdx.x; t < min(nt, t0 + 1024); t += blockDim.x) {
+        const int cls = classify_tile(rel[dir], Fa.tiles[t], Fb);
+        if (cls == 1 && Fa.tile_count[t] > 0) any_in = true;
+        if (cls == 2) partial[atomicAdd(&n_partial, 1)] = t;
+      }
+      if (__syncthreads_or(any_in)) {
+        found = true;
+        break;
+      }
+      const int np = n_partial;
+      for (int k = 0; k < np && !found; ++k) {
+        const int t = partial[k];
+        const int x = (t % Fa.tiles_x) * SFB_TILE + (threadIdx.x % SFB_TILE);
+        const int y = (t / Fa.tiles_x) * SFB_TILE + (threadIdx.x / SFB_TILE);
+        bool in = false;
+        if (x < Fa.w && y < Fa.h) {
+          const float4 P = __ldg(&Fa.P[y * Fa.w + x]);
+          in = (__float_as_uint(P.w) & SFB_FLAG_VD) && point_inside(rel[dir], Fb, P, ord);
+        }
+        if (__syncthreads_or(in)) found = true;
+      }
+      __syncthreads();
+    }
+    ok = found;
+  }
+  if (threadIdx.x == 0) pass[blockIdx.x] = ok ? 1 : 0;
+}
+
 void launch_overlap(const FrameDev* frames, const PoseDev* poses, const int2* cand, int n_cand,
                     Rounding rd, int full_count, uint8_t* pass, int* counts, cudaStream_t s) {
   if (n_cand <= 0) return;
   sfb_count_launch();
-  k_overlap<<<n_cand, 256, 0, s>>>(frames, poses, cand, rd, full_count, pass, counts);
+  if (full_count)
+    k_overlap<<<n_cand, 256, 0, s>>>(frames, poses, cand, rd, full_count, pass, counts);
+  else
+    k_overlap_culled<<<n_cand, 256, 0, s>>>(frames, poses, cand, rd, pass);
 }

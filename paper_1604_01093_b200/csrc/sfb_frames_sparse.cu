@@ -302,3 +302,56 @@ void launch_pose_update(PoseDev* poses, int n_frames, const double* dx, double* 
   sfb_count_launch();
   k_pose_update<<<blocks, 256, 0, s>>>(poses, n_frames, dx, step_norm, skip);
 }
+
+// ---------------------------------------------------------------------------
+// Per-tile bounding spheres of the valid points (one warp per 16x16 tile):
+// centre = AABB centre, radius = max distance, inflated so the sphere bounds
+// every point with margin to spare for rounding.
+__global__ void k_tiles(const float4* P, int w, int h, int tx, int ty, double4* tiles, int* counts) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= tx * ty) return;
+  const int x0 = (warp % tx) * SFB_TILE, y0 = (warp / tx) * SFB_TILE;
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  int c = 0;
+  for (int k = lane; k < SFB_TILE * SFB_TILE; k += 32) {
+    const int x = x0 + (k % SFB_TILE), y = y0 + (k / SFB_TILE);
+    if (x >= w || y >= h) continue;
+    const float4 p = P[y * w + x];
+    if (!(__float_as_uint(p.w) & SFB_FLAG_VD)) continue;
+    const double q[3] = {p.x, p.y, p.z};
+    for (int d = 0; d < 3; ++d) { lo[d] = fmin(lo[d], q[d]); hi[d] = fmax(hi[d], q[d]); }
+    ++c;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    c += __shfl_xor_sync(0xffffffffu, c, o);
+    for (int d = 0; d < 3; ++d) {
+      lo[d] = fmin(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], o));
+      hi[d] = fmax(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], o));
+    }
+  }
+  double ctr[3];
+  for (int d = 0; d < 3; ++d) ctr[d] = 0.5 * (lo[d] + hi[d]);
+  double r2 = 0.0;
+  for (int k = lane; k < SFB_TILE * SFB_TILE; k += 32) {
+    const int x = x0 + (k % SFB_TILE), y = y0 + (k / SFB_TILE);
+    if (x >= w || y >= h) continue;
+    const float4 p = P[y * w + x];
+    if (!(__float_as_uint(p.w) & SFB_FLAG_VD)) continue;
+    const double dx = p.x - ctr[0], dy = p.y - ctr[1], dz = p.z - ctr[2];
+    r2 = fmax(r2, dx * dx + dy * dy + dz * dz);
+  }
+  for (int o = 16; o > 0; o >>= 1) r2 = fmax(r2, __shfl_xor_sync(0xffffffffu, r2, o));
+  if (lane == 0) {
+    const double r = sqrt(r2) * (1.0 + 1e-9) + 1e-9;
+    tiles[warp] = c > 0 ? make_double4(ctr[0], ctr[1], ctr[2], r) : make_double4(0, 0, 0, -1.0);
+    counts[warp] = c;
+  }
+}
+
+void launch_tiles(const float4* P, int w, int h, int tx, int ty, double4* tiles, int* counts,
+                  cudaStream_t s) {
+  const int n = tx * ty;
+  sfb_count_launch();
+  k_tiles<<<(n * 32 + 255) / 256, 256, 0, s>>>(P, w, h, tx, ty, tiles, counts);
+}

@@ -23,7 +23,14 @@ struct FrameDev {
   int w, h;
   int n_valid_depth;  // #valid_depth pixels (NumPy m == 1 rounding special case)
   int n_valid_geo;    // #(valid_depth & valid_normal) pixels
+  // 16x16 pixel tiles: conservative bounding sphere of the valid points
+  // (cx, cy, cz, r) and their count; used to cull the frame-pair filter.
+  const double4* tiles;
+  const int* tile_count;
+  int tiles_x, tiles_y;
 };
+
+#define SFB_TILE 16
 
 struct PoseDev {
   double R[9];  // row-major
@@ -181,6 +188,8 @@ __host__ __device__ constexpr int sym6(int r, int c) {
 #define SFB_ITEM_STRIDE 32
 #define SFB_ITEM_EP 27
 #define SFB_ITEM_EG 28
+#define SFB_ITEM_PP 29  // frozen energy of the previous linearisation (fused pass)
+#define SFB_ITEM_PG 30
 // Per-sparse-set output: Hii[36] Hjj[36] Hij[36] gi[6] gj[6] E (+3 pad).
 #define SFB_SET_STRIDE 128
 #define SFB_SET_GI 108

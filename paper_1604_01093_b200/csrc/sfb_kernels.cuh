@@ -40,6 +40,9 @@ struct DenseArgs {
   const int64_t* geo_off;   // per dir edge: u16 offset
   uint32_t* photo_mask;
   uint16_t* geo_tgt;
+  const uint32_t* photo_mask_prev;  // previous linearisation's frozen sets (fused
+  const uint16_t* geo_tgt_prev;     // energy-after), or null
+  int prev_photo, prev_geo;         // which frozen terms the previous pass produced
   double* item_out;         // SFB_ITEM_STRIDE per item
   Rounding rd;
   double s_photo, s_geo;
@@ -61,21 +64,23 @@ struct AssembleArgs {
   double* D;          // n_blk * 36
   double* B;          // n_pairs * 36
   double* g;          // n_blk * 6
+  const int* row_ptr;    // matvec slots: row_ptr[v] is v's diagonal slot
+  const int* pair_slot;  // 2 per pair: slot in row a (as is), in row b (transposed)
+  double* Brow;          // slots * 36
   int dense_on;
 };
 
 struct PcgArgs {
   int n_blk;
-  const double* D;
-  const double* B;
-  const int* row_ptr;
-  const int* row_ent;  // pair << 1 | transposed
-  const int* row_col;
+  const double* Brow;  // slot blocks, row-major, oriented for their row
+  const int* row_ptr;  // slots of row v: [row_ptr[v], row_ptr[v+1]), first = diagonal
+  const int* row_col;  // column block of each slot
   const double* g;
   double* x;
   double* r;
   double* z;
   double* p;
+  double* p2;          // ping-pong partner of p
   double* Ap;
   double* inv_diag;
   double* b;
@@ -93,6 +98,8 @@ struct PcgArgs {
 void sfb_count_launch(int n = 1);
 
 void launch_pack(const PackArgs& a, cudaStream_t s);
+void launch_tiles(const float4* P, int w, int h, int tx, int ty, double4* tiles, int* counts,
+                  cudaStream_t s);
 void launch_sparse(const SparseArgs& a, cudaStream_t s);
 void launch_dense_linearize(const DenseArgs& a, cudaStream_t s);
 void launch_dense_energy(const DenseArgs& a, double* item_e2, cudaStream_t s);

@@ -1,60 +1,116 @@
 // Block-sparse normal equations: matvec and the persistent scalar-Jacobi PCG.
 //
-// The system is stored as 6x6 blocks: one diagonal block per variable frame
-// and one off-diagonal block per frame pair that shares a correspondence set
-// or a dense edge.  NormalEquations.apply (solver.py:403-410) is then a block
-// row product; pcg_solve (solver.py:463-508) runs as ONE cooperative kernel
-// whose blocks all compute the same scalars from the same fixed-order
-// partial sums, so control flow (breaks, restarts) is grid-uniform and
-// bit-reproducible.
-#include <cooperative_groups.h>
-
+// The system is stored per block row as contiguous, pre-oriented 6x6 slot
+// blocks (diagonal first, then one per coupled frame).  NormalEquations.apply
+// (solver.py:403-410) is one pass over the slots; pcg_solve (solver.py:463-508)
+// is ONE cooperative kernel:
+//  * each CTA owns a contiguous range of block rows (one warp per row) and
+//    stages that range's slot blocks in shared memory once per solve - the
+//    matrix is constant across PCG iterations;
+//  * per iteration a warp gathers the (6-vector) neighbour inputs of its row
+//    into shared memory with all loads in flight at once, then multiplies
+//    from shared memory;
+//  * p = z + beta p is folded into the next matvec (neighbours form it on the
+//    fly, the owner stores it in a ping-pong buffer): two grid barriers per
+//    iteration, three on restart iterations;
+//  * every CTA sums the per-CTA partials in the same order, so all scalars,
+//    breaks and restarts are grid-uniform and bit-reproducible.
 #include "sfb_kernels.cuh"
-
-namespace cg = cooperative_groups;
 
 #define PCG_THREADS 256
 #define PCG_WARPS (PCG_THREADS / 32)
+#define PCG_GATHER_CAP 80                    // neighbour slots gathered per pass
+#define PCG_SMEM_BYTES (200 * 1024)          // dynamic smem request
+#define PCG_GATHER_BYTES (PCG_WARPS * PCG_GATHER_CAP * 6 * 8)
 
-// y_v = D_v x_v + sum_w B_vw x_w for one block row, computed by one warp:
-// lanes are 5 groups of 6 (lane = 6*group + row); each group walks every 5th
-// neighbour block, each lane one row of it; groups are summed in fixed order.
-// Returns y_v[row] in lanes 0..5 (other lanes undefined).
-__device__ __forceinline__ double block_row(const PcgArgs& a, int v, const double* __restrict__ xin,
-                                            int lane) {
-  const int grp = lane / 6, row = lane - 6 * (lane / 6);
-  double acc = 0.0;
-  if (grp < 5) {
-    if (grp == 0) {
-      const double* Dm = a.D + (int64_t)v * 36 + row * 6;
-      const double* xv = xin + 6 * v;
-#pragma unroll
-      for (int c = 0; c < 6; ++c) acc = fma(Dm[c], xv[c], acc);
+// Grid-wide barrier for a co-resident (cooperative) grid: one arrival counter
+// in global memory, zeroed before launch; thread 0 of each CTA releases the
+// CTA's writes, arrives, spins on a relaxed load and acquires.
+struct GridBarrier {
+  unsigned* ctr;
+  unsigned epoch;
+  __device__ __forceinline__ void sync(unsigned G) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      ++epoch;
+      __threadfence();
+      atomicAdd(ctr, 1u);
+      const unsigned target = epoch * G;
+      unsigned v;
+      do {
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+      } while (v < target);
+      __threadfence();
     }
-    for (int e = a.row_ptr[v] + grp; e < a.row_ptr[v + 1]; e += 5) {
-      const int ent = a.row_ent[e];
-      const double* Bm = a.B + (int64_t)(ent >> 1) * 36;
-      const double* xw = xin + 6 * a.row_col[e];
-      if (ent & 1) {
+    __syncthreads();
+  }
+};
+
+// Per-CTA view of the block rows it owns.
+struct RowCtx {
+  int r0, r1;          // owned rows [r0, r1)
+  int s0;              // first slot of r0
+  const double* Bs;    // staged slot blocks (shared) or null
+  double* gbuf;        // this warp's gather buffer (shared), PCG_GATHER_CAP x 6
+};
+
+// y = (row v of A) . xin, xin = FOLD ? z + beta*pold : pold.  Lanes 6g+r
+// (g < 5) walk slots g, g+5, ... of the current gather chunk; lanes 0..5
+// return y[r].
+template <bool FOLD>
+__device__ __forceinline__ double row_product(const PcgArgs& a, const RowCtx& rc, int v,
+                                              const double* __restrict__ z,
+                                              const double* __restrict__ pold, double beta,
+                                              int lane) {
+  const int grp = lane / 6, r = lane - 6 * grp;
+  const int e0 = a.row_ptr[v], e1 = a.row_ptr[v + 1];
+  double acc = 0.0;
+  for (int c0 = e0; c0 < e1; c0 += PCG_GATHER_CAP) {
+    const int c1 = min(e1, c0 + PCG_GATHER_CAP);
+    // gather the chunk's neighbour vectors: every load of the chunk in flight
+    for (int k = c0 + lane; k < c1; k += 32) {
+      const int w = a.row_col[k];
+      const double2* pw = reinterpret_cast<const double2*>(pold + 6 * w);
+      double2 x01 = __ldcg(pw), x23 = __ldcg(pw + 1), x45 = __ldcg(pw + 2);
+      if (FOLD) {
+        const double2* zw = reinterpret_cast<const double2*>(z + 6 * w);
+        const double2 z01 = __ldcg(zw), z23 = __ldcg(zw + 1), z45 = __ldcg(zw + 2);
+        x01.x = fma(beta, x01.x, z01.x); x01.y = fma(beta, x01.y, z01.y);
+        x23.x = fma(beta, x23.x, z23.x); x23.y = fma(beta, x23.y, z23.y);
+        x45.x = fma(beta, x45.x, z45.x); x45.y = fma(beta, x45.y, z45.y);
+      }
+      double2* gb = reinterpret_cast<double2*>(rc.gbuf + 6 * (k - c0));
+      gb[0] = x01;
+      gb[1] = x23;
+      gb[2] = x45;
+    }
+    __syncwarp();
+    if (grp < 5) {
+      for (int k = c0 + grp; k < c1; k += 5) {
+        const double* Bm = rc.Bs ? rc.Bs + (int64_t)(k - rc.s0) * 36 + r * 6
+                                 : a.Brow + (int64_t)k * 36 + r * 6;
+        const double* xv = rc.gbuf + 6 * (k - c0);
 #pragma unroll
-        for (int c = 0; c < 6; ++c) acc = fma(Bm[c * 6 + row], xw[c], acc);
-      } else {
-#pragma unroll
-        for (int c = 0; c < 6; ++c) acc = fma(Bm[row * 6 + c], xw[c], acc);
+        for (int c = 0; c < 6; ++c) acc = fma(Bm[c], xv[c], acc);
       }
     }
+    __syncwarp();
   }
   double s = 0.0;
+  const int rr = lane % 6;
 #pragma unroll
-  for (int g = 0; g < 5; ++g) s += __shfl_sync(0xffffffffu, acc, 6 * g + (lane % 6));
+  for (int g = 0; g < 5; ++g) s += __shfl_sync(0xffffffffu, acc, 6 * g + rr);
   return s;
 }
 
+// Plain matvec (NormalEquations.apply): one warp per row, no staging.
 __global__ void k_matvec(PcgArgs a, const double* xin, double* yout) {
+  __shared__ double gb[PCG_WARPS][PCG_GATHER_CAP * 6];
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= a.n_blk) return;
-  const double y = block_row(a, warp, xin, lane);
+  RowCtx rc{0, 0, 0, nullptr, gb[threadIdx.x >> 5]};
+  const double y = row_product<false>(a, rc, warp, nullptr, xin, 0.0, lane);
   if (lane < 6) yout[6 * warp + lane] = y;
 }
 
@@ -64,14 +120,14 @@ void launch_matvec(const PcgArgs& a, const double* xin, double* yout, cudaStream
   k_matvec<<<(a.n_blk * 32 + 255) / 256, 256, 0, s>>>(a, xin, yout);
 }
 
-// Deterministic block sum of NV values; every thread of the block gets them.
+// Deterministic block sum of NV per-warp values (lane 0 holds them); every
+// thread of the block receives the totals.
 template <int NV>
 __device__ __forceinline__ void block_allsum(double (&v)[NV], double (*sh)[PCG_WARPS]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
 #pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    const double s = warp_sum(v[k]);
-    if (lane == 0) sh[k][warp] = s;
+    for (int k = 0; k < NV; ++k) sh[k][warp] = v[k];
   }
   __syncthreads();
 #pragma unroll
@@ -84,7 +140,7 @@ __device__ __forceinline__ void block_allsum(double (&v)[NV], double (*sh)[PCG_W
   __syncthreads();
 }
 
-// Every block sums the per-block partials part[k*G + b] in the same fixed order.
+// Every CTA sums the per-CTA partials part[k*G + b] in the same order.
 template <int NV>
 __device__ __forceinline__ void grid_allsum(const double* part, double (&out)[NV], int G) {
   const int lane = threadIdx.x & 31;
@@ -96,157 +152,205 @@ __device__ __forceinline__ void grid_allsum(const double* part, double (&out)[NV
   }
 }
 
-// Matvec policies: the block-sparse normal equations, or a dense padded
-// matrix (pcg_solve on a duck-typed system, solver.py:463-508).
+// fixed-order sum of lanes 0..5 (one row value each), result in all lanes
+__device__ __forceinline__ double sum6(double v) {
+  double t = 0.0;
+#pragma unroll
+  for (int c = 0; c < 6; ++c) t += __shfl_sync(0xffffffffu, v, c);
+  return t;
+}
+
+// Matvec policies: block-row slots, or a dense padded matrix (pcg_solve on a
+// duck-typed system, solver.py:463-508).
 struct BsrMv {
-  __device__ __forceinline__ double row(const PcgArgs& a, int v, const double* x, int lane) const {
-    return block_row(a, v, x, lane);
+  template <bool FOLD>
+  __device__ __forceinline__ double row(const PcgArgs& a, const RowCtx& rc, int v, const double* z,
+                                        const double* pold, double beta, int lane) const {
+    return row_product<FOLD>(a, rc, v, z, pold, beta, lane);
   }
+  __device__ __forceinline__ bool stageable() const { return true; }
 };
 
 struct DenseMv {
   const double* A;  // (6 n_blk)^2 row-major, zero padded
-  __device__ __forceinline__ double row(const PcgArgs& a, int v, const double* x, int lane) const {
+  template <bool FOLD>
+  __device__ __forceinline__ double row(const PcgArgs& a, const RowCtx&, int v, const double* z,
+                                        const double* pold, double beta, int lane) const {
     const int n6 = 6 * a.n_blk;
     double out = 0.0;
     for (int r = 0; r < 6; ++r) {
       const double* Ar = A + (int64_t)(6 * v + r) * n6;
       double s = 0.0;
-      for (int c = lane; c < n6; c += 32) s = fma(Ar[c], x[c], s);
+      for (int c = lane; c < n6; c += 32) {
+        const double xc = FOLD ? fma(beta, __ldcg(pold + c), __ldcg(z + c)) : __ldcg(pold + c);
+        s = fma(Ar[c], xc, s);
+      }
       s = warp_sum(s);
       if (lane == r) out = s;
     }
     return out;
   }
+  __device__ __forceinline__ bool stageable() const { return false; }
 };
 
 template <class Mv>
-__global__ void __launch_bounds__(PCG_THREADS) k_pcg(PcgArgs a, Mv mv) {
-  cg::grid_group grid = cg::this_grid();
+__global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg(PcgArgs a, Mv mv, int rows_per_cta) {
+  extern __shared__ __align__(16) double smem[];
+  GridBarrier grid{reinterpret_cast<unsigned*>(a.flags), 0u};
   __shared__ double sh[4][PCG_WARPS];
   const int G = gridDim.x;
-  const int n = 6 * a.n_blk;
-  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-  const int nthreads = G * blockDim.x;
-  const int lane = threadIdx.x & 31, warp_in_blk = threadIdx.x >> 5;
-  const int gwarp = blockIdx.x * PCG_WARPS + warp_in_blk, nwarps = G * PCG_WARPS;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const bool own = lane < 6;
   if (a.skip && *a.skip != 0.0) return;  // grid-uniform
+  RowCtx rc;
+  rc.r0 = min(a.n_blk, blockIdx.x * rows_per_cta);
+  rc.r1 = min(a.n_blk, rc.r0 + rows_per_cta);
+  rc.s0 = 0;
+  rc.Bs = nullptr;
+  rc.gbuf = smem + wid * PCG_GATHER_CAP * 6;
+  if (mv.stageable() && rc.r1 > rc.r0) {
+    rc.s0 = a.row_ptr[rc.r0];
+    const int64_t n = (int64_t)(a.row_ptr[rc.r1] - rc.s0) * 36;
+    if ((int64_t)PCG_GATHER_BYTES + n * 8 <= PCG_SMEM_BYTES) {
+      double* dst = smem + PCG_WARPS * PCG_GATHER_CAP * 6;
+      const double* src = a.Brow + (int64_t)rc.s0 * 36;
+      for (int64_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+      rc.Bs = dst;
+    }
+  }
+  __syncthreads();
+  double* pa = a.p;   // p of the previous iteration (read by neighbours)
+  double* pb = a.p2;  // p of this iteration (written by owners)
+  double* partA = a.part;          // G   : p.Ap
+  double* partB = a.part + G;      // 3G  : r.r, r.z, non-finite(x)
 
-  // ---- setup: b = -g, x = 0, inv_diag, r = b, z = M^-1 r, p = z (solver.py:472-481)
+  // ---- setup (solver.py:472-481), owner rows
   {
     double v[2] = {0.0, 0.0};
-    for (int i = tid; i < n; i += nthreads) {
-      const double bi = -a.g[i];
-      const double di = a.jdiag[i];
-      const double inv = 1.0 / fmax(di, 1e-12);
-      const double zi = inv * bi;
-      a.b[i] = bi;
-      a.x[i] = 0.0;
-      a.inv_diag[i] = inv;
-      a.r[i] = bi;
-      a.z[i] = zi;
-      a.p[i] = zi;
-      v[0] += bi * bi;
-      v[1] += bi * zi;
+    for (int row = rc.r0 + wid; row < rc.r1; row += PCG_WARPS) {
+      double bb = 0.0, bz = 0.0;
+      if (own) {
+        const int i = 6 * row + lane;
+        const double bi = -a.g[i];
+        const double inv = 1.0 / fmax(a.jdiag[i], 1e-12);
+        const double zi = inv * bi;
+        a.b[i] = bi;
+        a.x[i] = 0.0;
+        a.inv_diag[i] = inv;
+        a.r[i] = bi;
+        a.z[i] = zi;
+        pa[i] = zi;
+        bb = bi * bi;
+        bz = bi * zi;
+      }
+      v[0] += sum6(bb);
+      v[1] += sum6(bz);
     }
     block_allsum<2>(v, sh);
-    if (threadIdx.x == 0) { a.part[0 * G + blockIdx.x] = v[0]; a.part[1 * G + blockIdx.x] = v[1]; }
+    if (threadIdx.x == 0) { partB[blockIdx.x] = v[0]; partB[G + blockIdx.x] = v[1]; }
   }
-  grid.sync();
+  grid.sync(G);
   double tot[2];
-  grid_allsum<2>(a.part, tot, G);
+  grid_allsum<2>(partB, tot, G);
   const double norm_b = sqrt(tot[0]);
   double rz = tot[1];
   int iterations = 0;
   double relative = 1.0;
   int status = 0;
+  double beta = 0.0;
+  bool fold = false;  // first iteration: p = z already in pa
   if (norm_b == 0.0) {
     relative = 0.0;
   } else {
     for (int k = 1; k <= a.max_it; ++k) {
       iterations = k;
-      grid.sync();  // p complete; everyone is done reading last iteration's partials
-      // ---- Ap = A p, partial p.Ap (block rows -> warps)
+      // ---- Ap = A p with p = z + beta pold formed on the fly; owners store p
       {
         double v[1] = {0.0};
-        for (int row = gwarp; row < a.n_blk; row += nwarps) {
-          const double y = mv.row(a, row, a.p, lane);
-          double pa = 0.0;
-          if (lane < 6) {
-            a.Ap[6 * row + lane] = y;
-            pa = a.p[6 * row + lane] * y;
+        for (int row = rc.r0 + wid; row < rc.r1; row += PCG_WARPS) {
+          const double y = fold ? mv.template row<true>(a, rc, row, a.z, pa, beta, lane)
+                                : mv.template row<false>(a, rc, row, a.z, pa, beta, lane);
+          double pAp = 0.0;
+          if (own) {
+            const int i = 6 * row + lane;
+            const double pi = fold ? fma(beta, __ldcg(pa + i), __ldcg(a.z + i)) : __ldcg(pa + i);
+            pb[i] = pi;
+            a.Ap[i] = y;
+            pAp = pi * y;
           }
-          // fixed-order sum over the 6 rows of the block
-          double t = 0.0;
-#pragma unroll
-          for (int c = 0; c < 6; ++c) t += __shfl_sync(0xffffffffu, pa, c);
-          if (lane == 0) v[0] += t;
+          v[0] += sum6(pAp);
         }
         block_allsum<1>(v, sh);
-        if (threadIdx.x == 0) a.part[blockIdx.x] = v[0];
+        if (threadIdx.x == 0) partA[blockIdx.x] = v[0];
       }
-      grid.sync();
+      grid.sync(G);
       double pAp_a[1];
-      grid_allsum<1>(a.part, pAp_a, G);
+      grid_allsum<1>(partA, pAp_a, G);
       const double pAp = pAp_a[0];
       if (!isfinite(pAp)) { status = 1; break; }  // PcgDivergenceError
       if (pAp <= 0.0) break;                       // singular direction
       const double alpha = rz / pAp;
       const bool restart = (k % a.restart) == 0;
-      double* pr = a.part + G;  // r-phase partials live apart from the p.Ap ones
-      // ---- x += alpha p ; r -= alpha Ap (or r = b - A x after a sync)
-      if (!restart) {
+      // ---- x += alpha p ; r -= alpha Ap (or r = b - A x) ; z = M^-1 r
+      {
         double v[3] = {0.0, 0.0, 0.0};
-        for (int i = tid; i < n; i += nthreads) {
-          const double xi = a.x[i] + alpha * a.p[i];
-          const double ri = a.r[i] - alpha * a.Ap[i];
-          const double zi = a.inv_diag[i] * ri;
-          a.x[i] = xi;
-          a.r[i] = ri;
-          a.z[i] = zi;
-          v[0] += ri * ri;
-          v[1] += ri * zi;
-          v[2] += isfinite(xi) ? 0.0 : 1.0;
+        for (int row = rc.r0 + wid; row < rc.r1; row += PCG_WARPS) {
+          double rr = 0.0, rzv = 0.0, bad = 0.0;
+          if (own) {
+            const int i = 6 * row + lane;
+            const double xi = fma(alpha, pb[i], a.x[i]);
+            a.x[i] = xi;
+            bad = isfinite(xi) ? 0.0 : 1.0;
+            if (!restart) {
+              const double ri = fma(-alpha, a.Ap[i], a.r[i]);
+              const double zi = a.inv_diag[i] * ri;
+              a.r[i] = ri;
+              a.z[i] = zi;
+              rr = ri * ri;
+              rzv = ri * zi;
+            }
+          }
+          v[0] += sum6(rr);
+          v[1] += sum6(rzv);
+          v[2] += sum6(bad);
+        }
+        if (restart) {
+          grid.sync(G);  // x complete
+          for (int row = rc.r0 + wid; row < rc.r1; row += PCG_WARPS) {
+            const double y = mv.template row<false>(a, rc, row, nullptr, a.x, 0.0, lane);
+            double rr = 0.0, rzv = 0.0;
+            if (own) {
+              const int i = 6 * row + lane;
+              const double ri = a.b[i] - y;
+              const double zi = a.inv_diag[i] * ri;
+              a.r[i] = ri;
+              a.z[i] = zi;
+              rr = ri * ri;
+              rzv = ri * zi;
+            }
+            v[0] += sum6(rr);
+            v[1] += sum6(rzv);
+          }
         }
         block_allsum<3>(v, sh);
-        if (threadIdx.x == 0)
-          for (int q = 0; q < 3; ++q) pr[q * G + blockIdx.x] = v[q];
-      } else {
-        double v[1] = {0.0};
-        for (int i = tid; i < n; i += nthreads) {
-          const double xi = a.x[i] + alpha * a.p[i];
-          a.x[i] = xi;
-          v[0] += isfinite(xi) ? 0.0 : 1.0;
+        if (threadIdx.x == 0) {
+#pragma unroll
+          for (int q = 0; q < 3; ++q) partB[q * G + blockIdx.x] = v[q];
         }
-        block_allsum<1>(v, sh);
-        if (threadIdx.x == 0) pr[2 * G + blockIdx.x] = v[0];
-        grid.sync();
-        for (int row = gwarp; row < a.n_blk; row += nwarps) {
-          const double y = mv.row(a, row, a.x, lane);
-          if (lane < 6) a.r[6 * row + lane] = a.b[6 * row + lane] - y;
-        }
-        grid.sync();
-        double w[2] = {0.0, 0.0};
-        for (int i = tid; i < n; i += nthreads) {
-          const double ri = a.r[i];
-          const double zi = a.inv_diag[i] * ri;
-          a.z[i] = zi;
-          w[0] += ri * ri;
-          w[1] += ri * zi;
-        }
-        block_allsum<2>(w, sh);
-        if (threadIdx.x == 0) { pr[0 * G + blockIdx.x] = w[0]; pr[1 * G + blockIdx.x] = w[1]; }
       }
-      grid.sync();
+      grid.sync(G);
       double s3[3];
-      grid_allsum<3>(pr, s3, G);
+      grid_allsum<3>(partB, s3, G);
       if (s3[2] != 0.0) { status = 1; break; }  // non-finite iterate
       relative = sqrt(s3[0]) / norm_b;
       if (relative < a.tol) break;
       const double rz_new = s3[1];
-      const double beta = rz_new / rz;
+      beta = rz_new / rz;
       rz = rz_new;
-      for (int i = tid; i < n; i += nthreads) a.p[i] = a.z[i] + beta * a.p[i];
+      double* t = pa;  // this iteration's p becomes "previous"
+      pa = pb;
+      pb = t;
+      fold = true;
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -258,19 +362,36 @@ __global__ void __launch_bounds__(PCG_THREADS) k_pcg(PcgArgs a, Mv mv) {
 
 template <class Mv>
 static cudaError_t launch_pcg_t(const PcgArgs& a, Mv mv, int n_sm, cudaStream_t s) {
-  int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg<Mv>, PCG_THREADS, 0);
-  if (e != cudaSuccess) return e;
-  int want = (a.n_blk + PCG_WARPS - 1) / PCG_WARPS;
-  const int cap = n_sm * (per_sm < 1 ? 1 : per_sm);
-  if (want > n_sm) want = n_sm;  // one CTA per SM at most: cheapest grid barrier
-  if (want > cap) want = cap;
-  if (want < 1) want = 1;
+  static bool attr_set = false;
+  cudaError_t e;
+  if (!attr_set) {
+    e = cudaFuncSetAttribute(k_pcg<BsrMv>, cudaFuncAttributeMaxDynamicSharedMemorySize, PCG_SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_pcg<DenseMv>, cudaFuncAttributeMaxDynamicSharedMemorySize, PCG_SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  // one CTA per SM at most (co-residency, cheapest barrier); rows split evenly
+  int G = (a.n_blk + PCG_WARPS - 1) / PCG_WARPS;
+  if (G > n_sm) G = n_sm;
+  static const int forced = [] {
+    const char* v = getenv("SFB_PCG_BLOCKS");
+    return v ? atoi(v) : 0;
+  }();
+  if (forced > 0 && forced <= n_sm) G = forced;
+  if (G < 1) G = 1;
+  int rows_per_cta = (a.n_blk + G - 1) / G;
+  if (rows_per_cta < 1) rows_per_cta = 1;
+  G = (a.n_blk + rows_per_cta - 1) / rows_per_cta;
+  if (G < 1) G = 1;
   PcgArgs args = a;
   Mv m = mv;
-  void* params[] = {&args, &m};
+  void* params[] = {&args, &m, &rows_per_cta};
+  e = cudaMemsetAsync(a.flags, 0, sizeof(unsigned), s);  // grid barrier counter
+  if (e != cudaSuccess) return e;
   sfb_count_launch();
-  return cudaLaunchCooperativeKernel((void*)k_pcg<Mv>, dim3(want), dim3(PCG_THREADS), params, 0, s);
+  return cudaLaunchCooperativeKernel((void*)k_pcg<Mv>, dim3(G), dim3(PCG_THREADS), params,
+                                     PCG_SMEM_BYTES, s);
 }
 
 cudaError_t launch_pcg(const PcgArgs& a, int n_sm, cudaStream_t s) {

@@ -3,6 +3,7 @@
 from __future__ import annotations
 
 import ctypes as C
+import functools
 import math
 
 import numpy as np
@@ -24,6 +25,7 @@ def _pose_arrays(poses: list):
     return R, t, fl
 
 
+@functools.lru_cache(maxsize=64)
 def view_cos_threshold(max_deg: float) -> float:
     """Smallest c in [-1,1] with degrees(arccos(c)) < max_deg, evaluated with NumPy.
 
@@ -159,6 +161,17 @@ class DeviceProblem:
                                         C.byref(cfg), _abi.ptr(e)))
         self.version += 1
         return e
+
+    def energy_and_linearize(self, weights, prev_dense: bool, w_dense_next, config):
+        """(frozen energies of the last linearisation, next linearisation energies)
+        at the current poses, in one fused device pass."""
+        out = np.zeros(6)
+        w, cfg = self._w(weights), self._cfg(config)
+        self._ck(self.lib.sfb_energy_and_linearize(self.handle, C.byref(w), 1 if prev_dense else 0,
+                                                   C.c_double(w_dense_next), C.byref(cfg),
+                                                   _abi.ptr(out)))
+        self.version += 1
+        return out[:3], out[3:]
 
     def pcg(self, max_iterations, tolerance, restart_interval):
         it, st = C.c_int32(), C.c_int32()

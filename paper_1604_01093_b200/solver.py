@@ -599,9 +599,11 @@ class AlignmentProblem:
         dp.save_best()
         consecutive_increases = 0
         moved = False
+        e_next = None
         for it in range(max_iterations):
             w_dense = dense_ramp_weight(weights, it)
-            e = dp.linearize(weights, w_dense, config)
+            e = e_next if e_next is not None else dp.linearize(weights, w_dense, config)
+            e_next = None
             dense_on = self.caches is not None and w_dense > 0.0 and bool(self.dense_edges)
             energy_before = weights.sparse * float(e[0])
             if dense_on:
@@ -618,7 +620,13 @@ class AlignmentProblem:
                 break
             step_norm = dp.apply_step()
             moved = True
-            ea = dp.energy_frozen(w_dense > 0.0)
+            if it + 1 < max_iterations:
+                # E_after(it) and the linearisation of it+1 happen at the same
+                # poses: one fused device pass (discarded if the loop stops).
+                ea, e_next = dp.energy_and_linearize(
+                    weights, w_dense > 0.0, dense_ramp_weight(weights, it + 1), config)
+            else:
+                ea = dp.energy_frozen(w_dense > 0.0)
             energy_after = weights.sparse * float(ea[0])
             if w_dense > 0.0:
                 energy_after += w_dense * (weights.photo * float(ea[1]) + weights.geo * float(ea[2]))

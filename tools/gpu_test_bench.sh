@@ -1,0 +1,5 @@
+cd $GRAFT_REPO_ROOT
+timeout 1200 python -m pytest tests -x -q -m gpu -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1
+echo pytest rc=$?
+timeout 1200 python bench.py --config ${CFG:-cfg4} --steps 3 --warmup 2 --no-cpu-baseline ${BENCH_ARGS} > gpurun_out/bench.log 2>&1
+echo bench rc=$?
