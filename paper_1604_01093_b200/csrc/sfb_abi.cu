@@ -623,8 +623,8 @@ int sfb_frames_upload(sfb_ctx* c, int32_t n, const sfb_frame_desc* d, int32_t* s
   void* block = nullptr;
   CK(c, cudaMalloc(&block, total));
   CK(c, c->staging.ensure(stage));
-  CK(c, c->counts.ensure(2 * (size_t)n));
-  CK(c, cudaMemsetAsync(c->counts.p, 0, sizeof(int) * 2 * n, c->stream));
+  CK(c, c->counts.ensure(3 * (size_t)n));
+  CK(c, cudaMemsetAsync(c->counts.p, 0, sizeof(int) * 3 * n, c->stream));
   char* dst = static_cast<char*>(block);
   char* stg = reinterpret_cast<char*>(c->staging.p);
   std::vector<FrameDev> devs(n);
@@ -657,21 +657,26 @@ int sfb_frames_upload(sfb_ctx* c, int32_t n, const sfb_frame_desc* d, int32_t* s
     CK(c, cudaMemcpyAsync(snr, d[k].normals, hw * 12, cudaMemcpyHostToDevice, c->stream));
     CK(c, cudaMemcpyAsync(sgr, d[k].grad, hw * 8, cudaMemcpyHostToDevice, c->stream));
     PackArgs pa{svd, svn, spt, snr, sgr, const_cast<float4*>(f.P), const_cast<float4*>(f.N),
-                const_cast<float2*>(f.G), const_cast<float4*>(f.T), w, h, c->counts.p + 2 * k};
+                const_cast<float2*>(f.G), const_cast<float4*>(f.T), w, h, c->counts.p + 3 * k};
     launch_pack(pa, c->stream);
     launch_tiles(f.P, w, h, f.tiles_x, f.tiles_y, const_cast<double4*>(f.tiles),
                  const_cast<int*>(f.tile_count), c->stream);
     CKL(c);
     devs[k] = f;
   }
-  std::vector<int> cnt(2 * n);
-  CK(c, cudaMemcpyAsync(cnt.data(), c->counts.p, sizeof(int) * 2 * n, cudaMemcpyDeviceToHost, c->stream));
+  std::vector<int> cnt(3 * n);
+  CK(c, cudaMemcpyAsync(cnt.data(), c->counts.p, sizeof(int) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
   CK(c, cudaStreamSynchronize(c->stream));
+  for (int k = 0; k < n; ++k)
+    if (cnt[3 * k + 2] != 0) {
+      cudaFree(block);
+      return fail(c, SFB_E_ARG, "cache planes contain non-finite values (frame " + std::to_string(k) + ")");
+    }
   c->block_refs[block] = n;
   int search = 0;
   for (int k = 0; k < n; ++k) {
-    devs[k].n_valid_depth = cnt[2 * k];
-    devs[k].n_valid_geo = cnt[2 * k + 1];
+    devs[k].n_valid_depth = cnt[3 * k];
+    devs[k].n_valid_geo = cnt[3 * k + 1];
     while (search < (int)c->slots.size() && c->slots[search].alive) ++search;
     if (search == (int)c->slots.size()) c->slots.emplace_back();
     Slot& sl = c->slots[search];

@@ -370,8 +370,12 @@ __global__ void __launch_bounds__(DENSE_THREADS, 2) k_dense_fused(DenseArgs a) {
               const double x0 = __dsub_rn(q0, (double)PT.x);
               const double x1 = __dsub_rn(q1, (double)PT.y);
               const double x2 = __dsub_rn(q2, (double)PT.z);
-              const double dist = __dsqrt_rn(__dadd_rn(
-                  __dadd_rn(__dmul_rn(x0, x0), __dmul_rn(x1, x1)), __dmul_rn(x2, x2)));
+              // norm < dmax: compare squares; correctly rounded sqrt only near the gate
+              const double s2 = __dadd_rn(__dadd_rn(__dmul_rn(x0, x0), __dmul_rn(x1, x1)),
+                                          __dmul_rn(x2, x2));
+              const double dm2 = a.geo_dmax * a.geo_dmax;
+              const double dist = s2 < dm2 * (1.0 - 1e-12) ? 0.0
+                                  : (s2 > dm2 * (1.0 + 1e-12) ? a.geo_dmax : __dsqrt_rn(s2));
               const double n0 = N.x, n1 = N.y, n2 = N.z;
               double nr0, nr1, nr2;
               if (STD && ord_ge == 0) {

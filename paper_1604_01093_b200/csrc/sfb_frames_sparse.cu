@@ -30,6 +30,11 @@ __global__ void k_pack(PackArgs a) {
     a.T[2 * p + 1] = t1;
     cnt_vd += (int)vd;
     cnt_geo += (int)(vd & vn);
+    // the kernels convert planes with f2d(), exact for finite floats only
+    const bool fin = isfinite(a.pts[3 * p]) && isfinite(a.pts[3 * p + 1]) && isfinite(a.pts[3 * p + 2]) &&
+                     isfinite(a.nrm[3 * p]) && isfinite(a.nrm[3 * p + 1]) && isfinite(a.nrm[3 * p + 2]) &&
+                     isfinite(g.x) && isfinite(g.y);
+    if (!fin) atomicAdd(&a.counts[2], 1);
   }
   // integer counts: atomics are exact and order-independent
   for (int o = 16; o > 0; o >>= 1) {
