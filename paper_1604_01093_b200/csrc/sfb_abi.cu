@@ -10,6 +10,7 @@
 #include <cstring>
 #include <map>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include <cub/device/device_select.cuh>
@@ -159,6 +160,7 @@ struct sfb_problem : Handle {
   DBuf<int64_t> photo_off, geo_off;
   DBuf<uint32_t> photo_mask[2];  // frozen associations, double-buffered so the
   DBuf<uint16_t> geo_tgt[2];     // next linearisation can evaluate the last one
+  DBuf<uint8_t> tile_any[2];     // per (edge, source tile): any frozen association
   int cur = 0;                   // buffer holding the latest linearisation
   DBuf<double> item_out, edge_out, item_e2;
   bool dense_active = false;
@@ -177,6 +179,10 @@ struct sfb_problem : Handle {
   DBuf<double> dscal;       // device scalars
   double* hscal = nullptr;  // pinned mirror
   Prof prof;
+  // pair-filter scratch
+  DBuf<int2> f_all, f_cand, f_sel;
+  DBuf<uint8_t> f_fl, f_pass, f_temp;
+  DBuf<int> f_cnt;
 };
 
 namespace {
@@ -263,7 +269,9 @@ int rebuild_structure(sfb_problem* p, int bidir) {
     for (const int2& e : p->edges) dir.push_back(make_int2(e.y, e.x));
   p->n_dir = (int)dir.size();
 
-  // dense work items: (dir edge, pixel tile); tiles start on 32-pixel bounds
+  // dense work items: (dir edge, range of 16x16 source tiles); enough items
+  // to fill the GPU, at most 1024 tiles each.  Frozen associations live in
+  // tile-major slots: 256 per tile (8 photo-mask words, 256 geo targets).
   std::vector<int4> items;
   std::vector<int> eptr(1, 0);
   std::vector<int64_t> poff, goff;
@@ -271,71 +279,79 @@ int rebuild_structure(sfb_problem* p, int bidir) {
   const int target = 148 * 8;
   for (int d = 0; d < p->n_dir; ++d) {
     const FrameDev& F = p->frames_h[dir[d].x];
-    const int hw = F.w * F.h;
-    int tiles = std::max(1, (target + p->n_dir - 1) / std::max(1, p->n_dir));
-    tiles = std::min(tiles, std::max(1, (hw + 255) / 256));
-    int tile = (hw + tiles - 1) / tiles;
-    tile = (tile + 31) & ~31;
-    for (int b = 0; b < hw; b += tile) items.push_back(make_int4(d, b, std::min(hw, b + tile), 0));
+    const int nt = F.tiles_x * F.tiles_y;
+    int parts = std::max(1, (target + p->n_dir - 1) / std::max(1, p->n_dir));
+    parts = std::max(parts, (nt + 1023) / 1024);
+    parts = std::min(parts, nt);
+    const int per = (nt + parts - 1) / parts;
+    for (int b = 0; b < nt; b += per) items.push_back(make_int4(d, b, std::min(nt, b + per), 0));
     eptr.push_back((int)items.size());
     poff.push_back(pw);
     goff.push_back(gw);
-    pw += (hw + 31) / 32;
-    gw += (hw + 7) & ~7;
+    pw += (int64_t)nt * 8;
+    gw += (int64_t)nt * 256;
   }
   p->n_items = (int)items.size();
 
-  // contribution lists
-  std::map<std::pair<int, int>, int> pid;
-  std::vector<std::vector<int>> dl(nb), bl;
+  // Contribution lists as CSR, built in two counting passes (entries keep
+  // set order then edge order, so every sum is assembled in a fixed order).
+  // D/g entries per var: (id << 3) | kind; B entries per coupled pair.
+  struct Contrib {
+    int var, ent;
+  };
+  std::vector<Contrib> dc;
+  dc.reserve(2 * (size_t)(p->n_sets + p->n_dir) + 8);
+  std::vector<Contrib> bc;  // var = pair id
+  bc.reserve((size_t)(p->n_sets + p->n_dir) + 8);
+  std::unordered_map<int64_t, int> pid;
+  pid.reserve(2 * (size_t)(p->n_sets + p->n_dir) + 8);
   std::vector<int2> pv;
   auto pair_of = [&](int a, int b) {
-    auto key = std::make_pair(a, b);
-    auto it = pid.find(key);
-    if (it != pid.end()) return it->second;
-    const int q = (int)pv.size();
-    pid[key] = q;
-    pv.push_back(make_int2(a, b));
-    bl.emplace_back();
-    return q;
+    const int64_t key = (int64_t)a * nb + b;
+    auto ins = pid.emplace(key, (int)pv.size());
+    if (ins.second) pv.push_back(make_int2(a, b));
+    return ins.first->second;
   };
   for (int s = 0; s < p->n_sets; ++s) {
     const int vi = p->set_fi_h[s] - 1, vj = p->set_fj_h[s] - 1;
     if (vi == vj) {
       if (vi >= 0) {
-        dl[vi].push_back(s << 3 | 0);
-        dl[vi].push_back(s << 3 | 1);
-        dl[vi].push_back(s << 3 | 2);
+        dc.push_back({vi, s << 3 | 0});
+        dc.push_back({vi, s << 3 | 1});
+        dc.push_back({vi, s << 3 | 2});
       }
       continue;
     }
-    if (vi >= 0) dl[vi].push_back(s << 3 | 0);
-    if (vj >= 0) dl[vj].push_back(s << 3 | 1);
+    if (vi >= 0) dc.push_back({vi, s << 3 | 0});
+    if (vj >= 0) dc.push_back({vj, s << 3 | 1});
     if (vi >= 0 && vj >= 0) {
       const int a = std::min(vi, vj), b = std::max(vi, vj);
-      bl[pair_of(a, b)].push_back(s << 3 | (vi == a ? 0 : 1));
+      bc.push_back({pair_of(a, b), s << 3 | (vi == a ? 0 : 1)});
     }
   }
   for (int d = 0; d < p->n_dir; ++d) {
     const int vs = dir[d].x - 1, vd = dir[d].y - 1;
-    if (vs >= 0) dl[vs].push_back(d << 3 | 4);
-    if (vd >= 0) dl[vd].push_back(d << 3 | 5);
+    if (vs >= 0) dc.push_back({vs, d << 3 | 4});
+    if (vd >= 0) dc.push_back({vd, d << 3 | 5});
     if (vs >= 0 && vd >= 0) {
       const int a = std::min(vs, vd), b = std::max(vs, vd);
-      bl[pair_of(a, b)].push_back(d << 3 | 4);
+      bc.push_back({pair_of(a, b), d << 3 | 4});
     }
   }
   p->n_pairs = (int)pv.size();
   p->pair_vars = pv;
-  std::vector<int> dptr(1, 0), dent, bptr(1, 0), bent;
-  for (int v = 0; v < nb; ++v) {
-    dent.insert(dent.end(), dl[v].begin(), dl[v].end());
-    dptr.push_back((int)dent.size());
-  }
-  for (int q = 0; q < p->n_pairs; ++q) {
-    bent.insert(bent.end(), bl[q].begin(), bl[q].end());
-    bptr.push_back((int)bent.size());
-  }
+  auto to_csr = [](const std::vector<Contrib>& c, int rows, std::vector<int>& ptr,
+                   std::vector<int>& ent) {
+    ptr.assign(rows + 1, 0);
+    for (const Contrib& e : c) ++ptr[e.var + 1];
+    for (int r = 0; r < rows; ++r) ptr[r + 1] += ptr[r];
+    ent.resize(c.size());
+    std::vector<int> fill(ptr.begin(), ptr.end() - 1);
+    for (const Contrib& e : c) ent[fill[e.var]++] = e.ent;  // stable: input order kept
+  };
+  std::vector<int> dptr, dent, bptr, bent;
+  to_csr(dc, nb, dptr, dent);
+  to_csr(bc, p->n_pairs, bptr, bent);
   // matvec rows: slot 0 of row v is its diagonal block, then one pre-oriented
   // copy of every off-diagonal block touching v (pair_slot[2q] in row a as
   // is, pair_slot[2q+1] in row b transposed).
@@ -369,6 +385,7 @@ int rebuild_structure(sfb_problem* p, int bidir) {
   for (int b = 0; b < 2; ++b) {
     CK(p, p->photo_mask[b].ensure((size_t)std::max<int64_t>(pw, 1)));
     CK(p, p->geo_tgt[b].ensure((size_t)std::max<int64_t>(gw, 1)));
+    CK(p, p->tile_any[b].ensure((size_t)std::max<int64_t>(gw / 256, 1)));
   }
   CK(p, p->item_out.ensure((size_t)p->n_items * SFB_ITEM_STRIDE));
   CK(p, p->edge_out.ensure((size_t)p->n_dir * SFB_ITEM_STRIDE));
@@ -400,6 +417,7 @@ DenseArgs dense_args(sfb_problem* p) {
   a.geo_off = p->geo_off.p;
   a.photo_mask = p->photo_mask[p->cur].p;
   a.geo_tgt = p->geo_tgt[p->cur].p;
+  a.tile_any = p->tile_any[p->cur].p;
   a.item_out = p->item_out.p;
   a.rd = p->ctx->rd;
   a.n_items = p->n_items;
@@ -468,9 +486,11 @@ int enqueue_linearize(sfb_problem* p, const sfb_weights* w, double w_dense, cons
       const int nxt = 1 - p->cur;
       da.photo_mask = p->photo_mask[nxt].p;
       da.geo_tgt = p->geo_tgt[nxt].p;
+      da.tile_any = p->tile_any[nxt].p;
       if (prev_avail) {
         da.photo_mask_prev = p->photo_mask[p->cur].p;
         da.geo_tgt_prev = p->geo_tgt[p->cur].p;
+        da.tile_any_prev = p->tile_any[p->cur].p;
         da.prev_photo = p->last_do_photo;
         da.prev_geo = p->last_do_geo;
         if (prev_mode) *prev_mode = 1;
@@ -810,8 +830,16 @@ int sfb_problem_destroy(sfb_problem* p) {
   for (int b = 0; b < 2; ++b) {
     p->photo_mask[b].release();
     p->geo_tgt[b].release();
+    p->tile_any[b].release();
   }
   p->prof.destroy();
+  p->f_all.release();
+  p->f_cand.release();
+  p->f_sel.release();
+  p->f_fl.release();
+  p->f_pass.release();
+  p->f_temp.release();
+  p->f_cnt.release();
   if (p->hscal) cudaFreeHost(p->hscal);
   if (p->stream) cudaStreamDestroy(p->stream);
   delete p;
@@ -875,9 +903,14 @@ int sfb_build_dense_edges(sfb_problem* p, double cos_min, int64_t* n_out) {
   p->edges.clear();
   if (P > 0) {
     if (P > INT32_MAX) return fail(p, SFB_E_ARG, "too many frames for the pair filter");
-    DBuf<int2> all, cand, sel;
-    DBuf<uint8_t> fl, pass, temp;
-    DBuf<int> cnt;
+    // persistent scratch: no cudaMalloc/cudaFree (which synchronise) per solve
+    DBuf<int2>& all = p->f_all;
+    DBuf<int2>& cand = p->f_cand;
+    DBuf<int2>& sel = p->f_sel;
+    DBuf<uint8_t>& fl = p->f_fl;
+    DBuf<uint8_t>& pass = p->f_pass;
+    DBuf<uint8_t>& temp = p->f_temp;
+    DBuf<int>& cnt = p->f_cnt;
     CK(p, all.ensure(P));
     CK(p, cand.ensure(P));
     CK(p, fl.ensure(P));
@@ -914,7 +947,6 @@ int sfb_build_dense_edges(sfb_problem* p, double cos_min, int64_t* n_out) {
         CK(p, cudaMemcpyAsync(p->edges.data(), sel.p, sizeof(int2) * ne, cudaMemcpyDeviceToHost, s));
       CK(p, cudaStreamSynchronize(s));
     }
-    all.release(); cand.release(); sel.release(); fl.release(); pass.release(); temp.release(); cnt.release();
   }
   *n_out = (int64_t)p->edges.size();
   return rebuild_structure(p, p->struct_bidir < 0 ? 0 : p->struct_bidir);

@@ -270,6 +270,29 @@ __device__ __forceinline__ void bilinear_fast(const FrameDev& f, double x, doubl
   }
 }
 
+#define DENSE_MAX_TILES 1024
+
+// Can any point of this tile's bounding sphere (moved by rel) project into
+// the target frustum widened to [-0.5, w-0.5] x [-0.5, h-0.5], z > 0?  The
+// radius carries a 1e-7 m margin (>> rounding of the exact per-pixel path).
+__device__ __forceinline__ unsigned char tile_maybe_visible(const Xf& rel, const double4 s,
+                                                            const FrameDev& Fb) {
+  if (s.w < 0.0) return 0;  // no valid pixel in the tile
+  double c[3];
+  xf_apply(rel.R, rel.t, s.x, s.y, s.z, c);
+  const double r = s.w * (1.0 + 1e-7) + 1e-7;
+  if (c[2] + r <= 0.0) return 0;
+  const double wb = (double)Fb.w - 0.5, hb = (double)Fb.h - 0.5;
+  const double n[4][3] = {{Fb.fx, 0.0, Fb.cx + 0.5}, {-Fb.fx, 0.0, wb - Fb.cx},
+                          {0.0, Fb.fy, Fb.cy + 0.5}, {0.0, -Fb.fy, hb - Fb.cy}};
+  for (int k = 0; k < 4; ++k) {
+    const double d = n[k][0] * c[0] + n[k][1] * c[1] + n[k][2] * c[2];
+    const double nn = sqrt(n[k][0] * n[k][0] + n[k][1] * n[k][1] + n[k][2] * n[k][2]);
+    if (d + r * nn < 0.0) return 0;
+  }
+  return 1;
+}
+
 template <bool STD, bool PREV>
 __global__ void __launch_bounds__(DENSE_THREADS, 2) k_dense_fused(DenseArgs a) {
   __shared__ FusedCtx ec;
@@ -289,28 +312,54 @@ __global__ void __launch_bounds__(DENSE_THREADS, 2) k_dense_fused(DenseArgs a) {
   const double wm1 = (double)(Fj.w - 1), hm1 = (double)(Fj.h - 1);
   const double dwj = (double)Fj.w, dhj = (double)Fj.h;
 
+  // Tile culling: a 16x16 source tile whose bounding sphere lies outside
+  // the target frustum widened to the geo rounding bounds [-0.5, w-0.5]
+  // cannot associate any pixel (photo bounds [0, w-1] are inside that), so
+  // its pixels skip the association entirely - decisions are unchanged.
+  // tile_state bit0: may be visible now; bit1: the previous pass froze an
+  // association in it; bit2 (set below): this pass freezes one.  Slots of a
+  // tile whose bit2 ends up clear are never read (the flag says so).
+  __shared__ unsigned char tile_state[DENSE_MAX_TILES];
+  const int toff = (int)(a.geo_off[it.x] >> 8);  // this edge's first tile flag
+  for (int t = it.y + threadIdx.x; t < it.z; t += blockDim.x) {
+    unsigned char s = tile_maybe_visible(ec.rel, Fi.tiles[t], Fj);
+    if (PREV && a.tile_any_prev[toff + t]) s |= 2;
+    tile_state[t - it.y] = s;
+  }
+  __syncthreads();
+
   double acc[29];
 #pragma unroll
   for (int k = 0; k < 29; ++k) acc[k] = 0.0;
   double eprev_p = 0.0, eprev_g = 0.0;
 
-  for (int base = it.y; base < it.z; base += DENSE_THREADS) {
-    const int p = base + threadIdx.x;
-    const bool live = p < it.z;
+  // pixels in tile-major order: slot m = tile * 256 + threadIdx.x (the frozen
+  // association buffers use the same slots; a warp covers 16x2 pixels)
+  int tx = it.y % Fi.tiles_x, ty = it.y / Fi.tiles_x;
+  for (int t = it.y; t < it.z; ++t, (++tx == Fi.tiles_x ? (tx = 0, ++ty) : 0)) {
+    const unsigned st = tile_state[t - it.y];
+    if (!(st & 3u)) continue;  // nothing to associate, nothing frozen
+    const bool vis = st & 1u;
+    const bool prev_here = PREV && (st & 2u);
+    const int x = tx * SFB_TILE + (threadIdx.x & (SFB_TILE - 1));
+    const int y = ty * SFB_TILE + (threadIdx.x / SFB_TILE);
+    const bool live = x < Fi.w && y < Fi.h;
+    const int p = y * Fi.w + x;           // pixel
+    const int m = t * 256 + threadIdx.x;  // slot
     float4 P = make_float4(0.f, 0.f, 0.f, 0.f);
     unsigned fl = 0;
     if (live) {
       P = __ldg(&Fi.P[p]);
       fl = __float_as_uint(P.w);
     }
-    const bool sok = live && stride_ok(p, Fi.w, a.stride);
+    const bool sok = vis && live && stride_ok(p, Fi.w, a.stride);
     const bool ph = a.do_photo && sok && (fl & SFB_FLAG_VD);
     const bool ge = a.do_geo && sok && (fl & SFB_FLAG_VD) && (fl & SFB_FLAG_VN);
     bool pph = false;
     int ptg = 0xFFFF;
-    if (PREV && live) {
-      if (a.prev_photo) pph = (pmask_prev[p >> 5] >> (p & 31)) & 1u;
-      if (a.prev_geo) ptg = gtgt_prev[p];
+    if (prev_here && live) {
+      if (a.prev_photo) pph = (pmask_prev[m >> 5] >> (m & 31)) & 1u;
+      if (a.prev_geo) ptg = gtgt_prev[m];
     }
     bool ph_in = false;
     int tgt = -1;
@@ -337,12 +386,17 @@ __global__ void __launch_bounds__(DENSE_THREADS, 2) k_dense_fused(DenseArgs a) {
       ua = fma(tu, rz, Fj.cx);
       va = fma(tv, rz, Fj.cy);
       if (ph) {
-        double u = ua, v = va;
-        if (near_val(ua, 0.0) || near_val(ua, wm1) || near_val(va, 0.0) || near_val(va, hm1)) {
-          u = __dadd_rn(__ddiv_rn(tu, z), Fj.cx);
-          v = __dadd_rn(__ddiv_rn(tv, z), Fj.cy);
+        // decide with a 1e-6 px guard band; exact IEEE quotient only inside it
+        const double E = 1e-6;
+        const bool in_c = ua > E && ua < wm1 - E && va > E && va < hm1 - E;
+        const bool out_c = ua < -E || ua > wm1 + E || va < -E || va > hm1 + E;
+        if (in_c | out_c) {
+          ph_in = front && in_c;
+        } else {
+          const double u = __dadd_rn(__ddiv_rn(tu, z), Fj.cx);
+          const double v = __dadd_rn(__ddiv_rn(tv, z), Fj.cy);
+          ph_in = front && u >= 0.0 && u <= wm1 && v >= 0.0 && v <= hm1;
         }
-        ph_in = front && u >= 0.0 && u <= wm1 && v >= 0.0 && v <= hm1;
       }
       if (ge) {
         double u = ua, v = va;
@@ -353,12 +407,17 @@ __global__ void __launch_bounds__(DENSE_THREADS, 2) k_dense_fused(DenseArgs a) {
         }
         const bool fr = q2 > 0.0;
         const double zz = fr ? q2 : 1.0;
-        if (fabs(u) < 1e9 && fabs(v) < 1e9 && (near_half(u) || near_half(v) || (ph && ord_ge != ord_ph))) {
+        const bool finite_uv = fabs(u) < 1e9 && fabs(v) < 1e9;
+        double xr = finite_uv ? rint_magic(u) : 0.0, yr = finite_uv ? rint_magic(v) : 0.0;
+        // np.round ties: recompute the exact quotient when within 1e-6 px of a .5
+        if (finite_uv && (fabs(u - xr) > 0.5 - 1e-6 || fabs(v - yr) > 0.5 - 1e-6 ||
+                          (ph && ord_ge != ord_ph))) {
           u = __dadd_rn(__ddiv_rn(__dmul_rn(Fj.fx, q0), zz), Fj.cx);
           v = __dadd_rn(__ddiv_rn(__dmul_rn(Fj.fy, q1), zz), Fj.cy);
+          xr = rint_magic(u);
+          yr = rint_magic(v);
         }
-        if (fr && fabs(u) < 1e9 && fabs(v) < 1e9) {
-          const double xr = rint_magic(u), yr = rint_magic(v);
+        if (fr && finite_uv) {
           if (xr >= 0.0 && xr < dwj && yr >= 0.0 && yr < dhj) {
             const int ti = __double2loint(__dadd_rn(yr, 6755399441055744.0)) * Fj.w +
                            __double2loint(__dadd_rn(xr, 6755399441055744.0));
@@ -398,9 +457,10 @@ __global__ void __launch_bounds__(DENSE_THREADS, 2) k_dense_fused(DenseArgs a) {
     }
     if (a.do_photo) {
       const unsigned word = __ballot_sync(0xffffffffu, ph_in);
-      if (lane == 0 && base + (threadIdx.x & ~31) < it.z) pmask[(p - lane) >> 5] = word;
+      if (lane == 0) pmask[m >> 5] = word;
     }
-    if (a.do_geo && live) gtgt[p] = tgt >= 0 ? (uint16_t)tgt : (uint16_t)0xFFFF;
+    if (a.do_geo) gtgt[m] = tgt >= 0 ? (uint16_t)tgt : (uint16_t)0xFFFF;
+    if (__ballot_sync(0xffffffffu, ph_in || tgt >= 0) && lane == 0) tile_state[t - it.y] |= 4u;
 
     // ---- photometric: one bilinear sample serves the frozen energy and J
     if (ph_in || pph) {
@@ -479,6 +539,9 @@ __global__ void __launch_bounds__(DENSE_THREADS, 2) k_dense_fused(DenseArgs a) {
     block_reduce_store<29>(acc, out);
     if (threadIdx.x == 0) { out[29] = 0.0; out[30] = 0.0; }
   }
+  // (block_reduce_store synchronised the CTA: tile_state bit2 is final)
+  for (int t = it.y + threadIdx.x; t < it.z; t += blockDim.x)
+    a.tile_any[toff + t] = (tile_state[t - it.y] & 4u) ? 1 : 0;
 }
 
 void launch_dense_linearize(const DenseArgs& a, cudaStream_t s) {
@@ -521,10 +584,15 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_dense_energy(DenseArgs a, dou
   const uint32_t* pmask = a.photo_mask + a.photo_off[it.x];
   const uint16_t* gtgt = a.geo_tgt + a.geo_off[it.x];
   double acc[2] = {0.0, 0.0};
-  for (int p = it.y + threadIdx.x; p < it.z; p += DENSE_THREADS) {
-    const bool ph = a.do_photo && ((pmask[p >> 5] >> (p & 31)) & 1u);
-    const int tg = a.do_geo ? (int)gtgt[p] : 0xFFFF;
+  const int toff = (int)(a.geo_off[it.x] >> 8);
+  for (int t = it.y; t < it.z; ++t) {  // tile-major slots, as k_dense_fused
+    if (!a.tile_any[toff + t]) continue;  // nothing frozen in this tile
+    const int m = t * 256 + threadIdx.x;
+    const bool ph = a.do_photo && ((pmask[m >> 5] >> (m & 31)) & 1u);
+    const int tg = a.do_geo ? (int)gtgt[m] : 0xFFFF;
     if (!ph && tg == 0xFFFF) continue;
+    const int p = ((t / Fi.tiles_x) * SFB_TILE + (threadIdx.x / SFB_TILE)) * Fi.w +
+                  (t % Fi.tiles_x) * SFB_TILE + (threadIdx.x & (SFB_TILE - 1));
     const float4 P = __ldg(&Fi.P[p]);
     if (ph) {
       double q[3];

@@ -43,6 +43,8 @@ struct DenseArgs {
   const uint32_t* photo_mask_prev;  // previous linearisation's frozen sets (fused
   const uint16_t* geo_tgt_prev;     // energy-after), or null
   int prev_photo, prev_geo;         // which frozen terms the previous pass produced
+  uint8_t* tile_any;                // per (edge, source tile): any frozen association
+  const uint8_t* tile_any_prev;
   double* item_out;         // SFB_ITEM_STRIDE per item
   Rounding rd;
   double s_photo, s_geo;
