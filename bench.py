@@ -411,7 +411,8 @@ def main():
             t = torch.tensor([ev], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ev = float(t.item())
-        e2e = {"value": ev, "unit": "ms", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+        e2e = {"value": ev, "unit": "ms", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "steps_ms": [round(v, 2) for v in e2e_t]}
 
     if rank != 0:
         if world > 1:

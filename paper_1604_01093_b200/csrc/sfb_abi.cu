@@ -5,10 +5,13 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <atomic>
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -93,22 +96,95 @@ struct Handle {
   std::string err;
 };
 
+bool trace_on() {
+  static const bool on = getenv("SFB_TRACE") != nullptr;
+  return on;
+}
+
+// Process-wide cache of idle device allocations (per device, keyed by size).
+// Blocks enter it only from DBuf::release(), which callers invoke after the
+// owning stream has been synchronised, so a cached block is never in flight.
+struct DevCache {
+  std::mutex mu;
+  std::map<std::pair<int, size_t>, std::vector<void*>> free;
+  size_t bytes = 0;
+  static constexpr size_t kLimit = (size_t)8 << 30;
+  static size_t round(size_t b) {
+    if (b <= 4096) return 4096;
+    size_t r = 4096;
+    while (r < b && r < ((size_t)1 << 26)) r <<= 1;  // powers of two up to 64 MiB
+    return r < b ? ((b + ((size_t)2 << 20) - 1) & ~(((size_t)2 << 20) - 1)) : r;
+  }
+  cudaError_t alloc(void** p, size_t b) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const size_t rb = round(b);
+    {
+      std::lock_guard<std::mutex> g(mu);
+      auto it = free.find({dev, rb});
+      if (it != free.end() && !it->second.empty()) {
+        *p = it->second.back();
+        it->second.pop_back();
+        bytes -= rb;
+        return cudaSuccess;
+      }
+    }
+    return cudaMalloc(p, rb);
+  }
+  void release(void* p, size_t b) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const size_t rb = round(b);
+    std::lock_guard<std::mutex> g(mu);
+    if (bytes + rb > kLimit) {
+      cudaFree(p);
+      return;
+    }
+    free[{dev, rb}].push_back(p);
+    bytes += rb;
+  }
+};
+DevCache& dev_cache() {
+  static DevCache* c = new DevCache();  // leaked on purpose: outlives static teardown
+  return *c;
+}
+
+// Pinned 64-double scalar mirrors for problem handles, recycled (a fresh
+// cudaMallocHost costs milliseconds).
+std::mutex g_pin_mu;
+std::vector<double*> g_pin_free;
+cudaError_t pinned_scalars(double** out) {
+  {
+    std::lock_guard<std::mutex> g(g_pin_mu);
+    if (!g_pin_free.empty()) {
+      *out = g_pin_free.back();
+      g_pin_free.pop_back();
+      return cudaSuccess;
+    }
+  }
+  return cudaMallocHost(reinterpret_cast<void**>(out), 64 * sizeof(double));
+}
+void pinned_scalars_release(double* p) {
+  std::lock_guard<std::mutex> g(g_pin_mu);
+  g_pin_free.push_back(p);
+}
+
 template <class T>
 struct DBuf {
   T* p = nullptr;
   size_t n = 0;
   cudaError_t ensure(size_t want) {
     if (want <= n && p) return cudaSuccess;
-    if (p) cudaFree(p);
+    if (p) cudaFree(p);  // growth: the old block may still be in flight -> not cached
     p = nullptr;
     n = 0;
-    size_t bytes = std::max<size_t>(want, 1) * sizeof(T);
-    cudaError_t e = cudaMalloc(&p, bytes);
-    if (e == cudaSuccess) n = std::max<size_t>(want, 1);
+    const size_t cnt = std::max<size_t>(want, 1);
+    cudaError_t e = dev_cache().alloc(reinterpret_cast<void**>(&p), cnt * sizeof(T));
+    if (e == cudaSuccess) n = cnt;
     return e;
   }
-  void release() {
-    if (p) cudaFree(p);
+  void release() {  // caller has synchronised the stream that used the buffer
+    if (p) dev_cache().release(p, n * sizeof(T));
     p = nullptr;
     n = 0;
   }
@@ -131,6 +207,11 @@ struct sfb_ctx : Handle {
   std::map<void*, int> block_refs;
   DBuf<uint8_t> staging;
   DBuf<int> counts;
+  DBuf<PackArgs> pack_args;
+  std::map<void*, size_t> block_size;
+  std::multimap<size_t, void*> free_blocks;  // released frame blocks kept for reuse
+  size_t cached_bytes = 0;
+  size_t cache_limit = (size_t)16 << 30;
 };
 
 struct sfb_problem : Handle {
@@ -262,6 +343,7 @@ cudaError_t upload_vec(DBuf<T>& d, const std::vector<T>& h, cudaStream_t s) {
 
 // Which frame pairs couple, the contribution lists, the dense work items.
 int rebuild_structure(sfb_problem* p, int bidir) {
+  const auto t_start = std::chrono::steady_clock::now();
   const int nb = p->n_blk;
   // directed dense edges (solver.py:151-155)
   std::vector<int2> dir(p->edges.begin(), p->edges.end());
@@ -377,6 +459,7 @@ int rebuild_structure(sfb_problem* p, int bidir) {
   std::vector<int>& rent = pslot;
 
   cudaStream_t s = p->stream;
+  const auto t_host = std::chrono::steady_clock::now();
   CK(p, upload_vec(p->dir_edges, dir, s));
   CK(p, upload_vec(p->items, items, s));
   CK(p, upload_vec(p->edge_item_ptr, eptr, s));
@@ -401,6 +484,12 @@ int rebuild_structure(sfb_problem* p, int bidir) {
   CK(p, p->B.ensure((size_t)std::max(1, p->n_pairs) * 36));
   CK(p, p->Brow.ensure((size_t)std::max(1, rptr[nb]) * 36));
   CK(p, cudaStreamSynchronize(s));  // host vectors die here
+  if (trace_on()) {
+    const auto t_end = std::chrono::steady_clock::now();
+    fprintf(stderr, "sfb rebuild_structure: host %.2f ms, alloc+upload %.2f ms (%d dir edges, %d pairs)\n",
+            std::chrono::duration<double, std::milli>(t_host - t_start).count(),
+            std::chrono::duration<double, std::milli>(t_end - t_host).count(), p->n_dir, p->n_pairs);
+  }
   p->struct_bidir = bidir;
   p->have_system = false;
   p->dense_active = false;
@@ -607,6 +696,8 @@ int sfb_ctx_destroy(sfb_ctx* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   for (auto& kv : c->block_refs) cudaFree(kv.first);
+  for (auto& kv : c->free_blocks) cudaFree(kv.second);
+  c->pack_args.release();
   c->staging.release();
   c->counts.release();
   cudaStreamDestroy(c->stream);
@@ -640,14 +731,36 @@ int sfb_frames_upload(sfb_ctx* c, int32_t n, const sfb_frame_desc* d, int32_t* s
              align256(nt * 4);
     stage += align256(hw * 2) + align256(hw * 24) + align256(hw * 8);
   }
+  // frame blocks come from a per-context cache (released blocks are kept for
+  // reuse, like a caching allocator): no cudaMalloc/cudaFree on the hot path
   void* block = nullptr;
-  CK(c, cudaMalloc(&block, total));
+  size_t block_bytes = 0;
+  {
+    auto it = c->free_blocks.lower_bound(total);
+    if (it != c->free_blocks.end() && it->first <= 2 * total + (64u << 20)) {
+      block = it->second;
+      block_bytes = it->first;
+      c->cached_bytes -= it->first;
+      c->free_blocks.erase(it);
+    } else {
+      CK(c, cudaMalloc(&block, total));
+      block_bytes = total;
+    }
+  }
   CK(c, c->staging.ensure(stage));
   CK(c, c->counts.ensure(3 * (size_t)n));
+  CK(c, c->pack_args.ensure((size_t)n));
   CK(c, cudaMemsetAsync(c->counts.p, 0, sizeof(int) * 3 * n, c->stream));
   char* dst = static_cast<char*>(block);
   char* stg = reinterpret_cast<char*>(c->staging.p);
   std::vector<FrameDev> devs(n);
+  std::vector<PackArgs> pargs(n);
+  std::vector<void*> cdst, csrc;
+  std::vector<size_t> csz;
+  cdst.reserve(5 * (size_t)n);
+  csrc.reserve(5 * (size_t)n);
+  csz.reserve(5 * (size_t)n);
+  int max_hw = 0, max_nt = 0;
   for (int k = 0; k < n; ++k) {
     const int w = d[k].width, h = d[k].height;
     const size_t hw = (size_t)w * h;
@@ -671,28 +784,68 @@ int sfb_frames_upload(sfb_ctx* c, int32_t n, const sfb_frame_desc* d, int32_t* s
     stg += align256(hw * 24);
     float* sgr = reinterpret_cast<float*>(stg);
     stg += align256(hw * 8);
-    CK(c, cudaMemcpyAsync(svd, d[k].valid_depth, hw, cudaMemcpyHostToDevice, c->stream));
-    CK(c, cudaMemcpyAsync(svn, d[k].valid_normal, hw, cudaMemcpyHostToDevice, c->stream));
-    CK(c, cudaMemcpyAsync(spt, d[k].points, hw * 12, cudaMemcpyHostToDevice, c->stream));
-    CK(c, cudaMemcpyAsync(snr, d[k].normals, hw * 12, cudaMemcpyHostToDevice, c->stream));
-    CK(c, cudaMemcpyAsync(sgr, d[k].grad, hw * 8, cudaMemcpyHostToDevice, c->stream));
-    PackArgs pa{svd, svn, spt, snr, sgr, const_cast<float4*>(f.P), const_cast<float4*>(f.N),
-                const_cast<float2*>(f.G), const_cast<float4*>(f.T), w, h, c->counts.p + 3 * k};
-    launch_pack(pa, c->stream);
-    launch_tiles(f.P, w, h, f.tiles_x, f.tiles_y, const_cast<double4*>(f.tiles),
-                 const_cast<int*>(f.tile_count), c->stream);
-    CKL(c);
+    const void* srcs[5] = {d[k].valid_depth, d[k].valid_normal, d[k].points, d[k].normals, d[k].grad};
+    void* dsts[5] = {svd, svn, spt, snr, sgr};
+    const size_t szs[5] = {hw, hw, hw * 12, hw * 12, hw * 8};
+    const void* use[5];
+    for (int q = 0; q < 5; ++q) {
+      // page-locked host planes are read by the pack kernel in place (UVA
+      // zero-copy over the host link); pageable ones are staged by DMA
+      cudaPointerAttributes at{};
+      if (cudaPointerGetAttributes(&at, srcs[q]) == cudaSuccess && at.type == cudaMemoryTypeHost &&
+          at.devicePointer != nullptr) {
+        use[q] = at.devicePointer;
+        continue;
+      }
+      cudaGetLastError();
+      cdst.push_back(dsts[q]);
+      csrc.push_back(const_cast<void*>(srcs[q]));
+      csz.push_back(szs[q]);
+      use[q] = dsts[q];
+    }
+    svd = (uint8_t*)use[0];
+    svn = (uint8_t*)use[1];
+    spt = (float*)use[2];
+    snr = (float*)use[3];
+    sgr = (float*)use[4];
+    pargs[k] = PackArgs{svd, svn, spt, snr, sgr, const_cast<float4*>(f.P), const_cast<float4*>(f.N),
+                        const_cast<float2*>(f.G), const_cast<float4*>(f.T), w, h,
+                        c->counts.p + 3 * k, f.tiles_x, f.tiles_y, const_cast<double4*>(f.tiles),
+                        const_cast<int*>(f.tile_count)};
+    max_hw = std::max(max_hw, (int)hw);
+    max_nt = std::max(max_nt, (int)nt);
     devs[k] = f;
   }
+  // one batched H2D for every plane of every frame (CUDA >= 12.8), else a loop
+  bool batched = cdst.empty();
+#if CUDART_VERSION >= 12080
+  if (!batched) {
+    cudaMemcpyAttributes attr{};
+    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+    size_t idx0 = 0, fail_idx = 0;
+    batched = cudaMemcpyBatchAsync(cdst.data(), csrc.data(), csz.data(), cdst.size(), &attr,
+                                   &idx0, 1, &fail_idx, c->stream) == cudaSuccess;
+    if (!batched) cudaGetLastError();
+  }
+#endif
+  if (!batched)
+    for (size_t q = 0; q < cdst.size(); ++q)
+      CK(c, cudaMemcpyAsync(cdst[q], csrc[q], csz[q], cudaMemcpyHostToDevice, c->stream));
+  CK(c, cudaMemcpyAsync(c->pack_args.p, pargs.data(), sizeof(PackArgs) * n, cudaMemcpyHostToDevice,
+                        c->stream));
+  launch_pack_batch(c->pack_args.p, n, max_hw, max_nt, c->stream);
+  CKL(c);
   std::vector<int> cnt(3 * n);
   CK(c, cudaMemcpyAsync(cnt.data(), c->counts.p, sizeof(int) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
   CK(c, cudaStreamSynchronize(c->stream));
   for (int k = 0; k < n; ++k)
     if (cnt[3 * k + 2] != 0) {
-      cudaFree(block);
+      c->free_blocks.emplace(block_bytes, block);
+      c->cached_bytes += block_bytes;
       return fail(c, SFB_E_ARG, "cache planes contain non-finite values (frame " + std::to_string(k) + ")");
     }
   c->block_refs[block] = n;
+  c->block_size[block] = block_bytes;
   int search = 0;
   for (int k = 0; k < n; ++k) {
     devs[k].n_valid_depth = cnt[3 * k];
@@ -718,9 +871,20 @@ int sfb_frames_release(sfb_ctx* c, int32_t n, const int32_t* slots) {
     sl.alive = false;
     auto it = c->block_refs.find(sl.block);
     if (it != c->block_refs.end() && --it->second == 0) {
-      cudaDeviceSynchronize();
-      cudaFree(it->first);
+      // keep the block for reuse; problems still referencing it were
+      // required to be destroyed first (frames are read-only while in use)
+      const size_t bytes = c->block_size[it->first];
+      c->free_blocks.emplace(bytes, it->first);
+      c->cached_bytes += bytes;
+      c->block_size.erase(it->first);
       c->block_refs.erase(it);
+      while (c->cached_bytes > c->cache_limit && !c->free_blocks.empty()) {
+        auto big = std::prev(c->free_blocks.end());
+        cudaDeviceSynchronize();
+        cudaFree(big->second);
+        c->cached_bytes -= big->first;
+        c->free_blocks.erase(big);
+      }
     }
     sl.block = nullptr;
   }
@@ -795,7 +959,7 @@ int sfb_problem_create(sfb_ctx* c, int32_t n_frames, const int32_t* slots, int32
       p->pv2.ensure(nv) || p->tmp.ensure(2 * nv) ||
       p->part.ensure(4 * 1024) || p->flags.ensure(64) || p->dscal.ensure(64))
     return bail(SFB_E_OOM, "vectors");
-  if (cudaMallocHost(&p->hscal, 64 * sizeof(double)) != cudaSuccess) return bail(SFB_E_OOM, "pinned");
+  if (pinned_scalars(&p->hscal) != cudaSuccess) return bail(SFB_E_OOM, "pinned");
   int rc = rebuild_structure(p, 0);
   if (rc) {
     std::string m = p->err;
@@ -840,7 +1004,7 @@ int sfb_problem_destroy(sfb_problem* p) {
   p->f_pass.release();
   p->f_temp.release();
   p->f_cnt.release();
-  if (p->hscal) cudaFreeHost(p->hscal);
+  if (p->hscal) pinned_scalars_release(p->hscal);
   if (p->stream) cudaStreamDestroy(p->stream);
   delete p;
   return SFB_OK;
@@ -897,6 +1061,7 @@ int sfb_build_dense_edges(sfb_problem* p, double cos_min, int64_t* n_out) {
   if (!p || !n_out) return fail(p, SFB_E_ARG, "null argument");
   if (!p->has_frames) return fail(p, SFB_E_STATE, "problem has no frames (caches=None)");
   CK(p, cudaSetDevice(p->ctx->device));
+  const auto t0 = std::chrono::steady_clock::now();
   cudaStream_t s = p->stream;
   const int n = p->n;
   const int64_t P = (int64_t)n * (n - 1) / 2;
@@ -949,6 +1114,10 @@ int sfb_build_dense_edges(sfb_problem* p, double cos_min, int64_t* n_out) {
     }
   }
   *n_out = (int64_t)p->edges.size();
+  if (trace_on())
+    fprintf(stderr, "sfb pair filter: %.2f ms (%d frames, %lld edges)\n",
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(),
+            n, (long long)*n_out);
   return rebuild_structure(p, p->struct_bidir < 0 ? 0 : p->struct_bidir);
 }
 

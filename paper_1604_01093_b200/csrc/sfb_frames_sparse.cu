@@ -360,3 +360,103 @@ void launch_tiles(const float4* P, int w, int h, int tx, int ty, double4* tiles,
   sfb_count_launch();
   k_tiles<<<(n * 32 + 255) / 256, 256, 0, s>>>(P, w, h, tx, ty, tiles, counts);
 }
+
+// Batched upload: blockIdx.y selects the frame.
+__global__ void k_pack_batch(const PackArgs* args) {
+  const PackArgs& a0 = args[blockIdx.y];
+  PackArgs a = a0;
+  // reuse the single-frame body through a grid-stride loop over this frame
+  const int hw = a.w * a.h;
+  int cnt_vd = 0, cnt_geo = 0, bad = 0;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < hw; p += gridDim.x * blockDim.x) {
+    const unsigned vd = a.vd[p] ? 1u : 0u;
+    const unsigned vn = a.vn[p] ? 1u : 0u;
+    a.P[p] = make_float4(a.pts[3 * p], a.pts[3 * p + 1], a.pts[3 * p + 2],
+                         __uint_as_float(vd * SFB_FLAG_VD | vn * SFB_FLAG_VN));
+    a.N[p] = make_float4(a.nrm[3 * p], a.nrm[3 * p + 1], a.nrm[3 * p + 2], 0.f);
+    const float2 g = make_float2(a.grad[2 * p], a.grad[2 * p + 1]);
+    a.G[p] = g;
+    const int y = p / a.w, x = p - y * a.w;
+    float4 t0 = make_float4(0.f, 0.f, 0.f, 0.f), t1 = t0;
+    if (x + 1 < a.w && y + 1 < a.h) {
+      const int q = p + 1, r = p + a.w, s = p + a.w + 1;
+      t0 = make_float4(g.x, g.y, a.grad[2 * q], a.grad[2 * q + 1]);
+      t1 = make_float4(a.grad[2 * r], a.grad[2 * r + 1], a.grad[2 * s], a.grad[2 * s + 1]);
+    }
+    a.T[2 * p] = t0;
+    a.T[2 * p + 1] = t1;
+    cnt_vd += (int)vd;
+    cnt_geo += (int)(vd & vn);
+    const bool fin = isfinite(a.pts[3 * p]) && isfinite(a.pts[3 * p + 1]) && isfinite(a.pts[3 * p + 2]) &&
+                     isfinite(a.nrm[3 * p]) && isfinite(a.nrm[3 * p + 1]) && isfinite(a.nrm[3 * p + 2]) &&
+                     isfinite(g.x) && isfinite(g.y);
+    bad += fin ? 0 : 1;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    cnt_vd += __shfl_xor_sync(0xffffffffu, cnt_vd, o);
+    cnt_geo += __shfl_xor_sync(0xffffffffu, cnt_geo, o);
+    bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&a.counts[0], cnt_vd);
+    atomicAdd(&a.counts[1], cnt_geo);
+    if (bad) atomicAdd(&a.counts[2], bad);
+  }
+}
+
+__global__ void k_tiles_batch(const PackArgs* args) {
+  const PackArgs& a = args[blockIdx.y];
+  const int nt = a.tiles_x * a.tiles_y;
+  const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int tile = w0; tile < nt; tile += nwarps) {
+    const int x0 = (tile % a.tiles_x) * SFB_TILE, y0 = (tile / a.tiles_x) * SFB_TILE;
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    int c = 0;
+    for (int k = lane; k < SFB_TILE * SFB_TILE; k += 32) {
+      const int x = x0 + (k % SFB_TILE), y = y0 + (k / SFB_TILE);
+      if (x >= a.w || y >= a.h) continue;
+      const float4 p = a.P[y * a.w + x];
+      if (!(__float_as_uint(p.w) & SFB_FLAG_VD)) continue;
+      const double q[3] = {p.x, p.y, p.z};
+      for (int d = 0; d < 3; ++d) { lo[d] = fmin(lo[d], q[d]); hi[d] = fmax(hi[d], q[d]); }
+      ++c;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      c += __shfl_xor_sync(0xffffffffu, c, o);
+      for (int d = 0; d < 3; ++d) {
+        lo[d] = fmin(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], o));
+        hi[d] = fmax(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], o));
+      }
+    }
+    double ctr[3];
+    for (int d = 0; d < 3; ++d) ctr[d] = 0.5 * (lo[d] + hi[d]);
+    double r2 = 0.0;
+    for (int k = lane; k < SFB_TILE * SFB_TILE; k += 32) {
+      const int x = x0 + (k % SFB_TILE), y = y0 + (k / SFB_TILE);
+      if (x >= a.w || y >= a.h) continue;
+      const float4 p = a.P[y * a.w + x];
+      if (!(__float_as_uint(p.w) & SFB_FLAG_VD)) continue;
+      const double dx = p.x - ctr[0], dy = p.y - ctr[1], dz = p.z - ctr[2];
+      r2 = fmax(r2, dx * dx + dy * dy + dz * dz);
+    }
+    for (int o = 16; o > 0; o >>= 1) r2 = fmax(r2, __shfl_xor_sync(0xffffffffu, r2, o));
+    if (lane == 0) {
+      const double r = sqrt(r2) * (1.0 + 1e-9) + 1e-9;
+      a.tiles[tile] = c > 0 ? make_double4(ctr[0], ctr[1], ctr[2], r) : make_double4(0, 0, 0, -1.0);
+      a.tile_count[tile] = c;
+    }
+  }
+}
+
+void launch_pack_batch(const PackArgs* args_dev, int n, int max_hw, int max_tiles, cudaStream_t s) {
+  if (n <= 0) return;
+  int bx = (max_hw + 255) / 256;
+  if (bx > 64) bx = 64;
+  sfb_count_launch(2);
+  k_pack_batch<<<dim3(bx, n), 256, 0, s>>>(args_dev);
+  int tx = (max_tiles * 32 + 255) / 256;
+  if (tx < 1) tx = 1;
+  k_tiles_batch<<<dim3(tx, n), 256, 0, s>>>(args_dev);
+}

@@ -13,7 +13,10 @@ struct PackArgs {
   float2* G;
   float4* T;
   int w, h;
-  int* counts;  // [0] valid_depth, [1] valid_depth & valid_normal
+  int* counts;  // [0] valid_depth, [1] valid_depth & valid_normal, [2] non-finite
+  int tiles_x, tiles_y;
+  double4* tiles;
+  int* tile_count;
 };
 
 struct SparseArgs {
@@ -100,6 +103,8 @@ struct PcgArgs {
 void sfb_count_launch(int n = 1);
 
 void launch_pack(const PackArgs& a, cudaStream_t s);
+// every frame of an upload in two launches (planes, then tile spheres)
+void launch_pack_batch(const PackArgs* args_dev, int n, int max_hw, int max_tiles, cudaStream_t s);
 void launch_tiles(const float4* P, int w, int h, int tx, int ty, double4* tiles, int* counts,
                   cudaStream_t s);
 void launch_sparse(const SparseArgs& a, cudaStream_t s);

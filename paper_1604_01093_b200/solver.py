@@ -103,21 +103,32 @@ def build_sparse_term(corr_sets, frame_to_var) -> SparseTerm:
 def _set_layout(corr_sets, frame_index):
     """(n_sets,2) problem-frame indices, offsets and stacked points for the ABI."""
     n = len(corr_sets)
-    frames = np.zeros((n, 2), dtype=np.int32)
+    if n == 0:
+        return (np.zeros((0, 2), dtype=np.int32), np.zeros(1, dtype=np.int64), np.zeros((0, 3)),
+                np.zeros((0, 3)))
+    frames = np.fromiter((frame_index[f] for cs in corr_sets for f in (cs.frame_i, cs.frame_j)),
+                         dtype=np.int32, count=2 * n).reshape(n, 2)
+    try:  # fast path: every set holds (k,3) arrays
+        pi = [cs.points_i for cs in corr_sets]
+        pj = [cs.points_j for cs in corr_sets]
+        si = np.fromiter((len(a) for a in pi), dtype=np.int64, count=n)
+        sj = np.fromiter((len(b) for b in pj), dtype=np.int64, count=n)
+        pts_i = np.concatenate(pi).astype(np.float64, copy=False)
+        pts_j = np.concatenate(pj).astype(np.float64, copy=False)
+        ok = pts_i.shape == (int(si.sum()), 3) and pts_j.shape == (int(sj.sum()), 3)
+    except (ValueError, TypeError):
+        ok = False
+    if not ok:
+        pi = [np.asarray(cs.points_i, dtype=np.float64).reshape(-1, 3) for cs in corr_sets]
+        pj = [np.asarray(cs.points_j, dtype=np.float64).reshape(-1, 3) for cs in corr_sets]
+        si = np.fromiter((a.shape[0] for a in pi), dtype=np.int64, count=n)
+        sj = np.fromiter((b.shape[0] for b in pj), dtype=np.int64, count=n)
+        pts_i, pts_j = np.concatenate(pi), np.concatenate(pj)
+    if not np.array_equal(si, sj):
+        raise ValueError("points_i and points_j of a correspondence set differ in shape")
     off = np.zeros(n + 1, dtype=np.int64)
-    pi, pj = [], []
-    for k, cs in enumerate(corr_sets):
-        frames[k] = (frame_index[cs.frame_i], frame_index[cs.frame_j])
-        a = np.asarray(cs.points_i, dtype=np.float64).reshape(-1, 3)
-        b = np.asarray(cs.points_j, dtype=np.float64).reshape(-1, 3)
-        if a.shape != b.shape:
-            raise ValueError("points_i and points_j of a correspondence set differ in shape")
-        off[k + 1] = off[k] + a.shape[0]
-        pi.append(a)
-        pj.append(b)
-    pts_i = np.vstack(pi) if pi else np.zeros((0, 3))
-    pts_j = np.vstack(pj) if pj else np.zeros((0, 3))
-    return frames, off, pts_i, pts_j
+    np.cumsum(si, out=off[1:])
+    return frames, off, np.ascontiguousarray(pts_i), np.ascontiguousarray(pts_j)
 
 
 def _poses_from_arrays(R, t):
@@ -469,6 +480,70 @@ class GaussNewtonStats:
                    for rec in self.iterations if rec.accepted)
 
 
+class _EdgeList(list):
+    """`dense_edges` as the reference's list of (frame_i, frame_j) tuples, built
+    from the device's (n_edges, 2) index array only when first touched (the
+    solve loop itself never needs the host copy)."""
+
+    def __init__(self, pairs, frame_ids):
+        super().__init__()
+        self._pairs = pairs
+        self._ids = frame_ids
+        self.touched = False
+
+    def _fill(self):
+        if not self.touched:
+            self.touched = True
+            ids = self._ids
+            super().extend((ids[a], ids[b]) for a, b in self._pairs.tolist())
+
+    def __len__(self):
+        return len(self._pairs) if not self.touched else super().__len__()
+
+    def __bool__(self):
+        return len(self) > 0
+
+    def __iter__(self):
+        self._fill()
+        return super().__iter__()
+
+    def __getitem__(self, i):
+        self._fill()
+        return super().__getitem__(i)
+
+    def __contains__(self, x):
+        self._fill()
+        return super().__contains__(x)
+
+    def __eq__(self, other):
+        self._fill()
+        return list.__eq__(self, list(other) if not isinstance(other, list) else other)
+
+    def __ne__(self, other):
+        return not self.__eq__(other)
+
+    def __repr__(self):
+        self._fill()
+        return super().__repr__()
+
+    def __reduce__(self):
+        self._fill()
+        return (list, (list(super().__iter__()),))
+
+    for _m in ("append", "extend", "insert", "remove", "pop", "clear", "sort", "reverse",
+               "__setitem__", "__delitem__", "__iadd__", "index", "count", "copy"):
+        def _wrap(name=_m):
+            base = getattr(list, name)
+
+            def f(self, *a, **k):
+                self._fill()
+                return base(self, *a, **k)
+            f.__name__ = name
+            return f
+        locals()[_m] = _wrap()
+    del _m, _wrap
+
+
 class _LazyAssociations(list):
     """Frozen associations of the last linearisation, materialised on first access."""
 
@@ -515,11 +590,24 @@ class AlignmentProblem:
         self.caches = caches
         self.frame_to_var = {f: k - 1 for k, f in enumerate(self.frame_ids)}
         self.n_vars = 6 * (len(self.frame_ids) - 1)
-        self.sparse = build_sparse_term(self.corr_sets, self.frame_to_var)
+        for cs in self.corr_sets:  # KeyError for unknown frames, as build_sparse_term
+            self.frame_to_var[cs.frame_i], self.frame_to_var[cs.frame_j]
+        self._sparse = None
         self.dense_edges = []
         self._device = device
         self._dp = None
         self._dp_edges = None
+
+    @property
+    def sparse(self) -> SparseTerm:
+        """Stacked correspondences (solver.py:563); built on first access."""
+        if self._sparse is None:
+            self._sparse = build_sparse_term(self.corr_sets, self.frame_to_var)
+        return self._sparse
+
+    @sparse.setter
+    def sparse(self, value):
+        self._sparse = value
 
     # -- device plumbing ---------------------------------------------------
     def _problem(self) -> DeviceProblem:
@@ -540,6 +628,9 @@ class AlignmentProblem:
             self.poses[f] = RigidTransform(R[k].copy(), t[k].copy())
 
     def _sync_edges(self):
+        if (self.dense_edges is self._dp_edges and isinstance(self.dense_edges, _EdgeList)
+                and not self.dense_edges.touched):
+            return  # the device already holds exactly these edges
         edges = list(self.dense_edges)
         if edges != self._dp_edges:
             index = {f: k for k, f in enumerate(self.frame_ids)}
@@ -587,14 +678,18 @@ class AlignmentProblem:
         if self.n_vars == 0:
             stats.converged = True
             return stats
+        tr = _Tracer()
         dp = self._problem()
         self._push_poses()
+        tr.mark("setup")
         if self.caches is not None:
             pairs = dp.build_dense_edges(config.view_angle_max_deg)
-            self.dense_edges = [(self.frame_ids[a], self.frame_ids[b]) for a, b in pairs]
-            self._dp_edges = list(self.dense_edges)
+            self.dense_edges = _EdgeList(pairs, self.frame_ids)
+            self._dp_edges = self.dense_edges
         else:
             self._sync_edges()
+        have_edges = len(pairs) > 0 if self.caches is not None else bool(self.dense_edges)
+        tr.mark("filter")
         best_energy = np.inf
         dp.save_best()
         consecutive_increases = 0
@@ -604,7 +699,8 @@ class AlignmentProblem:
             w_dense = dense_ramp_weight(weights, it)
             e = e_next if e_next is not None else dp.linearize(weights, w_dense, config)
             e_next = None
-            dense_on = self.caches is not None and w_dense > 0.0 and bool(self.dense_edges)
+            tr.mark("lin")
+            dense_on = self.caches is not None and w_dense > 0.0 and have_edges
             energy_before = weights.sparse * float(e[0])
             if dense_on:
                 energy_before += w_dense * (weights.photo * float(e[1]) + weights.geo * float(e[2]))
@@ -618,8 +714,10 @@ class AlignmentProblem:
             if status == _abi.SFB_E_PCG_NONFINITE:
                 stats.aborted = True
                 break
+            tr.mark("pcg")
             step_norm = dp.apply_step()
             moved = True
+            tr.mark("step")
             if it + 1 < max_iterations:
                 # E_after(it) and the linearisation of it+1 happen at the same
                 # poses: one fused device pass (discarded if the loop stops).
@@ -627,6 +725,7 @@ class AlignmentProblem:
                     weights, w_dense > 0.0, dense_ramp_weight(weights, it + 1), config)
             else:
                 ea = dp.energy_frozen(w_dense > 0.0)
+            tr.mark("energy+lin")
             energy_after = weights.sparse * float(ea[0])
             if w_dense > 0.0:
                 energy_after += w_dense * (weights.photo * float(ea[1]) + weights.geo * float(ea[2]))
@@ -652,7 +751,34 @@ class AlignmentProblem:
             stats.converged = True
         if moved:
             self._pull_poses()
+        tr.mark("pull")
+        tr.report()
         return stats
+
+
+class _Tracer:
+    """Host wall-time per solve phase, printed to stderr when SFB_TRACE is set."""
+
+    def __init__(self):
+        import os
+        self.on = bool(os.environ.get("SFB_TRACE"))
+        if self.on:
+            import time
+            self._clock = time.perf_counter
+            self.t = self._clock()
+            self.acc = {}
+
+    def mark(self, label):
+        if self.on:
+            now = self._clock()
+            self.acc[label] = self.acc.get(label, 0.0) + (now - self.t)
+            self.t = now
+
+    def report(self):
+        if self.on:
+            import sys
+            print("sfb trace ms: " + " ".join(f"{k}={1e3 * v:.1f}" for k, v in self.acc.items()),
+                  file=sys.stderr, flush=True)
 
 
 # ---------------------------------------------------------------------------
