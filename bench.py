@@ -193,6 +193,10 @@ def _time_pairs(args):
     return time.perf_counter() - t0, passed
 
 
+def _noop(_):
+    return 0
+
+
 _SCENES = {}
 
 
@@ -230,21 +234,28 @@ def cpu_extrapolate(scene_name, edges_undirected, records, workers: int, pair_sa
     pick = rng.choice(len(edge_pool), size=min(edge_sample, len(edge_pool)), replace=False)
     sample_edges = [edge_pool[k] for k in pick]
 
+    pool = None
+    if workers > 1:
+        import multiprocessing as mp
+        pool = mp.get_context("fork").Pool(workers)  # forked with the scene loaded
+        pool.map(_noop, range(workers))               # workers up before timing
+
     def run(fn, items):
         chunks = [items[k::workers] for k in range(workers)]
         chunks = [c for c in chunks if c]
         t0 = time.perf_counter()
-        if workers == 1:
+        if pool is None:
             outs = [fn((scene_name, chunks[0]))]
         else:
-            import multiprocessing as mp
-            with mp.get_context("fork").Pool(len(chunks)) as pool:
-                outs = pool.map(fn, [(scene_name, c) for c in chunks])
+            outs = pool.map(fn, [(scene_name, c) for c in chunks])
         return time.perf_counter() - t0, outs
 
     wall_p, outs_p = run(_time_pairs, pairs)
     passed = sum(o[1] for o in outs_p)
     wall_e, _ = run(_time_edges, sample_edges)
+    if pool is not None:
+        pool.close()
+        pool.join()
     per_pair = wall_p / len(pairs)
     per_edge = wall_e / len(sample_edges)
     E_u = len(edges_undirected) if edges_undirected else int(round(P * passed / max(1, len(pairs))))
@@ -285,8 +296,9 @@ def run_reference(args, rank):
     scene = _scene_cache(args.config)
     vals = []
     for k in range(args.warmup + args.steps):
-        ms, sample, _ = cpu_extrapolate(args.config, None, None, workers, pair_sample=800,
-                                        edge_sample=4 * workers, seed=k)
+        ms, sample, _ = cpu_extrapolate(args.config, None, None, workers,
+                                        pair_sample=120 * workers, edge_sample=12 * workers,
+                                        seed=k)
         if k >= args.warmup:
             vals.append(ms)
     v = float(np.median(vals))
@@ -421,7 +433,8 @@ def main():
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         edges = [(a, b) for (a, b) in problem.dense_edges]
-        cms, sample, spent = cpu_extrapolate(args.config, edges, records, 1)
+        cms, sample, spent = cpu_extrapolate(args.config, edges, records, 1, pair_sample=2000,
+                                             edge_sample=160)
         cpu = {"value": cms, "unit": "ms", "cores": 1, "kind": "port", "sample": sample,
                "sample_seconds": round(spent, 1)}
     line = {
