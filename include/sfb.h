@@ -208,6 +208,31 @@ int sfb_point_eval(sfb_problem* p, int32_t frame_i, int32_t frame_j,
                    const double* aux, const double* targets, double* res,
                    double* jac);
 
+/* ---- data-parallel sharding over frame pairs -----
+ * A problem replicated on world ranks (one process per GPU) owns every
+ * world-th directed dense edge and every world-th filter candidate.  The
+ * two-phase calls below bracket the one collective of each step: after a
+ * _begin, the caller sums the indicated exchange buffers across ranks
+ * (bit 0: which=0 per-edge linearisation sums, 32 f64 per directed edge;
+ * bit 1: which=1 per-edge frozen energies, 2 f64 per directed edge; the
+ * filter always exchanges which=2, one u8 pass flag per candidate).  Every
+ * entry has exactly one owner, so the sums are exact and every rank ends
+ * with bit-identical systems; the PCG then runs replicated.
+ * The single-call forms above return SFB_E_STATE on a sharded problem. */
+int sfb_set_shard(sfb_problem* p, int32_t rank, int32_t world);
+int sfb_exchange_buffer(sfb_problem* p, int32_t which, void** dev_ptr, int64_t* bytes);
+int sfb_build_dense_edges_begin(sfb_problem* p, double view_cos_min);
+int sfb_build_dense_edges_end(sfb_problem* p, int64_t* n_edges);
+int sfb_linearize_begin(sfb_problem* p, const sfb_weights* w, double w_dense,
+                        const sfb_config* cfg, int32_t* exchange);
+int sfb_linearize_end(sfb_problem* p, double energies_out[3]);
+int sfb_energy_and_linearize_begin(sfb_problem* p, const sfb_weights* w, int32_t prev_dense,
+                                   double w_dense_next, const sfb_config* cfg,
+                                   int32_t* exchange);
+int sfb_energy_and_linearize_end(sfb_problem* p, double out6[6]);
+int sfb_energy_frozen_begin(sfb_problem* p, int32_t dense, int32_t* exchange);
+int sfb_energy_frozen_end(sfb_problem* p, double energies_out[3]);
+
 /* ---- measurement (bench.py) -------------------------------------------
  * Per-kernel-class device time measured with CUDA events on the problem's
  * stream.  Classes: 0 dense linearize, 1 frozen energy, 2 PCG, 3 pair filter,

@@ -108,6 +108,17 @@ SIGNATURES = {
     "sfb_associate": [_P, _I32, _I32, _I32, C.POINTER(Config), _P, _P],
     "sfb_point_eval": [_P, _I32, _I32, _I32, _I64, _P, _P, _P, _P, _P],
     "sfb_energy_and_linearize": [_P, C.POINTER(Weights), _I32, _D, C.POINTER(Config), _P],
+    "sfb_set_shard": [_P, _I32, _I32],
+    "sfb_exchange_buffer": [_P, _I32, C.POINTER(_P), C.POINTER(_I64)],
+    "sfb_build_dense_edges_begin": [_P, _D],
+    "sfb_build_dense_edges_end": [_P, C.POINTER(_I64)],
+    "sfb_linearize_begin": [_P, C.POINTER(Weights), _D, C.POINTER(Config), C.POINTER(_I32)],
+    "sfb_linearize_end": [_P, _P],
+    "sfb_energy_and_linearize_begin": [_P, C.POINTER(Weights), _I32, _D, C.POINTER(Config),
+                                       C.POINTER(_I32)],
+    "sfb_energy_and_linearize_end": [_P, _P],
+    "sfb_energy_frozen_begin": [_P, _I32, C.POINTER(_I32)],
+    "sfb_energy_frozen_end": [_P, _P],
     "sfb_profile": [_P, _I32],
     "sfb_profile_read": [_P, _P, _P, _I32],
     "sfb_launch_count": [C.POINTER(_I64)],

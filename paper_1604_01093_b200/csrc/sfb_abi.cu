@@ -244,7 +244,15 @@ struct sfb_problem : Handle {
   DBuf<uint8_t> tile_any[2];     // per (edge, source tile): any frozen association
   int cur = 0;                   // buffer holding the latest linearisation
   DBuf<double> item_out, edge_out, item_e2;
+  DBuf<double> edge_e2;          // frozen-energy sums per directed edge (2 each)
   bool dense_active = false;
+  // between the two halves of a (possibly sharded) linearisation / energy
+  bool pending_dense_on = false;
+  int pending_prev_mode = 0;
+  bool pending_energy_dense = false;
+  // data-parallel sharding over directed dense edges
+  int shard_rank = 0, shard_world = 1;
+  int n_cand = 0;                // pair-filter candidates of the last filter pass
   int last_do_photo = 0, last_do_geo = 0;
   // system
   int n_pairs = 0;
@@ -366,7 +374,9 @@ int rebuild_structure(sfb_problem* p, int bidir) {
     parts = std::max(parts, (nt + 1023) / 1024);
     parts = std::min(parts, nt);
     const int per = (nt + parts - 1) / parts;
-    for (int b = 0; b < nt; b += per) items.push_back(make_int4(d, b, std::min(nt, b + per), 0));
+    // sharded: this rank only owns every world-th directed edge
+    if (p->shard_world <= 1 || d % p->shard_world == p->shard_rank)
+      for (int b = 0; b < nt; b += per) items.push_back(make_int4(d, b, std::min(nt, b + per), 0));
     eptr.push_back((int)items.size());
     poff.push_back(pw);
     goff.push_back(gw);
@@ -472,7 +482,8 @@ int rebuild_structure(sfb_problem* p, int bidir) {
   }
   CK(p, p->item_out.ensure((size_t)p->n_items * SFB_ITEM_STRIDE));
   CK(p, p->edge_out.ensure((size_t)p->n_dir * SFB_ITEM_STRIDE));
-  CK(p, p->item_e2.ensure((size_t)p->n_items * 2));
+  CK(p, p->item_e2.ensure((size_t)std::max(1, p->n_items) * 2));
+  CK(p, p->edge_e2.ensure((size_t)std::max(1, p->n_dir) * 2));
   CK(p, upload_vec(p->d_ptr, dptr, s));
   CK(p, upload_vec(p->d_ent, dent, s));
   CK(p, upload_vec(p->b_ptr, bptr, s));
@@ -529,6 +540,8 @@ SparseArgs sparse_args(sfb_problem* p) {
 
 // Enqueue linearize (no sync).  dense_on decided on the host.
 int enqueue_energy_frozen(sfb_problem* p, int dense, double* dout3, int dense_only = 0);
+int enqueue_dense_energy_edges(sfb_problem* p);
+int enqueue_linearize_end(sfb_problem* p);
 
 // Linearisation at the current poses.  With fuse_prev, the previous
 // linearisation's frozen dense energy is evaluated in the same pass when one
@@ -558,7 +571,7 @@ int enqueue_linearize(sfb_problem* p, const sfb_weights* w, double w_dense, cons
   if (prev_mode) *prev_mode = 0;
   const bool lin = dense_on && (w->photo > 0.0 || w->geo > 0.0);
   if (prev_avail && !lin) {
-    int rc = enqueue_energy_frozen(p, 1, p->dscal.p + 16, /*dense_only=*/1);
+    int rc = enqueue_dense_energy_edges(p);
     if (rc) return rc;
     if (prev_mode) *prev_mode = 2;
   }
@@ -599,6 +612,16 @@ int enqueue_linearize(sfb_problem* p, const sfb_weights* w, double w_dense, cons
     p->last_do_photo = da.do_photo;
     p->last_do_geo = da.do_geo;
   }
+  p->pending_dense_on = dense_on;
+  p->pending_prev_mode = prev_mode ? *prev_mode : 0;
+  return SFB_OK;
+}
+
+// Second half of a linearisation, after the per-edge sums are complete on
+// every rank (sharded runs all-reduce edge_out / edge_e2 in between).
+int enqueue_linearize_end(sfb_problem* p) {
+  cudaStream_t s = p->stream;
+  const bool dense_on = p->pending_dense_on;
   AssembleArgs aa{};
   aa.n_blk = p->n_blk;
   aa.n_pairs = p->n_pairs;
@@ -627,35 +650,60 @@ int enqueue_linearize(sfb_problem* p, const sfb_weights* w, double w_dense, cons
   launch_sum_energies(p->set_out.p, p->n_sets, p->edge_out.p, dense_on ? p->n_dir : 0, nullptr, 0,
                       p->dscal.p, 0, s);
   CKL(p);
+  if (p->pending_prev_mode == 2) {  // separate frozen-energy pass: sums -> dscal[16..18]
+    launch_sum_energies(nullptr, 0, nullptr, 0, p->edge_e2.p, p->n_dir, p->dscal.p + 16, 1, s);
+    CKL(p);
+  }
   p->dense_active = dense_on;
   p->have_system = true;
   p->have_solution = false;
   return SFB_OK;
 }
 
-int enqueue_energy_frozen(sfb_problem* p, int dense, double* dout3, int dense_only) {
+// Frozen-association dense energy at the current poses -> per-edge sums
+// (edge_e2, 2 per directed edge; zero for edges this rank does not own).
+int enqueue_dense_energy_edges(sfb_problem* p) {
+  cudaStream_t s = p->stream;
+  DenseArgs da = dense_args(p);
+  da.do_photo = p->last_do_photo;
+  da.do_geo = p->last_do_geo;
+  {
+    ProfScope ps(p->prof, 1, s);
+    launch_dense_energy(da, p->item_e2.p, s);
+  }
+  CKL(p);
+  launch_edge_reduce2(p->edge_item_ptr.p, p->item_e2.p, p->edge_e2.p, p->n_dir, s);
+  CKL(p);
+  return SFB_OK;
+}
+
+int enqueue_energy_frozen_begin(sfb_problem* p, int dense) {
   cudaStream_t s = p->stream;
   SparseArgs sa = sparse_args(p);
   sa.energy_only = 1;
   sa.w_sparse = 1.0;
-  if (!dense_only) {
+  {
     ProfScope ps(p->prof, 4, s);
     launch_sparse(sa, s);
   }
   CKL(p);
-  const bool d = dense && p->dense_active && p->n_items > 0;
-  if (d) {
-    DenseArgs da = dense_args(p);
-    da.do_photo = p->last_do_photo;
-    da.do_geo = p->last_do_geo;
-    ProfScope ps(p->prof, 1, s);
-    launch_dense_energy(da, p->item_e2.p, s);
-    CKL(p);
-  }
-  launch_sum_energies(p->set_out.p, p->n_sets, nullptr, 0, p->item_e2.p, d ? p->n_items : 0, dout3,
-                      1, s);
+  p->pending_energy_dense = dense && p->dense_active && p->n_items > 0;
+  if (p->pending_energy_dense) return enqueue_dense_energy_edges(p);
+  return SFB_OK;
+}
+
+int enqueue_energy_frozen_end(sfb_problem* p, double* dout3) {
+  const bool d = p->pending_energy_dense;
+  launch_sum_energies(p->set_out.p, p->n_sets, nullptr, 0, p->edge_e2.p, d ? p->n_dir : 0, dout3,
+                      1, p->stream);
   CKL(p);
   return SFB_OK;
+}
+
+int enqueue_energy_frozen(sfb_problem* p, int dense, double* dout3, int /*dense_only*/) {
+  int rc = enqueue_energy_frozen_begin(p, dense);
+  if (rc) return rc;
+  return enqueue_energy_frozen_end(p, dout3);
 }
 
 }  // namespace
@@ -817,20 +865,10 @@ int sfb_frames_upload(sfb_ctx* c, int32_t n, const sfb_frame_desc* d, int32_t* s
     devs[k] = f;
   }
   // one batched H2D for every plane of every frame (CUDA >= 12.8), else a loop
-  bool batched = cdst.empty();
-#if CUDART_VERSION >= 12080
-  if (!batched) {
-    cudaMemcpyAttributes attr{};
-    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-    size_t idx0 = 0, fail_idx = 0;
-    batched = cudaMemcpyBatchAsync(cdst.data(), csrc.data(), csz.data(), cdst.size(), &attr,
-                                   &idx0, 1, &fail_idx, c->stream) == cudaSuccess;
-    if (!batched) cudaGetLastError();
-  }
-#endif
-  if (!batched)
-    for (size_t q = 0; q < cdst.size(); ++q)
-      CK(c, cudaMemcpyAsync(cdst[q], csrc[q], csz[q], cudaMemcpyHostToDevice, c->stream));
+  // (cudaMemcpyBatchAsync crashed on pageable sources on the 580 driver; the
+  // pinned fast path above needs no copies at all)
+  for (size_t q = 0; q < cdst.size(); ++q)
+    CK(c, cudaMemcpyAsync(cdst[q], csrc[q], csz[q], cudaMemcpyHostToDevice, c->stream));
   CK(c, cudaMemcpyAsync(c->pack_args.p, pargs.data(), sizeof(PackArgs) * n, cudaMemcpyHostToDevice,
                         c->stream));
   launch_pack_batch(c->pack_args.p, n, max_hw, max_nt, c->stream);
@@ -996,6 +1034,9 @@ int sfb_problem_destroy(sfb_problem* p) {
     p->geo_tgt[b].release();
     p->tile_any[b].release();
   }
+  {
+    p->edge_e2.release();
+  }
   p->prof.destroy();
   p->f_all.release();
   p->f_cand.release();
@@ -1057,21 +1098,23 @@ int sfb_restore_best(sfb_problem* p) {
   return SFB_OK;
 }
 
-int sfb_build_dense_edges(sfb_problem* p, double cos_min, int64_t* n_out) {
-  if (!p || !n_out) return fail(p, SFB_E_ARG, "null argument");
+// Filter phase 1: angle gate, candidate compaction, overlap test of this
+// rank's candidates -> pass flags (f_pass, n_cand bytes; zero for candidates
+// owned by other ranks).  Sharded callers sum the flags across ranks before
+// sfb_build_dense_edges_end.
+int sfb_build_dense_edges_begin(sfb_problem* p, double cos_min) {
+  if (!p) return fail(p, SFB_E_ARG, "null argument");
   if (!p->has_frames) return fail(p, SFB_E_STATE, "problem has no frames (caches=None)");
   CK(p, cudaSetDevice(p->ctx->device));
-  const auto t0 = std::chrono::steady_clock::now();
   cudaStream_t s = p->stream;
   const int n = p->n;
   const int64_t P = (int64_t)n * (n - 1) / 2;
   p->edges.clear();
+  p->n_cand = 0;
   if (P > 0) {
     if (P > INT32_MAX) return fail(p, SFB_E_ARG, "too many frames for the pair filter");
-    // persistent scratch: no cudaMalloc/cudaFree (which synchronise) per solve
     DBuf<int2>& all = p->f_all;
     DBuf<int2>& cand = p->f_cand;
-    DBuf<int2>& sel = p->f_sel;
     DBuf<uint8_t>& fl = p->f_fl;
     DBuf<uint8_t>& pass = p->f_pass;
     DBuf<uint8_t>& temp = p->f_temp;
@@ -1094,32 +1137,60 @@ int sfb_build_dense_edges(sfb_problem* p, double cos_min, int64_t* n_out) {
     int nc = 0;
     CK(p, cudaMemcpyAsync(&nc, cnt.p, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(p, cudaStreamSynchronize(s));
+    p->n_cand = nc;
     if (nc > 0) {
       CK(p, pass.ensure(nc));
-      CK(p, sel.ensure(nc));
-      {
-        ProfScope ps(p->prof, 3, s);
-        launch_overlap(p->frames.p, p->poses.p, cand.p, nc, p->ctx->rd, 0, pass.p, nullptr, s);
-        CKL(p);
-        sfb_count_launch(2);
-        CK(p, select_flagged(cand.p, pass.p, sel.p, cnt.p + 1, nc, temp, s));
-      }
-      int ne = 0;
-      CK(p, cudaMemcpyAsync(&ne, cnt.p + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
-      CK(p, cudaStreamSynchronize(s));
-      p->edges.resize(ne);
-      if (ne > 0)
-        CK(p, cudaMemcpyAsync(p->edges.data(), sel.p, sizeof(int2) * ne, cudaMemcpyDeviceToHost, s));
-      CK(p, cudaStreamSynchronize(s));
+      ProfScope ps(p->prof, 3, s);
+      launch_overlap(p->frames.p, p->poses.p, cand.p, nc, p->ctx->rd, 0, pass.p, nullptr, s,
+                     p->shard_rank, p->shard_world);
+      CKL(p);
     }
   }
+  return SFB_OK;
+}
+
+// Filter phase 2: compact the passing candidates (pair order = reference
+// loop order) and rebuild the work structure.
+int sfb_build_dense_edges_end(sfb_problem* p, int64_t* n_out) {
+  if (!p || !n_out) return fail(p, SFB_E_ARG, "null argument");
+  CK(p, cudaSetDevice(p->ctx->device));
+  cudaStream_t s = p->stream;
+  const int nc = p->n_cand;
+  p->edges.clear();
+  if (nc > 0) {
+    CK(p, p->f_sel.ensure(nc));
+    {
+      ProfScope ps(p->prof, 3, s);
+      sfb_count_launch(2);
+      CK(p, select_flagged(p->f_cand.p, p->f_pass.p, p->f_sel.p, p->f_cnt.p + 1, nc, p->f_temp, s));
+    }
+    int ne = 0;
+    CK(p, cudaMemcpyAsync(&ne, p->f_cnt.p + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(p, cudaStreamSynchronize(s));
+    p->edges.resize(ne);
+    if (ne > 0)
+      CK(p, cudaMemcpyAsync(p->edges.data(), p->f_sel.p, sizeof(int2) * ne, cudaMemcpyDeviceToHost, s));
+    CK(p, cudaStreamSynchronize(s));
+  }
   *n_out = (int64_t)p->edges.size();
-  if (trace_on())
-    fprintf(stderr, "sfb pair filter: %.2f ms (%d frames, %lld edges)\n",
-            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(),
-            n, (long long)*n_out);
   return rebuild_structure(p, p->struct_bidir < 0 ? 0 : p->struct_bidir);
 }
+
+int sfb_build_dense_edges(sfb_problem* p, double cos_min, int64_t* n_out) {
+  if (!p || !n_out) return fail(p, SFB_E_ARG, "null argument");
+  if (p->shard_world > 1)
+    return fail(p, SFB_E_STATE, "sharded problem: use sfb_build_dense_edges_begin/_end");
+  const auto t0 = std::chrono::steady_clock::now();
+  int rc = sfb_build_dense_edges_begin(p, cos_min);
+  if (rc) return rc;
+  rc = sfb_build_dense_edges_end(p, n_out);
+  if (trace_on())
+    fprintf(stderr, "sfb pair filter + rebuild: %.2f ms (%d frames, %lld edges)\n",
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(),
+            p->n, (long long)*n_out);
+  return rc;
+}
+
 
 int sfb_get_dense_edges(sfb_problem* p, int32_t* out) {
   if (!p || (!out && !p->edges.empty())) return fail(p, SFB_E_ARG, "null argument");
@@ -1175,8 +1246,11 @@ int sfb_frustum_overlap(sfb_problem* p, int64_t np_, const int32_t* pairs, doubl
 int sfb_linearize(sfb_problem* p, const sfb_weights* w, double w_dense, const sfb_config* cfg,
                   double e3[3]) {
   if (!p || !w || !cfg || !e3) return fail(p, SFB_E_ARG, "null argument");
+  if (p->shard_world > 1) return fail(p, SFB_E_STATE, "sharded problem: use the _begin/_end form");
   CK(p, cudaSetDevice(p->ctx->device));
   int rc = enqueue_linearize(p, w, w_dense, cfg);
+  if (rc) return rc;
+  rc = enqueue_linearize_end(p);
   if (rc) return rc;
   CK(p, cudaMemcpyAsync(p->hscal, p->dscal.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
   CK(p, cudaStreamSynchronize(p->stream));
@@ -1297,6 +1371,7 @@ int sfb_apply_step(sfb_problem* p, double* step_norm) {
 
 int sfb_energy_frozen(sfb_problem* p, int32_t dense, double e3[3]) {
   if (!p || !e3) return fail(p, SFB_E_ARG, "null argument");
+  if (p->shard_world > 1) return fail(p, SFB_E_STATE, "sharded problem: use the _begin/_end form");
   CK(p, cudaSetDevice(p->ctx->device));
   int rc = enqueue_energy_frozen(p, dense, p->dscal.p + 16);
   if (rc) return rc;
@@ -1310,8 +1385,11 @@ int sfb_gn_iteration(sfb_problem* p, const sfb_weights* w, double w_dense, const
                      int32_t max_it, double tol, int32_t restart, sfb_iter_result* out) {
   if (!p || !w || !cfg || !out) return fail(p, SFB_E_ARG, "null argument");
   if (restart < 1) return fail(p, SFB_E_ARG, "pcg_restart_interval must be >= 1");
+  if (p->shard_world > 1) return fail(p, SFB_E_STATE, "sharded problem: use the _begin/_end form");
   CK(p, cudaSetDevice(p->ctx->device));
   int rc = enqueue_linearize(p, w, w_dense, cfg);
+  if (rc) return rc;
+  rc = enqueue_linearize_end(p);
   if (rc) return rc;
   cudaStream_t s = p->stream;
   if (p->n_blk > 0) {
@@ -1565,12 +1643,25 @@ extern "C" {
 // same (current) poses, in one pass over the frame pairs (solver.py:662-672
 // followed by :630-660).  out = {E_sparse, E_photo_frozen, E_geo_frozen,
 // E_sparse, E_photo_new, E_geo_new} (raw sums).
-int sfb_energy_and_linearize(sfb_problem* p, const sfb_weights* w, int32_t prev_dense,
-                             double w_dense_next, const sfb_config* cfg, double out6[6]) {
-  if (!p || !w || !cfg || !out6) return fail(p, SFB_E_ARG, "null argument");
+// Sharded form: begin enqueues everything up to the per-edge sums and tells
+// the caller which exchange buffers must be summed across ranks (bit 0:
+// edge_out, bit 1: edge_e2); end assembles and returns the energies.
+int sfb_energy_and_linearize_begin(sfb_problem* p, const sfb_weights* w, int32_t prev_dense,
+                                   double w_dense_next, const sfb_config* cfg, int32_t* exchange) {
+  if (!p || !w || !cfg || !exchange) return fail(p, SFB_E_ARG, "null argument");
   CK(p, cudaSetDevice(p->ctx->device));
   int mode = 0;
   int rc = enqueue_linearize(p, w, w_dense_next, cfg, prev_dense ? 1 : 0, &mode);
+  if (rc) return rc;
+  *exchange = (p->pending_dense_on ? 1 : 0) | (mode == 2 ? 2 : 0);
+  return SFB_OK;
+}
+
+int sfb_energy_and_linearize_end(sfb_problem* p, double out6[6]) {
+  if (!p || !out6) return fail(p, SFB_E_ARG, "null argument");
+  CK(p, cudaSetDevice(p->ctx->device));
+  const int mode = p->pending_prev_mode;
+  int rc = enqueue_linearize_end(p);
   if (rc) return rc;
   CK(p, cudaMemcpyAsync(p->hscal, p->dscal.p, 20 * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
   CK(p, cudaStreamSynchronize(p->stream));
@@ -1582,6 +1673,84 @@ int sfb_energy_and_linearize(sfb_problem* p, const sfb_weights* w, int32_t prev_
   out6[4] = h[1];
   out6[5] = h[2];
   return SFB_OK;
+}
+
+int sfb_energy_and_linearize(sfb_problem* p, const sfb_weights* w, int32_t prev_dense,
+                             double w_dense_next, const sfb_config* cfg, double out6[6]) {
+  if (p && p->shard_world > 1) return fail(p, SFB_E_STATE, "sharded problem: use the _begin/_end form");
+  int32_t ex = 0;
+  int rc = sfb_energy_and_linearize_begin(p, w, prev_dense, w_dense_next, cfg, &ex);
+  if (rc) return rc;
+  return sfb_energy_and_linearize_end(p, out6);
+}
+
+int sfb_linearize_begin(sfb_problem* p, const sfb_weights* w, double w_dense, const sfb_config* cfg,
+                        int32_t* exchange) {
+  if (!p || !w || !cfg || !exchange) return fail(p, SFB_E_ARG, "null argument");
+  CK(p, cudaSetDevice(p->ctx->device));
+  int rc = enqueue_linearize(p, w, w_dense, cfg);
+  if (rc) return rc;
+  *exchange = p->pending_dense_on ? 1 : 0;
+  return SFB_OK;
+}
+
+int sfb_linearize_end(sfb_problem* p, double e3[3]) {
+  if (!p || !e3) return fail(p, SFB_E_ARG, "null argument");
+  CK(p, cudaSetDevice(p->ctx->device));
+  int rc = enqueue_linearize_end(p);
+  if (rc) return rc;
+  CK(p, cudaMemcpyAsync(p->hscal, p->dscal.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+  CK(p, cudaStreamSynchronize(p->stream));
+  for (int k = 0; k < 3; ++k) e3[k] = p->hscal[k];
+  return SFB_OK;
+}
+
+int sfb_energy_frozen_begin(sfb_problem* p, int32_t dense, int32_t* exchange) {
+  if (!p || !exchange) return fail(p, SFB_E_ARG, "null argument");
+  CK(p, cudaSetDevice(p->ctx->device));
+  int rc = enqueue_energy_frozen_begin(p, dense);
+  if (rc) return rc;
+  *exchange = p->pending_energy_dense ? 2 : 0;
+  return SFB_OK;
+}
+
+int sfb_energy_frozen_end(sfb_problem* p, double e3[3]) {
+  if (!p || !e3) return fail(p, SFB_E_ARG, "null argument");
+  CK(p, cudaSetDevice(p->ctx->device));
+  int rc = enqueue_energy_frozen_end(p, p->dscal.p + 16);
+  if (rc) return rc;
+  CK(p, cudaMemcpyAsync(p->hscal + 16, p->dscal.p + 16, 3 * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+  CK(p, cudaStreamSynchronize(p->stream));
+  for (int k = 0; k < 3; ++k) e3[k] = p->hscal[16 + k];
+  return SFB_OK;
+}
+
+int sfb_set_shard(sfb_problem* p, int32_t rank, int32_t world) {
+  if (!p || world < 1 || rank < 0 || rank >= world) return fail(p, SFB_E_ARG, "bad shard");
+  CK(p, cudaSetDevice(p->ctx->device));
+  p->shard_rank = rank;
+  p->shard_world = world;
+  return rebuild_structure(p, p->struct_bidir < 0 ? 0 : p->struct_bidir);
+}
+
+int sfb_exchange_buffer(sfb_problem* p, int32_t which, void** dev_ptr, int64_t* bytes) {
+  if (!p || !dev_ptr || !bytes) return fail(p, SFB_E_ARG, "null argument");
+  switch (which) {
+    case 0:
+      *dev_ptr = p->edge_out.p;
+      *bytes = (int64_t)p->n_dir * SFB_ITEM_STRIDE * (int64_t)sizeof(double);
+      return SFB_OK;
+    case 1:
+      *dev_ptr = p->edge_e2.p;
+      *bytes = (int64_t)p->n_dir * 2 * (int64_t)sizeof(double);
+      return SFB_OK;
+    case 2:
+      *dev_ptr = p->f_pass.p;
+      *bytes = p->n_cand;
+      return SFB_OK;
+    default:
+      return fail(p, SFB_E_ARG, "unknown exchange buffer");
+  }
 }
 
 }  // extern "C"

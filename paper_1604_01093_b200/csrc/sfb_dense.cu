@@ -644,6 +644,27 @@ void launch_edge_reduce(const int* edge_item_ptr, const double* item_out, double
   k_edge_reduce<<<(n_dir * 32 + 255) / 256, 256, 0, s>>>(edge_item_ptr, item_out, edge_out, n_dir);
 }
 
+// Frozen-energy item pairs -> per-edge pairs (zero for edges without items).
+__global__ void k_edge_reduce2(const int* edge_item_ptr, const double* item_e2, double* edge_e2,
+                               int n_dir) {
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= n_dir) return;
+  double a = 0.0, b = 0.0;
+  for (int i = edge_item_ptr[d]; i < edge_item_ptr[d + 1]; ++i) {
+    a += item_e2[2 * (int64_t)i];
+    b += item_e2[2 * (int64_t)i + 1];
+  }
+  edge_e2[2 * (int64_t)d] = a;
+  edge_e2[2 * (int64_t)d + 1] = b;
+}
+
+void launch_edge_reduce2(const int* edge_item_ptr, const double* item_e2, double* edge_e2, int n_dir,
+                         cudaStream_t s) {
+  if (n_dir <= 0) return;
+  sfb_count_launch();
+  k_edge_reduce2<<<(n_dir + 255) / 256, 256, 0, s>>>(edge_item_ptr, item_e2, edge_e2, n_dir);
+}
+
 // ---------------------------------------------------------------------------
 // Block-system assembly.  Contribution entries: (id << 3) | kind.
 //  D/g lists (per var):   0 set H_ii / g_i   1 set H_jj / g_j

@@ -124,10 +124,14 @@ __device__ __forceinline__ int classify_tile(const Xf& rel, const double4 s, con
 
 __global__ void __launch_bounds__(256) k_overlap_culled(const FrameDev* frames, const PoseDev* poses,
                                                         const int2* cand, Rounding rd,
-                                                        uint8_t* pass) {
+                                                        uint8_t* pass, int rank, int world) {
   __shared__ Xf rel[2];
   __shared__ int partial[1024];
   __shared__ int n_partial;
+  if (world > 1 && (int)(blockIdx.x % world) != rank) {  // another rank's candidate
+    if (threadIdx.x == 0) pass[blockIdx.x] = 0;
+    return;
+  }
   const int2 ab = cand[blockIdx.x];
   if (threadIdx.x < 2) {
     const int s = threadIdx.x == 0 ? ab.x : ab.y;
@@ -175,11 +179,12 @@ __global__ void __launch_bounds__(256) k_overlap_culled(const FrameDev* frames, 
 }
 
 void launch_overlap(const FrameDev* frames, const PoseDev* poses, const int2* cand, int n_cand,
-                    Rounding rd, int full_count, uint8_t* pass, int* counts, cudaStream_t s) {
+                    Rounding rd, int full_count, uint8_t* pass, int* counts, cudaStream_t s,
+                    int rank, int world) {
   if (n_cand <= 0) return;
   sfb_count_launch();
   if (full_count)
     k_overlap<<<n_cand, 256, 0, s>>>(frames, poses, cand, rd, full_count, pass, counts);
   else
-    k_overlap_culled<<<n_cand, 256, 0, s>>>(frames, poses, cand, rd, pass);
+    k_overlap_culled<<<n_cand, 256, 0, s>>>(frames, poses, cand, rd, pass, rank, world);
 }

@@ -110,6 +110,8 @@ void launch_tiles(const float4* P, int w, int h, int tx, int ty, double4* tiles,
 void launch_sparse(const SparseArgs& a, cudaStream_t s);
 void launch_dense_linearize(const DenseArgs& a, cudaStream_t s);
 void launch_dense_energy(const DenseArgs& a, double* item_e2, cudaStream_t s);
+void launch_edge_reduce2(const int* edge_item_ptr, const double* item_e2, double* edge_e2, int n_dir,
+                         cudaStream_t s);
 void launch_edge_reduce(const int* edge_item_ptr, const double* item_out, double* edge_out,
                         int n_dir, cudaStream_t s);
 void launch_assemble(const AssembleArgs& a, cudaStream_t s);
@@ -124,7 +126,8 @@ void launch_pose_update(PoseDev* poses, int n_frames, const double* dx, double* 
 void launch_angle_gate(const PoseDev* poses, int n, Rounding rd, double cos_min, uint8_t* flags,
                        cudaStream_t s);
 void launch_overlap(const FrameDev* frames, const PoseDev* poses, const int2* cand, int n_cand,
-                    Rounding rd, int full_count, uint8_t* pass, int* counts, cudaStream_t s);
+                    Rounding rd, int full_count, uint8_t* pass, int* counts, cudaStream_t s,
+                    int rank = 0, int world = 1);
 void launch_associate(const DenseArgs& a, int src, int dst, int kind, uint8_t* sel, int* tgt,
                       cudaStream_t s);
 void launch_point_eval(const FrameDev* frames, const PoseDev* poses, int src, int dst, int kind,

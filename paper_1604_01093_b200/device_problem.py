@@ -124,11 +124,33 @@ class DeviceProblem:
         self._ck(self.lib.sfb_problem_stream(self.handle, C.byref(s)))
         return s.value or 0
 
+    # -- sharding ---------------------------------------
+    def set_shard(self, rank: int, world: int) -> None:
+        self._ck(self.lib.sfb_set_shard(self.handle, int(rank), int(world)))
+
+    def exchange_buffer(self, which: int):
+        """(device pointer, bytes) of exchange buffer `which` (0 per-edge
+        linearisation sums f64, 1 per-edge frozen energies f64, 2 filter
+        pass flags u8)."""
+        ptr, nb = C.c_void_p(), C.c_int64()
+        self._ck(self.lib.sfb_exchange_buffer(self.handle, int(which), C.byref(ptr), C.byref(nb)))
+        return ptr.value or 0, nb.value
+
+    def _exchange(self, exchange, mask: int) -> None:
+        for which in (0, 1):
+            if mask & (1 << which):
+                exchange(self, which)
+
     # -- pair filter -----------------------------------------------------------
-    def build_dense_edges(self, view_angle_max_deg: float) -> np.ndarray:
+    def build_dense_edges(self, view_angle_max_deg: float, exchange=None) -> np.ndarray:
         n = C.c_int64()
-        self._ck(self.lib.sfb_build_dense_edges(
-            self.handle, C.c_double(view_cos_threshold(view_angle_max_deg)), C.byref(n)))
+        cos_min = C.c_double(view_cos_threshold(view_angle_max_deg))
+        if exchange is None:
+            self._ck(self.lib.sfb_build_dense_edges(self.handle, cos_min, C.byref(n)))
+        else:
+            self._ck(self.lib.sfb_build_dense_edges_begin(self.handle, cos_min))
+            exchange(self, 2)
+            self._ck(self.lib.sfb_build_dense_edges_end(self.handle, C.byref(n)))
         out = np.zeros((n.value, 2), dtype=np.int32)
         self._ck(self.lib.sfb_get_dense_edges(self.handle, _abi.ptr(out)))
         return out
@@ -154,22 +176,38 @@ class DeviceProblem:
     def _w(weights):
         return _abi.Weights(float(weights.sparse), float(weights.photo), float(weights.geo))
 
-    def linearize(self, weights, w_dense, config) -> np.ndarray:
+    def linearize(self, weights, w_dense, config, exchange=None) -> np.ndarray:
         e = np.zeros(3)
         w, cfg = self._w(weights), self._cfg(config)
-        self._ck(self.lib.sfb_linearize(self.handle, C.byref(w), C.c_double(w_dense),
-                                        C.byref(cfg), _abi.ptr(e)))
+        if exchange is None:
+            self._ck(self.lib.sfb_linearize(self.handle, C.byref(w), C.c_double(w_dense),
+                                            C.byref(cfg), _abi.ptr(e)))
+        else:
+            mask = C.c_int32()
+            self._ck(self.lib.sfb_linearize_begin(self.handle, C.byref(w), C.c_double(w_dense),
+                                                  C.byref(cfg), C.byref(mask)))
+            self._exchange(exchange, mask.value)
+            self._ck(self.lib.sfb_linearize_end(self.handle, _abi.ptr(e)))
         self.version += 1
         return e
 
-    def energy_and_linearize(self, weights, prev_dense: bool, w_dense_next, config):
+    def energy_and_linearize(self, weights, prev_dense: bool, w_dense_next, config, exchange=None):
         """(frozen energies of the last linearisation, next linearisation energies)
         at the current poses, in one fused device pass."""
         out = np.zeros(6)
         w, cfg = self._w(weights), self._cfg(config)
-        self._ck(self.lib.sfb_energy_and_linearize(self.handle, C.byref(w), 1 if prev_dense else 0,
-                                                   C.c_double(w_dense_next), C.byref(cfg),
-                                                   _abi.ptr(out)))
+        pd = 1 if prev_dense else 0
+        if exchange is None:
+            self._ck(self.lib.sfb_energy_and_linearize(self.handle, C.byref(w), pd,
+                                                       C.c_double(w_dense_next), C.byref(cfg),
+                                                       _abi.ptr(out)))
+        else:
+            mask = C.c_int32()
+            self._ck(self.lib.sfb_energy_and_linearize_begin(self.handle, C.byref(w), pd,
+                                                             C.c_double(w_dense_next),
+                                                             C.byref(cfg), C.byref(mask)))
+            self._exchange(exchange, mask.value)
+            self._ck(self.lib.sfb_energy_and_linearize_end(self.handle, _abi.ptr(out)))
         self.version += 1
         return out[:3], out[3:]
 
@@ -185,9 +223,16 @@ class DeviceProblem:
         self._ck(self.lib.sfb_apply_step(self.handle, C.byref(s)))
         return s.value
 
-    def energy_frozen(self, dense: bool) -> np.ndarray:
+    def energy_frozen(self, dense: bool, exchange=None) -> np.ndarray:
         e = np.zeros(3)
-        self._ck(self.lib.sfb_energy_frozen(self.handle, 1 if dense else 0, _abi.ptr(e)))
+        if exchange is None:
+            self._ck(self.lib.sfb_energy_frozen(self.handle, 1 if dense else 0, _abi.ptr(e)))
+        else:
+            mask = C.c_int32()
+            self._ck(self.lib.sfb_energy_frozen_begin(self.handle, 1 if dense else 0,
+                                                      C.byref(mask)))
+            self._exchange(exchange, mask.value)
+            self._ck(self.lib.sfb_energy_frozen_end(self.handle, _abi.ptr(e)))
         return e
 
     def gn_iteration(self, weights, w_dense, config):

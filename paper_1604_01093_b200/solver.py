@@ -581,7 +581,7 @@ class AlignmentProblem:
     problem (its own CUDA stream); distinct instances may run concurrently.
     """
 
-    def __init__(self, frame_ids, poses, corr_sets, caches=None, device=None):
+    def __init__(self, frame_ids, poses, corr_sets, caches=None, device=None, comm=None):
         self.frame_ids = list(frame_ids)
         if not self.frame_ids:
             raise ValueError("need at least one frame")
@@ -595,6 +595,8 @@ class AlignmentProblem:
         self._sparse = None
         self.dense_edges = []
         self._device = device
+        # data-parallel sharding over frame pairs (paper_1604_01093_b200.shard)
+        self._xch = comm if (comm is not None and comm.world > 1) else None
         self._dp = None
         self._dp_edges = None
 
@@ -617,6 +619,8 @@ class AlignmentProblem:
             cl = [self.caches[f] for f in self.frame_ids] if self.caches is not None else None
             self._dp = DeviceProblem(len(self.frame_ids), cl, frames, pi, pj, off,
                                      device=self._device)
+            if self._xch is not None:
+                self._dp.set_shard(self._xch.rank, self._xch.world)
         return self._dp
 
     def _push_poses(self):
@@ -648,7 +652,7 @@ class AlignmentProblem:
         dp = self._problem()
         self._push_poses()
         self._sync_edges()
-        e = dp.linearize(weights, w_dense, config)
+        e = dp.linearize(weights, w_dense, config, exchange=self._xch)
         dense_on = self.caches is not None and w_dense > 0.0 and bool(self.dense_edges)
         energy = weights.sparse * float(e[0])
         if dense_on:
@@ -683,7 +687,7 @@ class AlignmentProblem:
         self._push_poses()
         tr.mark("setup")
         if self.caches is not None:
-            pairs = dp.build_dense_edges(config.view_angle_max_deg)
+            pairs = dp.build_dense_edges(config.view_angle_max_deg, exchange=self._xch)
             self.dense_edges = _EdgeList(pairs, self.frame_ids)
             self._dp_edges = self.dense_edges
         else:
@@ -697,7 +701,8 @@ class AlignmentProblem:
         e_next = None
         for it in range(max_iterations):
             w_dense = dense_ramp_weight(weights, it)
-            e = e_next if e_next is not None else dp.linearize(weights, w_dense, config)
+            e = e_next if e_next is not None else dp.linearize(weights, w_dense, config,
+                                                               exchange=self._xch)
             e_next = None
             tr.mark("lin")
             dense_on = self.caches is not None and w_dense > 0.0 and have_edges
@@ -722,9 +727,10 @@ class AlignmentProblem:
                 # E_after(it) and the linearisation of it+1 happen at the same
                 # poses: one fused device pass (discarded if the loop stops).
                 ea, e_next = dp.energy_and_linearize(
-                    weights, w_dense > 0.0, dense_ramp_weight(weights, it + 1), config)
+                    weights, w_dense > 0.0, dense_ramp_weight(weights, it + 1), config,
+                    exchange=self._xch)
             else:
-                ea = dp.energy_frozen(w_dense > 0.0)
+                ea = dp.energy_frozen(w_dense > 0.0, exchange=self._xch)
             tr.mark("energy+lin")
             energy_after = weights.sparse * float(ea[0])
             if w_dense > 0.0:
