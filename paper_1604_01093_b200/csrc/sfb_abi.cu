@@ -604,7 +604,8 @@ int enqueue_linearize(sfb_problem* p, const sfb_weights* w, double w_dense, cons
       CKL(p);
       p->cur = nxt;
       ProfScope ps(p->prof, 5, s);
-      launch_edge_reduce(p->edge_item_ptr.p, p->item_out.p, p->edge_out.p, p->n_dir, s);
+      launch_edge_reduce(p->edge_item_ptr.p, p->item_out.p, p->edge_out.p, p->n_dir, p->dir_edges.p,
+                         p->poses.p, s);
       CKL(p);
     } else {
       CK(p, cudaMemsetAsync(p->edge_out.p, 0, sizeof(double) * p->n_dir * SFB_ITEM_STRIDE, s));

@@ -471,27 +471,19 @@ __global__ void __launch_bounds__(DENSE_THREADS, 2) k_dense_fused(DenseArgs a) {
       const double e2 = r0 * r0 + r1 * r1;
       if (PREV && pph) eprev_p += e2;
       if (ph_in) {
+        // J_i = M_j v with M_j = [[R_j, -[t_j]x R_j], [0, -R_j]] (per edge) and
+        // v = [dq x q ; dq] in camera-j coordinates (dq = d value / d q):
+        // accumulate v v^T here, apply M_j once per edge (k_edge_reduce).
         acc[27] += e2;
-        double wld[3];
-        xf_apply(ec.Ri, ec.ti, d0, d1, d2, wld);
         const double a_ = Fj.fx * rz, b_ = Fj.fy * rz;
-        const double rz2 = rz * rz;
-        const double au = -Fj.fx * q0 * rz2, bv = -Fj.fy * q1 * rz2;
         const double res[2] = {r0, r1};
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
-          const double dq0 = ddx[c] * a_, dq1 = ddy[c] * b_, dq2 = ddx[c] * au + ddy[c] * bv;
-          double g[3];
-#pragma unroll
-          for (int k = 0; k < 3; ++k) g[k] = dq0 * ec.Rj[k * 3 + 0] + dq1 * ec.Rj[k * 3 + 1] + dq2 * ec.Rj[k * 3 + 2];
-          double J[6];
-          J[0] = g[1] * wld[2] - g[2] * wld[1];
-          J[1] = g[2] * wld[0] - g[0] * wld[2];
-          J[2] = g[0] * wld[1] - g[1] * wld[0];
-          J[3] = -g[0];
-          J[4] = -g[1];
-          J[5] = -g[2];
-          accum_row(acc, J, res[c], a.s_photo);
+          const double dq0 = ddx[c] * a_, dq1 = ddy[c] * b_;
+          const double dq2 = -(dq0 * q0 + dq1 * q1) * rz;
+          const double v[6] = {dq1 * q2 - dq2 * q1, dq2 * q0 - dq0 * q2, dq0 * q1 - dq1 * q0,
+                               dq0, dq1, dq2};
+          accum_row(acc, v, res[c], a.s_photo);
         }
       }
     }
@@ -515,14 +507,13 @@ __global__ void __launch_bounds__(DENSE_THREADS, 2) k_dense_fused(DenseArgs a) {
         const double m1 = ec.back[3] * t0 + ec.back[4] * t1 + ec.back[5] * t2 + ec.back[10];
         const double m2 = ec.back[6] * t0 + ec.back[7] * t1 + ec.back[8] * t2 + ec.back[11];
         const double r = n0 * (d0 - m0) + n1 * (d1 - m1) + n2 * (d2 - m2);
-        double wt[3];
-        xf_apply(ec.Rj, ec.tj, t0, t1, t2, wt);
-        double m[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) m[k] = ec.Ri[k * 3 + 0] * n0 + ec.Ri[k * 3 + 1] * n1 + ec.Ri[k * 3 + 2] * n2;
-        const double J[6] = {wt[1] * m[2] - wt[2] * m[1], wt[2] * m[0] - wt[0] * m[2],
-                             wt[0] * m[1] - wt[1] * m[0], m[0], m[1], m[2]};
-        accum_row(acc, J, r, a.s_geo);
+        // J_i = M_j v, v = [p_t x n_j ; -n_j], n_j = R_j^T R_i n = rel.R n
+        const double nj0 = ec.rel.R[0] * n0 + ec.rel.R[1] * n1 + ec.rel.R[2] * n2;
+        const double nj1 = ec.rel.R[3] * n0 + ec.rel.R[4] * n1 + ec.rel.R[5] * n2;
+        const double nj2 = ec.rel.R[6] * n0 + ec.rel.R[7] * n1 + ec.rel.R[8] * n2;
+        const double v[6] = {t1 * nj2 - t2 * nj1, t2 * nj0 - t0 * nj2, t0 * nj1 - t1 * nj0,
+                             -nj0, -nj1, -nj2};
+        accum_row(acc, v, r, a.s_geo);
         acc[28] += r * r;
       }
     }
@@ -625,23 +616,71 @@ void launch_dense_energy(const DenseArgs& a, double* item_e2, cudaStream_t s) {
   k_dense_energy<<<a.n_items, DENSE_THREADS, 0, s>>>(a, item_e2);
 }
 
-// Sum each directed edge's tiles in tile order (one warp per edge, lane = slot).
+// Sum each directed edge's tiles in tile order (one warp per edge, lane =
+// slot), then map the camera-j accumulators to the pose increments:
+// H_e = M_j K M_j^T, g_e = M_j k with M_j = [[R_j, -[t_j]x R_j], [0, -R_j]]
+// (both dense terms' J_i = M_j v, see k_dense_fused).
 __global__ void k_edge_reduce(const int* edge_item_ptr, const double* item_out, double* edge_out,
-                              int n_dir) {
+                              int n_dir, const int2* dir_edges, const PoseDev* poses) {
+  __shared__ double sK[8][36], sM[8][36], sk[8][6];
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int wl = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= n_dir) return;
   double s = 0.0;
   for (int i = edge_item_ptr[warp]; i < edge_item_ptr[warp + 1]; ++i)
     s += item_out[(int64_t)i * SFB_ITEM_STRIDE + lane];
-  edge_out[(int64_t)warp * SFB_ITEM_STRIDE + lane] = s;
+  double* out = edge_out + (int64_t)warp * SFB_ITEM_STRIDE;
+  if (lane >= 27) {
+    out[lane] = s;  // energies pass through
+  }
+  // unpack K (packed upper triangle) and k into shared memory
+  for (int r = 0; r < 6; ++r)
+    for (int c = r; c < 6; ++c)
+      if (lane == sym6(r, c)) sK[wl][r * 6 + c] = sK[wl][c * 6 + r] = s;
+  if (lane >= 21 && lane < 27) sk[wl][lane - 21] = s;
+  if (lane == 0) {
+    const PoseDev& Pj = poses[dir_edges[warp].y];
+    const double* R = Pj.R;
+    const double* t = Pj.t;
+    const double T[9] = {0, -t[2], t[1], t[2], 0, -t[0], -t[1], t[0], 0};  // [t]x
+    for (int r = 0; r < 6; ++r)
+      for (int c = 0; c < 6; ++c) sM[wl][r * 6 + c] = 0.0;
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) {
+        double tr = 0.0;
+        for (int k = 0; k < 3; ++k) tr += T[r * 3 + k] * R[k * 3 + c];
+        sM[wl][r * 6 + c] = R[r * 3 + c];
+        sM[wl][r * 6 + c + 3] = -tr;
+        sM[wl][(r + 3) * 6 + c + 3] = -R[r * 3 + c];
+      }
+  }
+  __syncwarp();
+  if (lane < 21) {
+    int r = 0, c = lane;
+    while (c >= 6 - r) { c -= 6 - r; ++r; }  // packed index -> (r, c >= r)
+    c += r;
+    double h = 0.0;
+    for (int k = 0; k < 6; ++k) {
+      double mk = 0.0;
+      for (int l = 0; l < 6; ++l) mk += sK[wl][k * 6 + l] * sM[wl][c * 6 + l];
+      h += sM[wl][r * 6 + k] * mk;
+    }
+    out[lane] = h;
+  } else if (lane < 27) {
+    const int r = lane - 21;
+    double g = 0.0;
+    for (int k = 0; k < 6; ++k) g += sM[wl][r * 6 + k] * sk[wl][k];
+    out[lane] = g;
+  }
 }
 
 void launch_edge_reduce(const int* edge_item_ptr, const double* item_out, double* edge_out,
-                        int n_dir, cudaStream_t s) {
+                        int n_dir, const int2* dir_edges, const PoseDev* poses, cudaStream_t s) {
   if (n_dir <= 0) return;
   sfb_count_launch();
-  k_edge_reduce<<<(n_dir * 32 + 255) / 256, 256, 0, s>>>(edge_item_ptr, item_out, edge_out, n_dir);
+  k_edge_reduce<<<(n_dir * 32 + 255) / 256, 256, 0, s>>>(edge_item_ptr, item_out, edge_out, n_dir,
+                                                         dir_edges, poses);
 }
 
 // Frozen-energy item pairs -> per-edge pairs (zero for edges without items).
