@@ -143,7 +143,7 @@ def load(path: os.PathLike | None = None) -> C.CDLL:
     with _lock:
         if _lib is not None:
             return _lib
-        p = Path(path) if path else LIB_PATH
+        p = Path(path) if path else Path(os.environ.get("SFB_LIB", LIB_PATH))
         if not p.exists():
             raise ImportError(
                 f"{p} is not built; run `python -m paper_1604_01093_b200._build` "

@@ -41,11 +41,14 @@ def needs_rebuild() -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not needs_rebuild():
+def build(force: bool = False, verbose: bool = False, out: Path | None = None,
+          extra: list[str] | None = None) -> Path:
+    """Compile libsfb.so (or a tuning variant at `out` with `extra` nvcc flags)."""
+    lib = Path(out) if out else LIB
+    if out is None and not force and not needs_rebuild():
         return LIB
-    tmp = LIB.with_suffix(".so.tmp")
-    cmd = [_nvcc(), *NVCC_FLAGS, "-I", str(ROOT / "include"), "-o", str(tmp),
+    tmp = lib.with_suffix(".so.tmp")
+    cmd = [_nvcc(), *NVCC_FLAGS, *(extra or []), "-I", str(ROOT / "include"), "-o", str(tmp),
            *map(str, sources())]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
@@ -55,8 +58,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stdout}\n{res.stderr}")
     if verbose and res.stderr:
         print(res.stderr, file=sys.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -294,7 +294,10 @@ __device__ __forceinline__ unsigned char tile_maybe_visible(const Xf& rel, const
 }
 
 template <bool STD, bool PREV>
-__global__ void __launch_bounds__(DENSE_THREADS, 2) k_dense_fused(DenseArgs a) {
+#ifndef DENSE_MIN_BLOCKS
+#define DENSE_MIN_BLOCKS 2
+#endif
+__global__ void __launch_bounds__(DENSE_THREADS, DENSE_MIN_BLOCKS) k_dense_fused(DenseArgs a) {
   __shared__ FusedCtx ec;
   const int4 it = a.items[blockIdx.x];
   const int2 de = a.dir_edges[it.x];
