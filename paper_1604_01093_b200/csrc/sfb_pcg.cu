@@ -30,17 +30,15 @@ struct GridBarrier {
   unsigned* ctr;
   unsigned epoch;
   __device__ __forceinline__ void sync(unsigned G) {
-    __syncthreads();
+    __syncthreads();  // the CTA's writes happen-before thread 0's release below
     if (threadIdx.x == 0) {
       ++epoch;
-      __threadfence();
-      atomicAdd(ctr, 1u);
       const unsigned target = epoch * G;
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
       unsigned v;
       do {
-        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
       } while (v < target);
-      __threadfence();
     }
     __syncthreads();
   }
@@ -51,6 +49,7 @@ struct RowCtx {
   int r0, r1;          // owned rows [r0, r1)
   int s0;              // first slot of r0
   const double* Bs;    // staged slot blocks (shared) or null
+  const int* cols;     // column block per global slot (shared when staged)
   double* gbuf;        // this warp's gather buffer (shared), PCG_GATHER_CAP x 6
 };
 
@@ -69,7 +68,7 @@ __device__ __forceinline__ double row_product(const PcgArgs& a, const RowCtx& rc
     const int c1 = min(e1, c0 + PCG_GATHER_CAP);
     // gather the chunk's neighbour vectors: every load of the chunk in flight
     for (int k = c0 + lane; k < c1; k += 32) {
-      const int w = a.row_col[k];
+      const int w = rc.cols[k];
       const double2* pw = reinterpret_cast<const double2*>(pold + 6 * w);
       double2 x01 = __ldcg(pw), x23 = __ldcg(pw + 1), x45 = __ldcg(pw + 2);
       if (FOLD) {
@@ -109,7 +108,7 @@ __global__ void k_matvec(PcgArgs a, const double* xin, double* yout) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= a.n_blk) return;
-  RowCtx rc{0, 0, 0, nullptr, gb[threadIdx.x >> 5]};
+  RowCtx rc{0, 0, 0, nullptr, a.row_col, gb[threadIdx.x >> 5]};
   const double y = row_product<false>(a, rc, warp, nullptr, xin, 0.0, lane);
   if (lane < 6) yout[6 * warp + lane] = y;
 }
@@ -120,8 +119,9 @@ void launch_matvec(const PcgArgs& a, const double* xin, double* yout, cudaStream
   k_matvec<<<(a.n_blk * 32 + 255) / 256, 256, 0, s>>>(a, xin, yout);
 }
 
-// Deterministic block sum of NV per-warp values (lane 0 holds them); every
-// thread of the block receives the totals.
+// Deterministic block sum of NV per-warp values (lane 0 holds them); thread 0
+// receives the totals (it alone publishes them).  `sh` is next rewritten only
+// after the grid barrier that follows every call, which synchronises the CTA.
 template <int NV>
 __device__ __forceinline__ void block_allsum(double (&v)[NV], double (*sh)[PCG_WARPS]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -130,24 +130,37 @@ __device__ __forceinline__ void block_allsum(double (&v)[NV], double (*sh)[PCG_W
     for (int k = 0; k < NV; ++k) sh[k][warp] = v[k];
   }
   __syncthreads();
+  if (threadIdx.x == 0) {
 #pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    double s = 0.0;
+    for (int k = 0; k < NV; ++k) {
+      double s = 0.0;
 #pragma unroll
-    for (int w = 0; w < PCG_WARPS; ++w) s += sh[k][w];
-    v[k] = s;
+      for (int w = 0; w < PCG_WARPS; ++w) s += sh[k][w];
+      v[k] = s;
+    }
   }
-  __syncthreads();
 }
 
 // Every CTA sums the per-CTA partials part[k*G + b] in the same order.
 template <int NV>
 __device__ __forceinline__ void grid_allsum(const double* part, double (&out)[NV], int G) {
+  // all NV x ceil(G/32) loads are issued before any is consumed (one L2
+  // round trip); then a fixed-order per-lane sum and butterfly
   const int lane = threadIdx.x & 31;
+  constexpr int MAXC = 8;  // G <= 256
+  double v[NV][MAXC];
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+      const int b = lane + 32 * c;
+      v[k][c] = b < G ? __ldcg(&part[k * G + b]) : 0.0;
+    }
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
     double s = 0.0;
-    for (int b = lane; b < G; b += 32) s += __ldcg(&part[k * G + b]);
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) s += v[k][c];
     out[k] = warp_sum(s);
   }
 }
@@ -207,15 +220,22 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg(PcgArgs a, Mv mv, int ro
   rc.r1 = min(a.n_blk, rc.r0 + rows_per_cta);
   rc.s0 = 0;
   rc.Bs = nullptr;
+  rc.cols = a.row_col;
   rc.gbuf = smem + wid * PCG_GATHER_CAP * 6;
   if (mv.stageable() && rc.r1 > rc.r0) {
     rc.s0 = a.row_ptr[rc.r0];
-    const int64_t n = (int64_t)(a.row_ptr[rc.r1] - rc.s0) * 36;
-    if ((int64_t)PCG_GATHER_BYTES + n * 8 <= PCG_SMEM_BYTES) {
+    const int64_t ns = a.row_ptr[rc.r1] - rc.s0;
+    const int64_t n = ns * 36;
+    if ((int64_t)PCG_GATHER_BYTES + n * 8 + ns * 4 <= PCG_SMEM_BYTES) {
+      // the matrix (and its column indices) is constant during the solve:
+      // stage this CTA's rows in shared memory once
       double* dst = smem + PCG_WARPS * PCG_GATHER_CAP * 6;
       const double* src = a.Brow + (int64_t)rc.s0 * 36;
       for (int64_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+      int* cdst = reinterpret_cast<int*>(dst + n);
+      for (int64_t i = threadIdx.x; i < ns; i += blockDim.x) cdst[i] = a.row_col[rc.s0 + i];
       rc.Bs = dst;
+      rc.cols = cdst - rc.s0;  // indexed by global slot
     }
   }
   __syncthreads();
