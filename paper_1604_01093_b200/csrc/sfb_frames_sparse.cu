@@ -1,59 +1,11 @@
 // Frame packing, sparse correspondence term, pose update.
 //
-//  k_pack           CachedFrame planes (frames.py:38-50) -> P/N/G/T device layout
+//  k_pack_batch     CachedFrame planes (frames.py:38-50) -> P/N/G/T device layout
 //  k_sparse         _sparse_state + sparse gradient/diagonal/J^T J blocks
 //                   (solver.py:568-580, 389-428, 644-646) and eval_sparse (:114-123)
 //  k_pose_update    _apply_step + exp_twist_vector (solver.py:674-677,
 //                   geometry.py:40-48,78-90,183-186)
 #include "sfb_kernels.cuh"
-
-// ---------------------------------------------------------------------------
-__global__ void k_pack(PackArgs a) {
-  const int hw = a.w * a.h;
-  int cnt_vd = 0, cnt_geo = 0;
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < hw; p += gridDim.x * blockDim.x) {
-    const unsigned vd = a.vd[p] ? 1u : 0u;
-    const unsigned vn = a.vn[p] ? 1u : 0u;
-    const unsigned flags = vd * SFB_FLAG_VD | vn * SFB_FLAG_VN;
-    a.P[p] = make_float4(a.pts[3 * p], a.pts[3 * p + 1], a.pts[3 * p + 2], __uint_as_float(flags));
-    a.N[p] = make_float4(a.nrm[3 * p], a.nrm[3 * p + 1], a.nrm[3 * p + 2], 0.f);
-    const float2 g = make_float2(a.grad[2 * p], a.grad[2 * p + 1]);
-    a.G[p] = g;
-    const int y = p / a.w, x = p - y * a.w;
-    float4 t0 = make_float4(0.f, 0.f, 0.f, 0.f), t1 = t0;
-    if (x + 1 < a.w && y + 1 < a.h) {
-      const int q = p + 1, r = p + a.w, s = p + a.w + 1;
-      t0 = make_float4(g.x, g.y, a.grad[2 * q], a.grad[2 * q + 1]);
-      t1 = make_float4(a.grad[2 * r], a.grad[2 * r + 1], a.grad[2 * s], a.grad[2 * s + 1]);
-    }
-    a.T[2 * p] = t0;
-    a.T[2 * p + 1] = t1;
-    cnt_vd += (int)vd;
-    cnt_geo += (int)(vd & vn);
-    // the kernels convert planes with f2d(), exact for finite floats only
-    const bool fin = isfinite(a.pts[3 * p]) && isfinite(a.pts[3 * p + 1]) && isfinite(a.pts[3 * p + 2]) &&
-                     isfinite(a.nrm[3 * p]) && isfinite(a.nrm[3 * p + 1]) && isfinite(a.nrm[3 * p + 2]) &&
-                     isfinite(g.x) && isfinite(g.y);
-    if (!fin) atomicAdd(&a.counts[2], 1);
-  }
-  // integer counts: atomics are exact and order-independent
-  for (int o = 16; o > 0; o >>= 1) {
-    cnt_vd += __shfl_xor_sync(0xffffffffu, cnt_vd, o);
-    cnt_geo += __shfl_xor_sync(0xffffffffu, cnt_geo, o);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    atomicAdd(&a.counts[0], cnt_vd);
-    atomicAdd(&a.counts[1], cnt_geo);
-  }
-}
-
-void launch_pack(const PackArgs& a, cudaStream_t s) {
-  const int hw = a.w * a.h;
-  int blocks = (hw + 255) / 256;
-  if (blocks > 1184) blocks = 1184;
-  sfb_count_launch();
-  k_pack<<<blocks, 256, 0, s>>>(a);
-}
 
 // ---------------------------------------------------------------------------
 // One warp per correspondence set.  Per set we accumulate the moments that
@@ -308,59 +260,9 @@ void launch_pose_update(PoseDev* poses, int n_frames, const double* dx, double* 
   k_pose_update<<<blocks, 256, 0, s>>>(poses, n_frames, dx, step_norm, skip);
 }
 
-// ---------------------------------------------------------------------------
-// Per-tile bounding spheres of the valid points (one warp per 16x16 tile):
-// centre = AABB centre, radius = max distance, inflated so the sphere bounds
-// every point with margin to spare for rounding.
-__global__ void k_tiles(const float4* P, int w, int h, int tx, int ty, double4* tiles, int* counts) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (warp >= tx * ty) return;
-  const int x0 = (warp % tx) * SFB_TILE, y0 = (warp / tx) * SFB_TILE;
-  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
-  int c = 0;
-  for (int k = lane; k < SFB_TILE * SFB_TILE; k += 32) {
-    const int x = x0 + (k % SFB_TILE), y = y0 + (k / SFB_TILE);
-    if (x >= w || y >= h) continue;
-    const float4 p = P[y * w + x];
-    if (!(__float_as_uint(p.w) & SFB_FLAG_VD)) continue;
-    const double q[3] = {p.x, p.y, p.z};
-    for (int d = 0; d < 3; ++d) { lo[d] = fmin(lo[d], q[d]); hi[d] = fmax(hi[d], q[d]); }
-    ++c;
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    c += __shfl_xor_sync(0xffffffffu, c, o);
-    for (int d = 0; d < 3; ++d) {
-      lo[d] = fmin(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], o));
-      hi[d] = fmax(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], o));
-    }
-  }
-  double ctr[3];
-  for (int d = 0; d < 3; ++d) ctr[d] = 0.5 * (lo[d] + hi[d]);
-  double r2 = 0.0;
-  for (int k = lane; k < SFB_TILE * SFB_TILE; k += 32) {
-    const int x = x0 + (k % SFB_TILE), y = y0 + (k / SFB_TILE);
-    if (x >= w || y >= h) continue;
-    const float4 p = P[y * w + x];
-    if (!(__float_as_uint(p.w) & SFB_FLAG_VD)) continue;
-    const double dx = p.x - ctr[0], dy = p.y - ctr[1], dz = p.z - ctr[2];
-    r2 = fmax(r2, dx * dx + dy * dy + dz * dz);
-  }
-  for (int o = 16; o > 0; o >>= 1) r2 = fmax(r2, __shfl_xor_sync(0xffffffffu, r2, o));
-  if (lane == 0) {
-    const double r = sqrt(r2) * (1.0 + 1e-9) + 1e-9;
-    tiles[warp] = c > 0 ? make_double4(ctr[0], ctr[1], ctr[2], r) : make_double4(0, 0, 0, -1.0);
-    counts[warp] = c;
-  }
-}
-
-void launch_tiles(const float4* P, int w, int h, int tx, int ty, double4* tiles, int* counts,
-                  cudaStream_t s) {
-  const int n = tx * ty;
-  sfb_count_launch();
-  k_tiles<<<(n * 32 + 255) / 256, 256, 0, s>>>(P, w, h, tx, ty, tiles, counts);
-}
-
+// Per-tile bounding spheres of the valid points (k_tiles_batch, one warp per
+// 16x16 tile): centre = AABB centre, radius = max distance, inflated so the
+// sphere bounds every point with margin to spare for rounding.
 // Batched upload: blockIdx.y selects the frame.
 __global__ void k_pack_batch(const PackArgs* args) {
   const PackArgs& a0 = args[blockIdx.y];

@@ -102,11 +102,8 @@ struct PcgArgs {
 // Library-wide kernel launch counter (sfb_launch_count).
 void sfb_count_launch(int n = 1);
 
-void launch_pack(const PackArgs& a, cudaStream_t s);
 // every frame of an upload in two launches (planes, then tile spheres)
 void launch_pack_batch(const PackArgs* args_dev, int n, int max_hw, int max_tiles, cudaStream_t s);
-void launch_tiles(const float4* P, int w, int h, int tx, int ty, double4* tiles, int* counts,
-                  cudaStream_t s);
 void launch_sparse(const SparseArgs& a, cudaStream_t s);
 void launch_dense_linearize(const DenseArgs& a, cudaStream_t s);
 void launch_dense_energy(const DenseArgs& a, double* item_e2, cudaStream_t s);
