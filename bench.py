@@ -141,6 +141,19 @@ def canonical_bytes(hw, n_dir, n_corr, n_undirected, n_vars):
     }
 
 
+def ncu_traffic(config: str):
+    """Per-launch DRAM bytes of k_dense_fused from the newest committed ncu
+    --set full summary for this config (profiles/r*_ncu_dense_fused_<cfg>.json,
+    written by tools/ncu_summary.py), or (None, None)."""
+    cands = sorted((ROOT / "profiles").glob(f"r*_ncu_dense_fused_{config}.json"))
+    if not cands:
+        return None, None
+    d = json.loads(cands[-1].read_text())
+    return d.get("traffic_bytes"), {"file": f"profiles/{cands[-1].name}", "label": d.get("label"),
+                                    "fp64_pipe_pct": d.get("fp64_pipe_pct"),
+                                    "dram_gbs": d.get("dram_gbs")}
+
+
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -435,11 +448,13 @@ def main():
         if world > 1:
             dist.destroy_process_group()
         return
+    traffic, traffic_src = ncu_traffic(args.config)
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         edges = [(a, b) for (a, b) in problem.dense_edges]
-        cms, sample, spent = cpu_extrapolate(args.config, edges, records, 1, pair_sample=2000,
-                                             edge_sample=160)
+        # ~10-20 s of single-core oracle work on the GPU box's host
+        cms, sample, spent = cpu_extrapolate(args.config, edges, records, 1, pair_sample=6000,
+                                             edge_sample=600)
         cpu = {"value": cms, "unit": "ms", "cores": 1, "kind": "port", "sample": sample,
                "sample_seconds": round(spent, 1)}
     line = {
@@ -452,9 +467,10 @@ def main():
                    "correspondences": n_corr, "n_vars": nv, "gn_iterations": len(records),
                    "pcg_iterations": pcg_iters, "l2": "flushed (384 MB write) between steps",
                    "parallelism": f"frame-pair shards x{world}" if world > 1 else "single"},
-        "roofline": {"bound": "hbm", "kernel": "k_dense_linearize",
+        "roofline": {"bound": "hbm", "kernel": "k_dense_fused",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak if peak else None, "traffic": None,
+                     "frac": achieved / peak if peak else None, "traffic": traffic,
+                     "traffic_source": traffic_src,
                      "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": cb["linearize"],
                      "ms_per_launch": lin_per, "launches": lin_n},
