@@ -85,13 +85,16 @@ __device__ __forceinline__ double row_product(const PcgArgs& a, const RowCtx& rc
     }
     __syncwarp();
     if (grp < 5) {
+      // six independent FMA chains (one per column) instead of one 6x longer chain
+      double ac[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
       for (int k = c0 + grp; k < c1; k += 5) {
         const double* Bm = rc.Bs ? rc.Bs + (int64_t)(k - rc.s0) * 36 + r * 6
                                  : a.Brow + (int64_t)k * 36 + r * 6;
         const double* xv = rc.gbuf + 6 * (k - c0);
 #pragma unroll
-        for (int c = 0; c < 6; ++c) acc = fma(Bm[c], xv[c], acc);
+        for (int c = 0; c < 6; ++c) ac[c] = fma(Bm[c], xv[c], ac[c]);
       }
+      acc += ((ac[0] + ac[1]) + (ac[2] + ac[3])) + (ac[4] + ac[5]);
     }
     __syncwarp();
   }
@@ -206,6 +209,25 @@ struct DenseMv {
   __device__ __forceinline__ bool stageable() const { return false; }
 };
 
+#ifdef PCG_TRACE
+// tuning builds only (-DPCG_TRACE): CTA 0 stamps %globaltimer at the phase
+// boundaries of the first 64 iterations; read with sfb_debug_pcg_trace.
+__device__ unsigned long long g_pcg_trace[64 * 8];
+__device__ __forceinline__ void trace_mark(int k, int ph) {
+  if (blockIdx.x == 0 && threadIdx.x == 0 && k < 64) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_pcg_trace[k * 8 + ph] = t;
+  }
+}
+extern "C" int sfb_debug_pcg_trace(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_pcg_trace, sizeof(g_pcg_trace));
+}
+#define TRACE(k, ph) trace_mark(k, ph)
+#else
+#define TRACE(k, ph)
+#endif
+
 template <class Mv>
 __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg(PcgArgs a, Mv mv, int rows_per_cta) {
   extern __shared__ __align__(16) double smem[];
@@ -284,6 +306,7 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg(PcgArgs a, Mv mv, int ro
   } else {
     for (int k = 1; k <= a.max_it; ++k) {
       iterations = k;
+      TRACE(k, 0);
       // ---- Ap = A p with p = z + beta pold formed on the fly; owners store p
       {
         double v[1] = {0.0};
@@ -300,12 +323,14 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg(PcgArgs a, Mv mv, int ro
           }
           v[0] += sum6(pAp);
         }
+        TRACE(k, 1);
         block_allsum<1>(v, sh);
         if (threadIdx.x == 0) partA[blockIdx.x] = v[0];
       }
       grid.sync(G);
       double pAp_a[1];
       grid_allsum<1>(partA, pAp_a, G);
+      TRACE(k, 2);
       const double pAp = pAp_a[0];
       if (!isfinite(pAp)) { status = 1; break; }  // PcgDivergenceError
       if (pAp <= 0.0) break;                       // singular direction
@@ -352,6 +377,7 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg(PcgArgs a, Mv mv, int ro
             v[1] += sum6(rzv);
           }
         }
+        TRACE(k, 3);
         block_allsum<3>(v, sh);
         if (threadIdx.x == 0) {
 #pragma unroll
@@ -361,6 +387,7 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg(PcgArgs a, Mv mv, int ro
       grid.sync(G);
       double s3[3];
       grid_allsum<3>(partB, s3, G);
+      TRACE(k, 4);
       if (s3[2] != 0.0) { status = 1; break; }  // non-finite iterate
       relative = sqrt(s3[0]) / norm_b;
       if (relative < a.tol) break;
@@ -380,6 +407,217 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg(PcgArgs a, Mv mv, int ro
   }
 }
 
+// Owner-register variant of k_pcg (same recurrence, same arithmetic): when a
+// warp owns at most PCG_RMAX block rows, lanes 0..5 keep x, r, z, b, M^-1, p
+// and Ap of those rows in registers for the whole solve.  Only what the
+// neighbours read goes to memory (p every iteration, z every iteration for
+// the folded p = z + beta p, x on restart iterations) and x once at the end;
+// the update phase issues no loads at all.
+#define PCG_RMAX 8
+
+__device__ __forceinline__ double rsel(const double (&a)[PCG_RMAX], int j) {
+  double v = a[0];
+#pragma unroll
+  for (int k = 1; k < PCG_RMAX; ++k) v = (k == j) ? a[k] : v;
+  return v;
+}
+__device__ __forceinline__ void rset(double (&a)[PCG_RMAX], int j, double v) {
+#pragma unroll
+  for (int k = 0; k < PCG_RMAX; ++k) a[k] = (k == j) ? v : a[k];
+}
+
+template <class Mv>
+__global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg_reg(PcgArgs a, Mv mv, int rows_per_cta) {
+  extern __shared__ __align__(16) double smem[];
+  GridBarrier grid{reinterpret_cast<unsigned*>(a.flags), 0u};
+  __shared__ double sh[4][PCG_WARPS];
+  const int G = gridDim.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const bool own = lane < 6;
+  if (a.skip && *a.skip != 0.0) return;  // grid-uniform
+  RowCtx rc;
+  rc.r0 = min(a.n_blk, blockIdx.x * rows_per_cta);
+  rc.r1 = min(a.n_blk, rc.r0 + rows_per_cta);
+  rc.s0 = 0;
+  rc.Bs = nullptr;
+  rc.cols = a.row_col;
+  rc.gbuf = smem + wid * PCG_GATHER_CAP * 6;
+  if (mv.stageable() && rc.r1 > rc.r0) {
+    rc.s0 = a.row_ptr[rc.r0];
+    const int64_t ns = a.row_ptr[rc.r1] - rc.s0;
+    const int64_t n = ns * 36;
+    if ((int64_t)PCG_GATHER_BYTES + n * 8 + ns * 4 <= PCG_SMEM_BYTES) {
+      double* dst = smem + PCG_WARPS * PCG_GATHER_CAP * 6;
+      const double* src = a.Brow + (int64_t)rc.s0 * 36;
+      for (int64_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+      int* cdst = reinterpret_cast<int*>(dst + n);
+      for (int64_t i = threadIdx.x; i < ns; i += blockDim.x) cdst[i] = a.row_col[rc.s0 + i];
+      rc.Bs = dst;
+      rc.cols = cdst - rc.s0;
+    }
+  }
+  __syncthreads();
+  // rows of this warp: rc.r0 + wid + PCG_WARPS * j, j < nrow (<= PCG_RMAX)
+  const int nrow = rc.r1 > rc.r0 + wid ? (rc.r1 - rc.r0 - wid + PCG_WARPS - 1) / PCG_WARPS : 0;
+  double xr[PCG_RMAX], rr_[PCG_RMAX], zr[PCG_RMAX], br[PCG_RMAX], idr[PCG_RMAX], pr[PCG_RMAX],
+      apr[PCG_RMAX];
+#pragma unroll
+  for (int j = 0; j < PCG_RMAX; ++j) xr[j] = rr_[j] = zr[j] = br[j] = idr[j] = pr[j] = apr[j] = 0.0;
+  double* pa = a.p;   // p of the previous iteration (read by neighbours)
+  double* pb = a.p2;  // p of this iteration (written by owners)
+  double* partA = a.part;
+  double* partB = a.part + G;
+
+  // ---- setup (solver.py:472-481)
+  {
+    double v[2] = {0.0, 0.0};
+    for (int j = 0; j < nrow; ++j) {
+      const int row = rc.r0 + wid + PCG_WARPS * j;
+      double bb = 0.0, bz = 0.0;
+      if (own) {
+        const int i = 6 * row + lane;
+        const double bi = -a.g[i];
+        const double inv = 1.0 / fmax(a.jdiag[i], 1e-12);
+        const double zi = inv * bi;
+        rset(br, j, bi);
+        rset(idr, j, inv);
+        rset(rr_, j, bi);
+        rset(zr, j, zi);
+        rset(pr, j, zi);
+        a.z[i] = zi;
+        pa[i] = zi;
+        bb = bi * bi;
+        bz = bi * zi;
+      }
+      v[0] += sum6(bb);
+      v[1] += sum6(bz);
+    }
+    block_allsum<2>(v, sh);
+    if (threadIdx.x == 0) { partB[blockIdx.x] = v[0]; partB[G + blockIdx.x] = v[1]; }
+  }
+  grid.sync(G);
+  double tot[2];
+  grid_allsum<2>(partB, tot, G);
+  const double norm_b = sqrt(tot[0]);
+  double rz = tot[1];
+  int iterations = 0;
+  double relative = 1.0;
+  int status = 0;
+  double beta = 0.0;
+  bool fold = false;
+  if (norm_b == 0.0) {
+    relative = 0.0;
+  } else {
+    for (int k = 1; k <= a.max_it; ++k) {
+      iterations = k;
+      TRACE(k, 0);
+      {
+        double v[1] = {0.0};
+        for (int j = 0; j < nrow; ++j) {
+          const int row = rc.r0 + wid + PCG_WARPS * j;
+          const double y = fold ? mv.template row<true>(a, rc, row, a.z, pa, beta, lane)
+                                : mv.template row<false>(a, rc, row, a.z, pa, beta, lane);
+          double pAp = 0.0;
+          if (own) {
+            const double pold = rsel(pr, j);
+            const double pi = fold ? fma(beta, pold, rsel(zr, j)) : pold;
+            pb[6 * row + lane] = pi;
+            rset(pr, j, pi);
+            rset(apr, j, y);
+            pAp = pi * y;
+          }
+          v[0] += sum6(pAp);
+        }
+        TRACE(k, 1);
+        block_allsum<1>(v, sh);
+        if (threadIdx.x == 0) partA[blockIdx.x] = v[0];
+      }
+      grid.sync(G);
+      double pAp_a[1];
+      grid_allsum<1>(partA, pAp_a, G);
+      TRACE(k, 2);
+      const double pAp = pAp_a[0];
+      if (!isfinite(pAp)) { status = 1; break; }
+      if (pAp <= 0.0) break;
+      const double alpha = rz / pAp;
+      const bool restart = (k % a.restart) == 0;
+      {
+        double v[3] = {0.0, 0.0, 0.0};
+        for (int j = 0; j < nrow; ++j) {
+          const int row = rc.r0 + wid + PCG_WARPS * j;
+          double rrv = 0.0, rzv = 0.0, bad = 0.0;
+          if (own) {
+            const int i = 6 * row + lane;
+            const double xi = fma(alpha, rsel(pr, j), rsel(xr, j));
+            rset(xr, j, xi);
+            bad = isfinite(xi) ? 0.0 : 1.0;
+            if (restart) {
+              a.x[i] = xi;  // read by the neighbours' r = b - A x
+            } else {
+              const double ri = fma(-alpha, rsel(apr, j), rsel(rr_, j));
+              const double zi = rsel(idr, j) * ri;
+              rset(rr_, j, ri);
+              rset(zr, j, zi);
+              a.z[i] = zi;
+              rrv = ri * ri;
+              rzv = ri * zi;
+            }
+          }
+          v[0] += sum6(rrv);
+          v[1] += sum6(rzv);
+          v[2] += sum6(bad);
+        }
+        if (restart) {
+          grid.sync(G);  // x complete
+          for (int j = 0; j < nrow; ++j) {
+            const int row = rc.r0 + wid + PCG_WARPS * j;
+            const double y = mv.template row<false>(a, rc, row, nullptr, a.x, 0.0, lane);
+            double rrv = 0.0, rzv = 0.0;
+            if (own) {
+              const double ri = rsel(br, j) - y;
+              const double zi = rsel(idr, j) * ri;
+              rset(rr_, j, ri);
+              rset(zr, j, zi);
+              a.z[6 * row + lane] = zi;
+              rrv = ri * ri;
+              rzv = ri * zi;
+            }
+            v[0] += sum6(rrv);
+            v[1] += sum6(rzv);
+          }
+        }
+        TRACE(k, 3);
+        block_allsum<3>(v, sh);
+        if (threadIdx.x == 0) {
+#pragma unroll
+          for (int q = 0; q < 3; ++q) partB[q * G + blockIdx.x] = v[q];
+        }
+      }
+      grid.sync(G);
+      double s3[3];
+      grid_allsum<3>(partB, s3, G);
+      TRACE(k, 4);
+      if (s3[2] != 0.0) { status = 1; break; }
+      relative = sqrt(s3[0]) / norm_b;
+      if (relative < a.tol) break;
+      const double rz_new = s3[1];
+      beta = rz_new / rz;
+      rz = rz_new;
+      double* t = pa;
+      pa = pb;
+      pb = t;
+      fold = true;
+    }
+  }
+  for (int j = 0; j < nrow; ++j)
+    if (own) a.x[6 * (rc.r0 + wid + PCG_WARPS * j) + lane] = rsel(xr, j);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    a.out_scalars[0] = (double)iterations;
+    a.out_scalars[1] = relative;
+    a.out_scalars[2] = (double)status;
+  }
+}
+
 template <class Mv>
 static cudaError_t launch_pcg_t(const PcgArgs& a, Mv mv, int n_sm, cudaStream_t s) {
   static bool attr_set = false;
@@ -388,6 +626,10 @@ static cudaError_t launch_pcg_t(const PcgArgs& a, Mv mv, int n_sm, cudaStream_t 
     e = cudaFuncSetAttribute(k_pcg<BsrMv>, cudaFuncAttributeMaxDynamicSharedMemorySize, PCG_SMEM_BYTES);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k_pcg<DenseMv>, cudaFuncAttributeMaxDynamicSharedMemorySize, PCG_SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_pcg_reg<BsrMv>, cudaFuncAttributeMaxDynamicSharedMemorySize, PCG_SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_pcg_reg<DenseMv>, cudaFuncAttributeMaxDynamicSharedMemorySize, PCG_SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
@@ -410,8 +652,12 @@ static cudaError_t launch_pcg_t(const PcgArgs& a, Mv mv, int n_sm, cudaStream_t 
   e = cudaMemsetAsync(a.flags, 0, sizeof(unsigned), s);  // grid barrier counter
   if (e != cudaSuccess) return e;
   sfb_count_launch();
-  return cudaLaunchCooperativeKernel((void*)k_pcg<Mv>, dim3(G), dim3(PCG_THREADS), params,
-                                     PCG_SMEM_BYTES, s);
+#ifndef PCG_REG
+#define PCG_REG 1
+#endif
+  const bool reg = PCG_REG && rows_per_cta <= PCG_WARPS * PCG_RMAX;
+  return cudaLaunchCooperativeKernel(reg ? (void*)k_pcg_reg<Mv> : (void*)k_pcg<Mv>, dim3(G),
+                                     dim3(PCG_THREADS), params, PCG_SMEM_BYTES, s);
 }
 
 cudaError_t launch_pcg(const PcgArgs& a, int n_sm, cudaStream_t s) {
