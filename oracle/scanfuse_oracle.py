@@ -529,3 +529,56 @@ def max_residual_set(poses, sets):
         if peak > worst:
             worst, worst_set = peak, idx
     return worst_set, worst
+
+
+# --------------------------------------------------------------------------
+# dense_verify (filters.py:200-277)
+
+
+def bilinear1(img, x, y):
+    """bilinear_sample (interp.py:17-33) of a single-channel image, with
+    _corner_indices (interp.py:8-14); NumPy evaluation order."""
+    img = np.asarray(img)
+    h, w = img.shape[:2]
+    x = np.clip(np.asarray(x, float), 0.0, w - 1.0)
+    y = np.clip(np.asarray(y, float), 0.0, h - 1.0)
+    x0 = np.minimum(np.floor(x), w - 2).astype(int)
+    y0 = np.minimum(np.floor(y), h - 2).astype(int)
+    fx, fy = x - x0, y - y0
+    return (img[y0, x0] * (1 - fx) * (1 - fy) + img[y0, x0 + 1] * fx * (1 - fy)
+            + img[y0 + 1, x0] * (1 - fx) * fy + img[y0 + 1, x0 + 1] * fx * fy)
+
+
+def verify_one_direction(src, dst, T, depth_max=0.15, normal_min=0.9, color_max=0.1):
+    """_verify_one_direction (filters.py:216-250): (mean_error, count).
+    T = (R, t) maps src camera space into dst camera space."""
+    eligible = src.valid_depth & src.valid_normal
+    if not np.any(eligible):
+        return 0.0, 0
+    pts = src.points_low[eligible].astype(np.float64)
+    nrm = src.normals_low[eligible].astype(np.float64)
+    inten = src.intensity_low[eligible].astype(np.float64)
+    moved = pts @ T[0].T + T[1]
+    k = dst.intrinsics_low
+    u, v, front = project(k, moved)
+    xi = np.round(u).astype(int)
+    yi = np.round(v).astype(int)
+    inside = front & (xi >= 0) & (xi < k.width) & (yi >= 0) & (yi < k.height)
+    xi, yi = np.clip(xi, 0, k.width - 1), np.clip(yi, 0, k.height - 1)
+    ok = dst.valid_depth[yi, xi] & dst.valid_normal[yi, xi] & inside
+    dist = np.linalg.norm(moved - dst.points_low[yi, xi].astype(np.float64), axis=1)
+    ndot = np.sum((nrm @ T[0].T) * dst.normals_low[yi, xi].astype(np.float64), axis=1)
+    cdiff = np.abs(inten - bilinear1(dst.intensity_low, u, v))
+    good = ok & (dist < depth_max) & (ndot > normal_min) & (cdiff < color_max)
+    count = int(np.count_nonzero(good))
+    return (float(dist[good].sum() / count) if count else 0.0), count
+
+
+def dense_verify(ci, cj, T, depth_max=0.15, normal_min=0.9, color_max=0.1, error_max=0.075,
+                 min_fraction=0.02):
+    """dense_verify (filters.py:253-277): (passed, err_ij, err_ji, count_ij, count_ji)."""
+    e1, n1 = verify_one_direction(ci, cj, T, depth_max, normal_min, color_max)
+    e2, n2 = verify_one_direction(cj, ci, inv(T), depth_max, normal_min, color_max)
+    k = ci.intrinsics_low
+    m = min_fraction * k.width * k.height
+    return (n1 >= m and n2 >= m and e1 <= error_max and e2 <= error_max), e1, e2, n1, n2

@@ -55,6 +55,10 @@ class Rounding(C.Structure):
                 ("matvec_c", "matvec_f", "gemm33", "apply_n", "apply_1", "dot3")]
 
 
+class VerifyConfig(C.Structure):
+    _fields_ = [("depth_max", C.c_double), ("normal_min", C.c_double), ("color_max", C.c_double)]
+
+
 class IterResult(C.Structure):
     _fields_ = [
         ("e_sparse", C.c_double), ("e_photo", C.c_double), ("e_geo", C.c_double),
@@ -122,6 +126,8 @@ SIGNATURES = {
     "sfb_profile": [_P, _I32],
     "sfb_profile_read": [_P, _P, _P, _I32],
     "sfb_launch_count": [C.POINTER(_I64)],
+    "sfb_frames_set_intensity": [_P, _I32, _P, _P],
+    "sfb_dense_verify": [_P, _I32, _P, _P, _P, _P, _P, _P, C.POINTER(VerifyConfig), _P, _P],
 }
 
 PROF_CLASSES = ("dense_linearize", "frozen_energy", "pcg", "pair_filter", "sparse_term",

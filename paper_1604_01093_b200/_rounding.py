@@ -21,7 +21,8 @@ from fractions import Fraction
 import numpy as np
 
 PERMS = [(0, 1, 2), (0, 2, 1), (1, 0, 2), (1, 2, 0), (2, 0, 1), (2, 1, 0)]
-DEFAULT = dict(matvec_c=2, matvec_f=0, gemm33=0, apply_n=0, apply_1=2, dot3=0)
+DEFAULT = dict(matvec_c=2, matvec_f=0, gemm33=0, apply_n=0, apply_1=2, dot3=0,
+               apply_nf=0, apply_1f=2)
 
 
 def _fma(a: float, b: float, c: float) -> float:
@@ -79,6 +80,20 @@ def _apply_1(a, b, rng):
     return float((a[None, :] @ R.T)[0, 0])
 
 
+def _apply_nf(a, b, rng):  # Fortran-ordered rotation (dense_verify's caller transform)
+    P = rng.normal(size=(64, 3))
+    R = np.asfortranarray(rng.normal(size=(3, 3)))
+    P[17] = a
+    R[2] = b
+    return float((P @ R.T)[17, 2])
+
+
+def _apply_1f(a, b, rng):
+    R = np.asfortranarray(rng.normal(size=(3, 3)))
+    R[0] = b
+    return float((a[None, :] @ R.T)[0, 0])
+
+
 def _dot(a, b, rng):
     return float(np.dot(a, b))
 
@@ -88,7 +103,8 @@ def probe(trials: int = 300) -> dict:
     rng = np.random.default_rng(20160404)
     out = {}
     for name, fn in (("matvec_c", _mv_c), ("matvec_f", _mv_f), ("gemm33", _gemm),
-                     ("apply_n", _apply_n), ("apply_1", _apply_1), ("dot3", _dot)):
+                     ("apply_n", _apply_n), ("apply_1", _apply_1), ("dot3", _dot),
+                     ("apply_nf", _apply_nf), ("apply_1f", _apply_1f)):
         alive = _survivors(trials, fn, rng)
         if alive:
             out[name] = DEFAULT[name] if DEFAULT[name] in alive else min(alive)

@@ -194,6 +194,8 @@ struct Slot {
   FrameDev dev;
   void* block = nullptr;
   bool alive = false;
+  float* intensity = nullptr;  // owned (dev_cache), dense_verify only
+  size_t intensity_bytes = 0;
 };
 
 }  // namespace
@@ -208,6 +210,9 @@ struct sfb_ctx : Handle {
   DBuf<uint8_t> staging;
   DBuf<int> counts;
   DBuf<PackArgs> pack_args;
+  DBuf<VerifyItem> verify_items;
+  DBuf<double> verify_err;
+  DBuf<long long> verify_cnt;
   std::map<void*, size_t> block_size;
   std::multimap<size_t, void*> free_blocks;  // released frame blocks kept for reuse
   size_t cached_bytes = 0;
@@ -746,6 +751,11 @@ int sfb_ctx_destroy(sfb_ctx* c) {
   cudaStreamSynchronize(c->stream);
   for (auto& kv : c->block_refs) cudaFree(kv.first);
   for (auto& kv : c->free_blocks) cudaFree(kv.second);
+  for (auto& sl : c->slots)
+    if (sl.intensity) dev_cache().release(sl.intensity, sl.intensity_bytes);
+  c->verify_items.release();
+  c->verify_err.release();
+  c->verify_cnt.release();
   c->pack_args.release();
   c->staging.release();
   c->counts.release();
@@ -908,6 +918,13 @@ int sfb_frames_release(sfb_ctx* c, int32_t n, const int32_t* slots) {
     if (s < 0 || s >= (int)c->slots.size() || !c->slots[s].alive) continue;
     Slot& sl = c->slots[s];
     sl.alive = false;
+    if (sl.intensity) {
+      cudaStreamSynchronize(c->stream);  // a dense_verify may still read it
+      dev_cache().release(sl.intensity, sl.intensity_bytes);
+      sl.intensity = nullptr;
+      sl.intensity_bytes = 0;
+      sl.dev.I = nullptr;
+    }
     auto it = c->block_refs.find(sl.block);
     if (it != c->block_refs.end() && --it->second == 0) {
       // keep the block for reuse; problems still referencing it were
@@ -927,6 +944,81 @@ int sfb_frames_release(sfb_ctx* c, int32_t n, const int32_t* slots) {
     }
     sl.block = nullptr;
   }
+  return SFB_OK;
+}
+
+int sfb_frames_set_intensity(sfb_ctx* c, int32_t n, const int32_t* slots,
+                             const float* const* intensity) {
+  if (!c || n < 0 || (n > 0 && (!slots || !intensity))) return fail(c, SFB_E_ARG, "bad arguments");
+  CK(c, cudaSetDevice(c->device));
+  for (int k = 0; k < n; ++k) {
+    const int s = slots[k];
+    if (s < 0 || s >= (int)c->slots.size() || !c->slots[s].alive)
+      return fail(c, SFB_E_ARG, "slot " + std::to_string(s) + " is not resident");
+    if (!intensity[k]) return fail(c, SFB_E_ARG, "null intensity plane");
+    Slot& sl = c->slots[s];
+    const size_t bytes = (size_t)sl.dev.w * sl.dev.h * sizeof(float);
+    if (!sl.intensity) {
+      void* p = nullptr;
+      CK(c, dev_cache().alloc(&p, bytes));
+      sl.intensity = static_cast<float*>(p);
+      sl.intensity_bytes = bytes;
+    }
+    CK(c, cudaMemcpyAsync(sl.intensity, intensity[k], bytes, cudaMemcpyHostToDevice, c->stream));
+    sl.dev.I = sl.intensity;
+  }
+  CK(c, cudaStreamSynchronize(c->stream));  // host planes are borrowed for the call only
+  return SFB_OK;
+}
+
+int sfb_dense_verify(sfb_ctx* c, int32_t n_items, const int32_t* src_slots,
+                     const int32_t* dst_slots, const double* R9, const double* t3,
+                     const int32_t* ord_n, const int32_t* ord_1, const sfb_verify_config* cfg,
+                     double* err_out, int64_t* count_out) {
+  if (!c || n_items < 0 || !cfg) return fail(c, SFB_E_ARG, "bad arguments");
+  if (n_items == 0) return SFB_OK;
+  if (!src_slots || !dst_slots || !R9 || !t3 || !ord_n || !ord_1 || !err_out || !count_out)
+    return fail(c, SFB_E_ARG, "null argument");
+  CK(c, cudaSetDevice(c->device));
+  std::vector<VerifyItem> items(n_items);
+  int max_hw = 1;
+  for (int k = 0; k < n_items; ++k) {
+    const int ss = src_slots[k], ds = dst_slots[k];
+    for (int s : {ss, ds}) {
+      if (s < 0 || s >= (int)c->slots.size() || !c->slots[s].alive)
+        return fail(c, SFB_E_ARG, "slot " + std::to_string(s) + " is not resident");
+      if (!c->slots[s].intensity)
+        return fail(c, SFB_E_ARG, "slot " + std::to_string(s) + " has no intensity plane");
+    }
+    if (ord_n[k] < 0 || ord_n[k] > 5 || ord_1[k] < 0 || ord_1[k] > 5)
+      return fail(c, SFB_E_ARG, "rounding code out of range");
+    VerifyItem& it = items[k];
+    it.src = c->slots[ss].dev;
+    it.dst = c->slots[ds].dev;
+    for (int q = 0; q < 9; ++q) it.R[q] = R9[9 * (size_t)k + q];
+    for (int q = 0; q < 3; ++q) it.t[q] = t3[3 * (size_t)k + q];
+    it.ord_n = ord_n[k];
+    it.ord_1 = ord_1[k];
+    max_hw = std::max(max_hw, it.src.w * it.src.h);
+  }
+  if (max_hw > verify_max_pixels())
+    return fail(c, SFB_E_ARG, "dense_verify supports frames of at most " +
+                                  std::to_string(verify_max_pixels()) + " pixels");
+  CK(c, c->verify_items.ensure(n_items));
+  CK(c, c->verify_err.ensure(n_items));
+  CK(c, c->verify_cnt.ensure(n_items));
+  CK(c, cudaMemcpyAsync(c->verify_items.p, items.data(), sizeof(VerifyItem) * n_items,
+                        cudaMemcpyHostToDevice, c->stream));
+  const VerifyCfg vc{cfg->depth_max, cfg->normal_min, cfg->color_max};
+  CK(c, launch_dense_verify(c->verify_items.p, n_items, max_hw, vc, c->verify_err.p,
+                            c->verify_cnt.p, c->stream));
+  CK(c, cudaMemcpyAsync(err_out, c->verify_err.p, sizeof(double) * n_items, cudaMemcpyDeviceToHost,
+                        c->stream));
+  std::vector<long long> cnt(n_items);
+  CK(c, cudaMemcpyAsync(cnt.data(), c->verify_cnt.p, sizeof(long long) * n_items,
+                        cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaStreamSynchronize(c->stream));
+  for (int k = 0; k < n_items; ++k) count_out[k] = cnt[k];
   return SFB_OK;
 }
 

@@ -28,6 +28,7 @@ struct FrameDev {
   const double4* tiles;
   const int* tile_count;
   int tiles_x, tiles_y;
+  const float* I;     // intensity_low (dense_verify only), null until uploaded
 };
 
 #define SFB_TILE 16

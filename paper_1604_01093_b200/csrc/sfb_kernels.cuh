@@ -99,6 +99,16 @@ struct PcgArgs {
   const double* skip;  // optional: skip when *skip != 0
 };
 
+// dense_verify (filters.py:216-277): one item = one direction of one pair
+struct VerifyItem {
+  FrameDev src, dst;
+  double R[9], t[3];  // transform src -> dst (row-major R)
+  int ord_n, ord_1;   // NumPy (m,3) @ R.T FMA chain order for m > 1 / m == 1
+};
+struct VerifyCfg {
+  double depth_max, normal_min, color_max;
+};
+
 // Library-wide kernel launch counter (sfb_launch_count).
 void sfb_count_launch(int n = 1);
 
@@ -130,4 +140,7 @@ void launch_associate(const DenseArgs& a, int src, int dst, int kind, uint8_t* s
 void launch_point_eval(const FrameDev* frames, const PoseDev* poses, int src, int dst, int kind,
                        int64_t m, const double* pts, const double* aux, const double* tgts,
                        double* res, double* jac, cudaStream_t s);
+int verify_max_pixels();
+cudaError_t launch_dense_verify(const VerifyItem* items, int n_items, int max_src_hw,
+                                const VerifyCfg& cfg, double* err, long long* cnt, cudaStream_t s);
 void launch_sparse_residuals(const SparseArgs& a, double* res, double* set_max, cudaStream_t s);

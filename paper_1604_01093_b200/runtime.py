@@ -39,9 +39,11 @@ class Runtime:
         h = C.c_void_p()
         _abi.check(self.lib.sfb_ctx_create(device, C.byref(h)))
         self.handle = h
-        r = _abi.Rounding(**probe())
+        pr = probe()
+        r = _abi.Rounding(**{k: pr[k] for k, _ in _abi.Rounding._fields_})
         _abi.check(self.lib.sfb_ctx_set_rounding(h, C.byref(r)), h)
         self._frames: dict[int, tuple[int, object]] = {}
+        self._with_intensity: set[int] = set()  # slots holding intensity_low
         self._lock = threading.Lock()
 
     # -- frame store --------------------------------------------------------
@@ -88,6 +90,27 @@ class Runtime:
             self._frames[id(c)] = (int(s), c)
         del keep
 
+    def intensity_slots_for(self, caches) -> list[int]:
+        """Slots of the caches with their intensity_low plane resident as well
+        (dense_verify's colour gate; the solver path never uploads it)."""
+        slots = self.slots_for(caches)
+        with self._lock:
+            todo, keep, seen = [], [], set()
+            for c, s in zip(caches, slots):
+                if s in self._with_intensity or s in seen:
+                    continue
+                h, w = np.asarray(c.valid_depth).shape
+                keep.append(_plane(c.intensity_low, np.float32, (h, w)))
+                todo.append(s)
+                seen.add(s)
+            if todo:
+                arr = np.asarray(todo, dtype=np.int32)
+                ptrs = (C.c_void_p * len(todo))(*[k.ctypes.data for k in keep])
+                _abi.check(self.lib.sfb_frames_set_intensity(self.handle, len(todo), _abi.ptr(arr),
+                                                             ptrs), self.handle)
+                self._with_intensity.update(todo)
+        return slots
+
     def clear_frames(self) -> None:
         with self._lock:
             if not self._frames:
@@ -96,6 +119,7 @@ class Runtime:
             _abi.check(self.lib.sfb_frames_release(self.handle, len(slots), _abi.ptr(slots)),
                        self.handle)
             self._frames.clear()
+            self._with_intensity.clear()
 
     def __del__(self):
         try:

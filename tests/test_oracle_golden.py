@@ -118,3 +118,20 @@ def test_units_oracle_associations():
             assert np.sum(J ** 2) == pytest.approx(sums[1], rel=1e-10)
             assert np.sum(res2 ** 2) == pytest.approx(sums[2], rel=1e-10)
             np.testing.assert_allclose(J[::9], u[key + "_J"], rtol=1e-9, atol=1e-12)
+
+
+def test_oracle_dense_verify_matches_reference_golden():
+    """oracle.dense_verify == scanfuse.filters.dense_verify on every golden
+    pair (tests/golden/make_verify_golden.py): counts, pass flags and the mean
+    errors bit-for-bit."""
+    from oracle import scanfuse_oracle as O
+    from paper_1604_01093_b200 import synth
+    sc = synth.make("cfg3")
+    g = load("verify")
+    for k, (a, b) in enumerate(g["pairs"]):
+        R = g["R"][k]
+        R = np.asfortranarray(R) if g["f_order"][k] else np.ascontiguousarray(R)
+        passed, e1, e2, n1, n2 = O.dense_verify(sc.caches[int(a)], sc.caches[int(b)], (R, g["t"][k]))
+        assert passed == bool(g["passed"][k])
+        assert (n1, n2) == (int(g["count_ij"][k]), int(g["count_ji"][k]))
+        assert e1 == g["err_ij"][k] and e2 == g["err_ji"][k]
