@@ -105,29 +105,33 @@ int sfb_frames_upload(sfb_ctx* ctx, int32_t n, const sfb_frame_desc* descs,
 int sfb_frames_release(sfb_ctx* ctx, int32_t n, const int32_t* slots);
 
 /* ---- dense_verify (filters.py:216-277) --------------------------------- */
-/* Gates of FilterConfig (filters.py:41-43). */
+/* Gates of FilterConfig (filters.py:41-43) and NumPy's FMA chain order of
+ * (m,3) @ R.T (RigidTransform.apply, geometry.py:139-142) for a C- or
+ * F-ordered rotation at m > 1 / m == 1 (sfb_rounding codes, host probe). */
 typedef struct {
   double depth_max;   /* verify_depth_max  */
   double normal_min;  /* verify_normal_min */
   double color_max;   /* verify_color_max  */
+  int32_t apply_n, apply_1, apply_nf, apply_1f;
 } sfb_verify_config;
 /* Attach CachedFrame.intensity_low ((h, w) f32, frames.py:38-50) to resident
  * slots; only dense_verify reads it, so the solver path never uploads it. */
 int sfb_frames_set_intensity(sfb_ctx* ctx, int32_t n, const int32_t* slots,
                              const float* const* intensity);
 /* n_items directions of dense_verify, one CTA each: item k reprojects slot
- * src_slots[k] into dst_slots[k] with (R9[9k..], t3[3k..]) =
- * transform.rotation (row-major) / .translation, i.e. _verify_one_direction
- * (filters.py:216-250).  ord_n / ord_1: NumPy's FMA chain order for
- * (m,3) @ rotation.T at m > 1 / m == 1 (sfb_rounding codes; the host picks
- * them from the rotation's memory layout).  Outputs: mean_error and count per
- * item - the count bit-exact, the mean the NumPy pairwise sum of the good
- * distances in row-major order.  The pass/fail rule (filters.py:269-276) is
- * host arithmetic on these.  Synchronous; frames of <= 25,600 pixels. */
+ * src_slots[k] into dst_slots[k] (_verify_one_direction, filters.py:216-250)
+ * with the transform (R9[9k..] row-major rotation, t3[3k..] translation):
+ * flags[k] bit 0 = use its inverse() (geometry.py:135-137, evaluated with
+ * NumPy's rounding: the j -> i direction of filters.py:268), bit 1 = the
+ * caller's rotation array is Fortran-ordered (selects the rounding order).
+ * Outputs per item: mean_error (the NumPy pairwise sum of the good distances
+ * in row-major order / count) and the count, both bit-exact.  The pass/fail
+ * rule (filters.py:269-276) is host arithmetic on these.  Synchronous; source
+ * frames of <= 25,600 pixels. */
 int sfb_dense_verify(sfb_ctx* ctx, int32_t n_items, const int32_t* src_slots,
                      const int32_t* dst_slots, const double* R9, const double* t3,
-                     const int32_t* ord_n, const int32_t* ord_1,
-                     const sfb_verify_config* cfg, double* err_out, int64_t* count_out);
+                     const uint8_t* flags, const sfb_verify_config* cfg, double* err_out,
+                     int64_t* count_out);
 
 /* ---- problem (AlignmentProblem.__init__, solver.py:554-564) ----------- */
 /* n_frames problem frames (slots may be NULL when no caches); n_sets

@@ -56,7 +56,9 @@ class Rounding(C.Structure):
 
 
 class VerifyConfig(C.Structure):
-    _fields_ = [("depth_max", C.c_double), ("normal_min", C.c_double), ("color_max", C.c_double)]
+    _fields_ = [("depth_max", C.c_double), ("normal_min", C.c_double), ("color_max", C.c_double),
+                ("apply_n", C.c_int32), ("apply_1", C.c_int32), ("apply_nf", C.c_int32),
+                ("apply_1f", C.c_int32)]
 
 
 class IterResult(C.Structure):
@@ -127,7 +129,7 @@ SIGNATURES = {
     "sfb_profile_read": [_P, _P, _P, _I32],
     "sfb_launch_count": [C.POINTER(_I64)],
     "sfb_frames_set_intensity": [_P, _I32, _P, _P],
-    "sfb_dense_verify": [_P, _I32, _P, _P, _P, _P, _P, _P, C.POINTER(VerifyConfig), _P, _P],
+    "sfb_dense_verify": [_P, _I32, _P, _P, _P, _P, _P, C.POINTER(VerifyConfig), _P, _P],
 }
 
 PROF_CLASSES = ("dense_linearize", "frozen_energy", "pcg", "pair_filter", "sparse_term",

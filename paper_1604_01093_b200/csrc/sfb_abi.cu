@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <chrono>
 #include <cstdlib>
 #include <atomic>
@@ -189,6 +190,16 @@ struct DBuf {
     n = 0;
   }
 };
+
+// Host twin of dot3o (sfb_internal.cuh): NumPy/OpenBLAS 3-term FMA chain
+// fma(a_k b_k, fma(a_j b_j, a_i * b_i)) for permutation code o.
+double host_dot3o(double a0, double a1, double a2, double b0, double b1, double b2, int o) {
+  static const int P[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+  const double a[3] = {a0, a1, a2}, b[3] = {b0, b1, b2};
+  const int i = P[o][0], j = P[o][1], k = P[o][2];
+  volatile double p = a[i] * b[i];  // rounded product, kept out of the fma
+  return std::fma(a[k], b[k], std::fma(a[j], b[j], (double)p));
+}
 
 struct Slot {
   FrameDev dev;
@@ -973,12 +984,14 @@ int sfb_frames_set_intensity(sfb_ctx* c, int32_t n, const int32_t* slots,
 
 int sfb_dense_verify(sfb_ctx* c, int32_t n_items, const int32_t* src_slots,
                      const int32_t* dst_slots, const double* R9, const double* t3,
-                     const int32_t* ord_n, const int32_t* ord_1, const sfb_verify_config* cfg,
+                     const uint8_t* flags, const sfb_verify_config* cfg,
                      double* err_out, int64_t* count_out) {
   if (!c || n_items < 0 || !cfg) return fail(c, SFB_E_ARG, "bad arguments");
   if (n_items == 0) return SFB_OK;
-  if (!src_slots || !dst_slots || !R9 || !t3 || !ord_n || !ord_1 || !err_out || !count_out)
+  if (!src_slots || !dst_slots || !R9 || !t3 || !flags || !err_out || !count_out)
     return fail(c, SFB_E_ARG, "null argument");
+  for (int32_t o : {cfg->apply_n, cfg->apply_1, cfg->apply_nf, cfg->apply_1f})
+    if (o < 0 || o > 5) return fail(c, SFB_E_ARG, "rounding code out of range");
   CK(c, cudaSetDevice(c->device));
   std::vector<VerifyItem> items(n_items);
   int max_hw = 1;
@@ -990,15 +1003,28 @@ int sfb_dense_verify(sfb_ctx* c, int32_t n_items, const int32_t* src_slots,
       if (!c->slots[s].intensity)
         return fail(c, SFB_E_ARG, "slot " + std::to_string(s) + " has no intensity plane");
     }
-    if (ord_n[k] < 0 || ord_n[k] > 5 || ord_1[k] < 0 || ord_1[k] > 5)
-      return fail(c, SFB_E_ARG, "rounding code out of range");
     VerifyItem& it = items[k];
     it.src = c->slots[ss].dev;
     it.dst = c->slots[ds].dev;
-    for (int q = 0; q < 9; ++q) it.R[q] = R9[9 * (size_t)k + q];
-    for (int q = 0; q < 3; ++q) it.t[q] = t3[3 * (size_t)k + q];
-    it.ord_n = ord_n[k];
-    it.ord_1 = ord_1[k];
+    const bool inv = flags[k] & 1, f_ord = flags[k] & 2;
+    const double* R = R9 + 9 * (size_t)k;
+    const double* t = t3 + 3 * (size_t)k;
+    if (inv) {
+      // RigidTransform.inverse (geometry.py:135-137): R.T.copy() (C-ordered)
+      // and -(R.T) @ t with NumPy's gemv order for R.T's memory layout
+      const int mv = f_ord ? c->rd.mv_c : c->rd.mv_f;
+      for (int r = 0; r < 3; ++r)
+        for (int q = 0; q < 3; ++q) it.R[r * 3 + q] = R[q * 3 + r];
+      for (int r = 0; r < 3; ++r)
+        it.t[r] = -host_dot3o(it.R[r * 3 + 0], it.R[r * 3 + 1], it.R[r * 3 + 2], t[0], t[1], t[2], mv);
+      it.ord_n = cfg->apply_n;
+      it.ord_1 = cfg->apply_1;
+    } else {
+      for (int q = 0; q < 9; ++q) it.R[q] = R[q];
+      for (int q = 0; q < 3; ++q) it.t[q] = t[q];
+      it.ord_n = f_ord ? cfg->apply_nf : cfg->apply_n;
+      it.ord_1 = f_ord ? cfg->apply_1f : cfg->apply_1;
+    }
     max_hw = std::max(max_hw, it.src.w * it.src.h);
   }
   if (max_hw > verify_max_pixels())

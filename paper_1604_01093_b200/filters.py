@@ -62,14 +62,9 @@ class DenseVerifyResult:
         return min(self.valid_count_ij, self.valid_count_ji)
 
 
-def _orders(rotation: np.ndarray) -> tuple[int, int]:
-    """NumPy's FMA chain order of `points @ rotation.T` (m > 1, m == 1) for
-    this rotation's memory layout (RigidTransform.apply, geometry.py:139-142)."""
-    pr = probe()
+def _f_ordered(rotation) -> bool:
     rot = np.asarray(rotation)
-    if rot.flags.f_contiguous and not rot.flags.c_contiguous:
-        return pr["apply_nf"], pr["apply_1f"]
-    return pr["apply_n"], pr["apply_1"]
+    return bool(rot.flags.f_contiguous and not rot.flags.c_contiguous)
 
 
 def dense_verify_many(pairs, config: FilterConfig, error_max: float | None = None,
@@ -78,7 +73,9 @@ def dense_verify_many(pairs, config: FilterConfig, error_max: float | None = Non
 
     `pairs`: iterable of (cache_i, cache_j, transform_ij).  Returns one
     `DenseVerifyResult` per pair, each equal to
-    `dense_verify(cache_i, cache_j, transform_ij, config, error_max)`.
+    `dense_verify(cache_i, cache_j, transform_ij, config, error_max)`.  The
+    j -> i direction uses transform_ij.inverse() evaluated on the device with
+    NumPy's rounding (geometry.py:135-137).
     """
     pairs = list(pairs)
     if not pairs:
@@ -86,32 +83,31 @@ def dense_verify_many(pairs, config: FilterConfig, error_max: float | None = Non
     if error_max is None:
         error_max = config.verify_error_max
     rt = runtime(device)
-    caches = []
-    for ci, cj, _ in pairs:
-        caches.extend((ci, cj))
-    slots = rt.intensity_slots_for(caches)
-    n = 2 * len(pairs)
-    src = np.empty(n, dtype=np.int32)
-    dst = np.empty(n, dtype=np.int32)
-    R9 = np.empty((n, 9), dtype=np.float64)
-    t3 = np.empty((n, 3), dtype=np.float64)
-    ord_n = np.empty(n, dtype=np.int32)
-    ord_1 = np.empty(n, dtype=np.int32)
+    caches = [c for ci, cj, _ in pairs for c in (ci, cj)]
+    slots = np.asarray(rt.intensity_slots_for(caches), dtype=np.int32).reshape(-1, 2)
+    n = len(pairs)
+    R = np.empty((n, 3, 3), dtype=np.float64)
+    t = np.empty((n, 3), dtype=np.float64)
+    fo = np.empty(n, dtype=np.uint8)
     for k, (_, _, T) in enumerate(pairs):
-        si, sj = slots[2 * k], slots[2 * k + 1]
-        # filters.py:267-268: i -> j with transform_ij, j -> i with its inverse()
-        for d, (s, t, X) in enumerate(((si, sj, T), (sj, si, T.inverse()))):
-            q = 2 * k + d
-            src[q], dst[q] = s, t
-            R9[q] = np.asarray(X.rotation, dtype=np.float64).reshape(9)
-            t3[q] = np.asarray(X.translation, dtype=np.float64).reshape(3)
-            ord_n[q], ord_1[q] = _orders(X.rotation)
+        R[k] = T.rotation
+        t[k] = T.translation
+        fo[k] = 2 if _f_ordered(T.rotation) else 0
+    # item 2k: i -> j with transform_ij; item 2k+1: j -> i with its inverse()
+    src = np.ascontiguousarray(slots.reshape(-1))
+    dst = np.ascontiguousarray(slots[:, ::-1].reshape(-1))
+    R9 = np.repeat(R.reshape(n, 9), 2, axis=0)
+    t3 = np.repeat(t, 2, axis=0)
+    flags = np.repeat(fo, 2)
+    flags[1::2] |= 1
+    pr = probe()
     cfg = _abi.VerifyConfig(float(config.verify_depth_max), float(config.verify_normal_min),
-                            float(config.verify_color_max))
-    err = np.zeros(n, dtype=np.float64)
-    cnt = np.zeros(n, dtype=np.int64)
-    _abi.check(rt.lib.sfb_dense_verify(rt.handle, n, _abi.ptr(src), _abi.ptr(dst), _abi.ptr(R9),
-                                       _abi.ptr(t3), _abi.ptr(ord_n), _abi.ptr(ord_1),
+                            float(config.verify_color_max), pr["apply_n"], pr["apply_1"],
+                            pr["apply_nf"], pr["apply_1f"])
+    err = np.zeros(2 * n, dtype=np.float64)
+    cnt = np.zeros(2 * n, dtype=np.int64)
+    _abi.check(rt.lib.sfb_dense_verify(rt.handle, 2 * n, _abi.ptr(src), _abi.ptr(dst),
+                                       _abi.ptr(R9), _abi.ptr(t3), _abi.ptr(flags),
                                        _abi.C.byref(cfg), _abi.ptr(err), _abi.ptr(cnt)),
                rt.handle)
     out = []
