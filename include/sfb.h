@@ -186,6 +186,16 @@ int sfb_pcg_dense(sfb_ctx* ctx, int32_t n, const double* A, const double* rhs,
 /* _apply_step (solver.py:674-677): T <- exp(dx) o T for every variable frame. */
 int sfb_apply_step(sfb_problem* p, double* step_norm);
 /* _energy_with_frozen_associations (solver.py:662-672): raw sums. */
+/* One GN iteration after a linearisation with ONE host round trip
+ * (AlignmentProblem.solve, solver.py:715-750): pcg_solve -> _apply_step
+ * (skipped on the device when the PCG diverged) -> the frozen energy at the
+ * new poses, fused with the next linearisation (w_dense_next) when
+ * relinearize != 0.  out[0] PCG iterations, [1] relative residual, [2] 1 if
+ * PcgDivergenceError, [3] step norm, [4..6] energy after (sparse, photo,
+ * geo raw sums), [7..9] the next linearisation's raw sums. */
+int sfb_gn_step(sfb_problem* p, int32_t pcg_max_it, double pcg_tol, int32_t pcg_restart,
+                const sfb_weights* w, int32_t prev_dense, int32_t relinearize,
+                double w_dense_next, const sfb_config* cfg, double out[10]);
 int sfb_energy_frozen(sfb_problem* p, int32_t dense, double energies_out[3]);
 /* E_after of the previous GN iteration and the next linearisation at the
  * same (current) poses in one fused pass (solver.py:662-672 then :630-660):

@@ -1794,6 +1794,75 @@ int sfb_energy_and_linearize_end(sfb_problem* p, double out6[6]) {
   return SFB_OK;
 }
 
+// One GN iteration after the linearisation, with a single host round trip:
+// pcg_solve (solver.py:463-508) -> _apply_step (:674-677, skipped on the
+// device when the PCG diverged) -> the frozen energy of this linearisation at
+// the new poses (:662-672), fused with the next linearisation when
+// `relinearize` (the GN loop evaluates both at identical poses).
+// out[0] PCG iterations, [1] relative residual, [2] 1 if non-finite,
+// [3] step norm, [4..6] energy after (sparse, photo, geo), [7..9] the next
+// linearisation's energies (relinearize only).
+int sfb_gn_step(sfb_problem* p, int32_t max_it, double tol, int32_t restart, const sfb_weights* w,
+                int32_t prev_dense, int32_t relinearize, double w_dense_next,
+                const sfb_config* cfg, double out[10]) {
+  if (!p || !w || !cfg || !out) return fail(p, SFB_E_ARG, "null argument");
+  if (!p->have_system) return fail(p, SFB_E_STATE, "gn_step before linearize");
+  if (restart < 1) return fail(p, SFB_E_ARG, "pcg_restart_interval must be >= 1");
+  if (p->shard_world > 1) return fail(p, SFB_E_STATE, "sharded problem: use the _begin/_end forms");
+  CK(p, cudaSetDevice(p->ctx->device));
+  cudaStream_t s = p->stream;
+  if (p->n_blk > 0) {
+    PcgArgs a = pcg_args(p);
+    a.max_it = max_it;
+    a.tol = tol;
+    a.restart = restart;
+    a.out_scalars = p->dscal.p + 8;
+    a.skip = nullptr;
+    {
+      ProfScope ps(p->prof, 2, s);
+      CK(p, launch_pcg(a, p->ctx->n_sm, s));
+    }
+    ProfScope ps(p->prof, 6, s);
+    launch_pose_update(p->poses.p, p->n, p->x.p, p->dscal.p + 12, p->dscal.p + 10, s);
+    CKL(p);
+  } else {
+    double z[5] = {0, 0, 0, 0, 0};
+    CK(p, cudaMemcpyAsync(p->dscal.p + 8, z, sizeof(z), cudaMemcpyHostToDevice, s));
+  }
+  p->have_solution = true;
+  int mode = 0;
+  if (relinearize) {
+    int rc = enqueue_linearize(p, w, w_dense_next, cfg, prev_dense ? 1 : 0, &mode);
+    if (rc) return rc;
+    rc = enqueue_linearize_end(p);
+    if (rc) return rc;
+  } else {
+    int rc = enqueue_energy_frozen(p, prev_dense, p->dscal.p + 16);
+    if (rc) return rc;
+  }
+  CK(p, cudaMemcpyAsync(p->hscal, p->dscal.p, 20 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(p, cudaStreamSynchronize(s));
+  const double* h = p->hscal;
+  out[0] = p->n_blk > 0 ? h[8] : 0.0;
+  out[1] = p->n_blk > 0 ? h[9] : 0.0;
+  out[2] = (p->n_blk > 0 && h[10] != 0.0) ? 1.0 : 0.0;
+  out[3] = p->n_blk > 0 ? h[12] : 0.0;
+  if (relinearize) {
+    out[4] = h[0];
+    out[5] = mode == 1 ? h[3] : (mode == 2 ? h[17] : 0.0);
+    out[6] = mode == 1 ? h[4] : (mode == 2 ? h[18] : 0.0);
+    out[7] = h[0];
+    out[8] = h[1];
+    out[9] = h[2];
+  } else {
+    out[4] = h[16];
+    out[5] = h[17];
+    out[6] = h[18];
+    out[7] = out[8] = out[9] = 0.0;
+  }
+  return SFB_OK;
+}
+
 int sfb_energy_and_linearize(sfb_problem* p, const sfb_weights* w, int32_t prev_dense,
                              double w_dense_next, const sfb_config* cfg, double out6[6]) {
   if (p && p->shard_world > 1) return fail(p, SFB_E_STATE, "sharded problem: use the _begin/_end form");
