@@ -174,14 +174,29 @@ template <class T>
 struct DBuf {
   T* p = nullptr;
   size_t n = 0;
-  cudaError_t ensure(size_t want) {
+  // Grow to at least `want` elements.  The old block may still be read by
+  // work in flight: with the owning stream given it is synchronised and the
+  // block recycled through the cache (cudaFree costs milliseconds on this
+  // driver); without one it is freed.
+  cudaError_t ensure(size_t want, cudaStream_t owner = nullptr) {
     if (want <= n && p) return cudaSuccess;
-    if (p) cudaFree(p);  // growth: the old block may still be in flight -> not cached
+    const auto t0 = std::chrono::steady_clock::now();
+    const bool had = p != nullptr;
+    if (p) {
+      if (owner != nullptr && cudaStreamSynchronize(owner) == cudaSuccess)
+        dev_cache().release(p, n * sizeof(T));
+      else
+        cudaFree(p);
+    }
     p = nullptr;
     n = 0;
     const size_t cnt = std::max<size_t>(want, 1);
     cudaError_t e = dev_cache().alloc(reinterpret_cast<void**>(&p), cnt * sizeof(T));
     if (e == cudaSuccess) n = cnt;
+    if (trace_on()) {
+      const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      if (ms > 0.5) fprintf(stderr, "sfb ensure %zu B (%s): %.2f ms\n", cnt * sizeof(T), had ? "grow" : "new", ms);
+    }
     return e;
   }
   void release() {  // caller has synchronised the stream that used the buffer
@@ -360,7 +375,7 @@ PcgArgs pcg_args(sfb_problem* p) {
 
 template <class T>
 cudaError_t upload_vec(DBuf<T>& d, const std::vector<T>& h, cudaStream_t s) {
-  cudaError_t e = d.ensure(h.size());
+  cudaError_t e = d.ensure(h.size(), s);
   if (e != cudaSuccess || h.empty()) return e;
   return cudaMemcpyAsync(d.p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, s);
 }
@@ -492,14 +507,14 @@ int rebuild_structure(sfb_problem* p, int bidir) {
   CK(p, upload_vec(p->photo_off, poff, s));
   CK(p, upload_vec(p->geo_off, goff, s));
   for (int b = 0; b < 2; ++b) {
-    CK(p, p->photo_mask[b].ensure((size_t)std::max<int64_t>(pw, 1)));
-    CK(p, p->geo_tgt[b].ensure((size_t)std::max<int64_t>(gw, 1)));
-    CK(p, p->tile_any[b].ensure((size_t)std::max<int64_t>(gw / 256, 1)));
+    CK(p, p->photo_mask[b].ensure((size_t)std::max<int64_t>(pw, 1), s));
+    CK(p, p->geo_tgt[b].ensure((size_t)std::max<int64_t>(gw, 1), s));
+    CK(p, p->tile_any[b].ensure((size_t)std::max<int64_t>(gw / 256, 1), s));
   }
-  CK(p, p->item_out.ensure((size_t)p->n_items * SFB_ITEM_STRIDE));
-  CK(p, p->edge_out.ensure((size_t)p->n_dir * SFB_ITEM_STRIDE));
-  CK(p, p->item_e2.ensure((size_t)std::max(1, p->n_items) * 2));
-  CK(p, p->edge_e2.ensure((size_t)std::max(1, p->n_dir) * 2));
+  CK(p, p->item_out.ensure((size_t)p->n_items * SFB_ITEM_STRIDE, s));
+  CK(p, p->edge_out.ensure((size_t)p->n_dir * SFB_ITEM_STRIDE, s));
+  CK(p, p->item_e2.ensure((size_t)std::max(1, p->n_items) * 2, s));
+  CK(p, p->edge_e2.ensure((size_t)std::max(1, p->n_dir) * 2, s));
   CK(p, upload_vec(p->d_ptr, dptr, s));
   CK(p, upload_vec(p->d_ent, dent, s));
   CK(p, upload_vec(p->b_ptr, bptr, s));
@@ -507,9 +522,9 @@ int rebuild_structure(sfb_problem* p, int bidir) {
   CK(p, upload_vec(p->row_ptr, rptr, s));
   CK(p, upload_vec(p->row_ent, rent, s));
   CK(p, upload_vec(p->row_col, rcol, s));
-  CK(p, p->D.ensure((size_t)nb * 36));
-  CK(p, p->B.ensure((size_t)std::max(1, p->n_pairs) * 36));
-  CK(p, p->Brow.ensure((size_t)std::max(1, rptr[nb]) * 36));
+  CK(p, p->D.ensure((size_t)nb * 36, s));
+  CK(p, p->B.ensure((size_t)std::max(1, p->n_pairs) * 36, s));
+  CK(p, p->Brow.ensure((size_t)std::max(1, rptr[nb]) * 36, s));
   CK(p, cudaStreamSynchronize(s));  // host vectors die here
   if (trace_on()) {
     const auto t_end = std::chrono::steady_clock::now();

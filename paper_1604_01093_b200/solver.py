@@ -23,6 +23,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
+import operator
+
 import numpy as np
 
 from . import _abi
@@ -100,27 +102,57 @@ def build_sparse_term(corr_sets, frame_to_var) -> SparseTerm:
                       np.repeat(fj, sizes))
 
 
+_get_fi = operator.attrgetter("frame_i")
+_get_fj = operator.attrgetter("frame_j")
+_get_pi = operator.attrgetter("points_i")
+_get_pj = operator.attrgetter("points_j")
+_get_dtype = operator.attrgetter("dtype")
+
+
 def _set_layout(corr_sets, frame_index):
-    """(n_sets,2) problem-frame indices, offsets and stacked points for the ABI."""
+    """(n_sets,2) problem-frame indices, offsets and stacked points for the ABI
+    (build_sparse_term's stacking, solver.py:89-111)."""
     n = len(corr_sets)
     if n == 0:
         return (np.zeros((0, 2), dtype=np.int32), np.zeros(1, dtype=np.int64), np.zeros((0, 3)),
                 np.zeros((0, 3)))
-    frames = np.fromiter((frame_index[f] for cs in corr_sets for f in (cs.frame_i, cs.frame_j)),
-                         dtype=np.int32, count=2 * n).reshape(n, 2)
-    try:  # fast path: every set holds (k,3) arrays
-        pi = [cs.points_i for cs in corr_sets]
-        pj = [cs.points_j for cs in corr_sets]
-        si = np.fromiter((len(a) for a in pi), dtype=np.int64, count=n)
-        sj = np.fromiter((len(b) for b in pj), dtype=np.int64, count=n)
-        pts_i = np.concatenate(pi).astype(np.float64, copy=False)
-        pts_j = np.concatenate(pj).astype(np.float64, copy=False)
-        ok = pts_i.shape == (int(si.sum()), 3) and pts_j.shape == (int(sj.sum()), 3)
-    except (ValueError, TypeError):
-        ok = False
-    if not ok:
-        pi = [np.asarray(cs.points_i, dtype=np.float64).reshape(-1, 3) for cs in corr_sets]
-        pj = [np.asarray(cs.points_j, dtype=np.float64).reshape(-1, 3) for cs in corr_sets]
+    fi = np.fromiter(map(_get_fi, corr_sets), dtype=np.int64, count=n)
+    fj = np.fromiter(map(_get_fj, corr_sets), dtype=np.int64, count=n)
+    keys = np.fromiter(frame_index.keys(), dtype=np.int64, count=len(frame_index))
+    vals = np.fromiter(frame_index.values(), dtype=np.int64, count=len(frame_index))
+    if keys.size and keys.min() >= 0 and keys.max() < 16 * keys.size + 1024:
+        lut = np.full(int(keys.max()) + 1, -1, dtype=np.int64)
+        lut[keys] = vals
+        ok_ids = (fi >= 0) & (fi < lut.size) & (fj >= 0) & (fj < lut.size)
+        if not ok_ids.all():
+            raise KeyError("correspondence set references a frame outside the problem")
+        fi, fj = lut[fi], lut[fj]
+        if (fi < 0).any() or (fj < 0).any():
+            raise KeyError("correspondence set references a frame outside the problem")
+    else:
+        fi = np.fromiter((frame_index[int(f)] for f in fi), dtype=np.int64, count=n)
+        fj = np.fromiter((frame_index[int(f)] for f in fj), dtype=np.int64, count=n)
+    frames = np.stack([fi, fj], axis=1).astype(np.int32)
+    pi = list(map(_get_pi, corr_sets))
+    pj = list(map(_get_pj, corr_sets))
+    si = np.fromiter(map(len, pi), dtype=np.int64, count=n)
+    sj = np.fromiter(map(len, pj), dtype=np.int64, count=n)
+    tot = int(si.sum())
+    pts_i = pts_j = None
+    try:
+        # fast path: one C-level join of the raw buffers (about 2x faster than
+        # np.concatenate); requires float64 arrays (checked), C-contiguous
+        # (bytes.join raises BufferError otherwise) and (k, 3) (byte count)
+        if set(map(_get_dtype, pi)) | set(map(_get_dtype, pj)) == {np.dtype(np.float64)}:
+            bi, bj = b"".join(pi), b"".join(pj)
+            if len(bi) == 24 * tot and len(bj) == 24 * int(sj.sum()):
+                pts_i = np.frombuffer(bi, dtype=np.float64).reshape(-1, 3)
+                pts_j = np.frombuffer(bj, dtype=np.float64).reshape(-1, 3)
+    except (AttributeError, TypeError, BufferError, ValueError):
+        pts_i = pts_j = None
+    if pts_i is None:
+        pi = [np.asarray(cs, dtype=np.float64).reshape(-1, 3) for cs in pi]
+        pj = [np.asarray(cs, dtype=np.float64).reshape(-1, 3) for cs in pj]
         si = np.fromiter((a.shape[0] for a in pi), dtype=np.int64, count=n)
         sj = np.fromiter((b.shape[0] for b in pj), dtype=np.int64, count=n)
         pts_i, pts_j = np.concatenate(pi), np.concatenate(pj)
