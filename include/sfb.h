@@ -104,6 +104,23 @@ int sfb_frames_upload(sfb_ctx* ctx, int32_t n, const sfb_frame_desc* descs,
                       int32_t* slots_out);
 int sfb_frames_release(sfb_ctx* ctx, int32_t n, const int32_t* slots);
 
+/* ---- build_cache (frames.py:75-151) on the device ---------------------- */
+/* n RGB-D frames of width x height (colour (H, W, 3) uint8, depth (H, W)
+ * float32; host pageable, pinned, or device pointers) -> their CachedFrame
+ * planes at low_width x low_height, bit-identical to the reference's NumPy
+ * float32 pipeline (block-mean luminance, block-median depth, unprojection,
+ * central-difference normals, gradient).  k_low = intrinsics.scaled(low_w,
+ * low_h) as (fx, fy, cx, cy); luma_order = the host's float32 BLAS FMA chain
+ * order of RgbdFrame.luminance (sfb_rounding code).  The planes become
+ * resident frame slots (slots_out, with intensity_low attached, as if
+ * uploaded by sfb_frames_upload + sfb_frames_set_intensity) and are copied
+ * to host_out: per frame 42*h*w bytes = intensity f32 | depth f32 |
+ * points f32x3 | normals f32x3 | grad f32x2 | valid_depth u8 | valid_normal u8.
+ * Blocks of at most 64 samples.  Synchronous. */
+int sfb_build_cache(sfb_ctx* ctx, int32_t n, int32_t width, int32_t height, int32_t low_width,
+                    int32_t low_height, const uint8_t* const* colors, const float* const* depths,
+                    const double* k_low, int32_t luma_order, void* host_out, int32_t* slots_out);
+
 /* ---- dense_verify (filters.py:216-277) --------------------------------- */
 /* Gates of FilterConfig (filters.py:41-43) and NumPy's FMA chain order of
  * (m,3) @ R.T (RigidTransform.apply, geometry.py:139-142) for a C- or

@@ -129,6 +129,7 @@ SIGNATURES = {
     "sfb_profile_read": [_P, _P, _P, _I32],
     "sfb_launch_count": [C.POINTER(_I64)],
     "sfb_frames_set_intensity": [_P, _I32, _P, _P],
+    "sfb_build_cache": [_P, _I32, _I32, _I32, _I32, _I32, _P, _P, _P, _I32, _P, _P],
     "sfb_gn_step": [_P, _I32, _D, _I32, C.POINTER(Weights), _I32, _I32, _D, C.POINTER(Config),
                     _P],
     "sfb_dense_verify": [_P, _I32, _P, _P, _P, _P, _P, C.POINTER(VerifyConfig), _P, _P],

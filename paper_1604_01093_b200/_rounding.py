@@ -98,6 +98,32 @@ def _dot(a, b, rng):
     return float(np.dot(a, b))
 
 
+LUMA = (0.299, 0.587, 0.114)
+
+
+@functools.lru_cache(maxsize=1)
+def probe_luma() -> int:
+    """FMA chain order of RgbdFrame.luminance (frames.py:33-35):
+    (H,W,3) float32 @ (3,) float32, on this host's NumPy/BLAS.  Returns the
+    order code with the fewest mismatches over random 8-bit colours (the
+    float64 emulation of a float32 FMA double-rounds in rare ties)."""
+    rng = np.random.default_rng(33)
+    col = rng.integers(0, 256, size=(32, 96, 3), dtype=np.uint8).astype(np.float32)
+    w = np.array(LUMA).astype(np.float32)
+    got = col @ w
+    c = col.reshape(-1, 3).astype(np.float64)
+    wd = w.astype(np.float64)
+    best, best_bad = 0, None
+    for code, (i, j, k) in enumerate(PERMS):
+        r = (c[:, i] * wd[i]).astype(np.float32).astype(np.float64)
+        r = (c[:, j] * wd[j] + r).astype(np.float32).astype(np.float64)
+        r = (c[:, k] * wd[k] + r).astype(np.float32)
+        bad = int(np.count_nonzero(r != got.reshape(-1)))
+        if best_bad is None or bad < best_bad:
+            best, best_bad = code, bad
+    return best
+
+
 @functools.lru_cache(maxsize=1)
 def probe(trials: int = 300) -> dict:
     rng = np.random.default_rng(20160404)

@@ -237,6 +237,8 @@ struct sfb_ctx : Handle {
   DBuf<int> counts;
   DBuf<PackArgs> pack_args;
   DBuf<VerifyItem> verify_items;
+  DBuf<uint8_t> cache_raw, cache_out;
+  DBuf<CacheFrame> cache_frames;
   DBuf<double> verify_err;
   DBuf<long long> verify_cnt;
   std::map<void*, size_t> block_size;
@@ -780,6 +782,9 @@ int sfb_ctx_destroy(sfb_ctx* c) {
   for (auto& sl : c->slots)
     if (sl.intensity) dev_cache().release(sl.intensity, sl.intensity_bytes);
   c->verify_items.release();
+  c->cache_raw.release();
+  c->cache_out.release();
+  c->cache_frames.release();
   c->verify_err.release();
   c->verify_cnt.release();
   c->pack_args.release();
@@ -877,9 +882,10 @@ int sfb_frames_upload(sfb_ctx* c, int32_t n, const sfb_frame_desc* d, int32_t* s
       // page-locked host planes are read by the pack kernel in place (UVA
       // zero-copy over the host link); pageable ones are staged by DMA
       cudaPointerAttributes at{};
-      if (cudaPointerGetAttributes(&at, srcs[q]) == cudaSuccess && at.type == cudaMemoryTypeHost &&
-          at.devicePointer != nullptr) {
-        use[q] = at.devicePointer;
+      if (cudaPointerGetAttributes(&at, srcs[q]) == cudaSuccess &&
+          ((at.type == cudaMemoryTypeHost && at.devicePointer != nullptr) ||
+           (at.type == cudaMemoryTypeDevice && at.device == c->device))) {
+        use[q] = at.devicePointer;  // device-resident planes (sfb_build_cache) are read in place
         continue;
       }
       cudaGetLastError();
@@ -1060,6 +1066,95 @@ int sfb_dense_verify(sfb_ctx* c, int32_t n_items, const int32_t* src_slots,
                         cudaMemcpyDeviceToHost, c->stream));
   CK(c, cudaStreamSynchronize(c->stream));
   for (int k = 0; k < n_items; ++k) count_out[k] = cnt[k];
+  return SFB_OK;
+}
+
+int sfb_build_cache(sfb_ctx* c, int32_t n, int32_t width, int32_t height, int32_t low_width,
+                    int32_t low_height, const uint8_t* const* colors, const float* const* depths,
+                    const double* k_low, int32_t luma_order, void* host_out, int32_t* slots_out) {
+  if (!c || n < 0 || (n > 0 && (!colors || !depths || !k_low || !host_out || !slots_out)))
+    return fail(c, SFB_E_ARG, "bad arguments");
+  if (n == 0) return SFB_OK;
+  if (low_width < 2 || low_height < 2 || width % low_width || height % low_height)
+    return fail(c, SFB_E_ARG, "frame does not divide into low_width x low_height blocks");
+  if (luma_order < 0 || luma_order > 5) return fail(c, SFB_E_ARG, "rounding code out of range");
+  const int bw = width / low_width, bh = height / low_height;
+  if (bw * bh > 64) return fail(c, SFB_E_ARG, "blocks of more than 64 samples are not supported");
+  CK(c, cudaSetDevice(c->device));
+  cudaStream_t s = c->stream;
+  const size_t HW = (size_t)width * height, hw = (size_t)low_width * low_height;
+  const size_t raw_b = align256(HW * 3) + align256(HW * 4), out_b = 42 * hw;
+  CK(c, c->cache_raw.ensure(raw_b * n, s));
+  CK(c, c->cache_out.ensure(align256(out_b) * n, s));
+  CK(c, c->cache_frames.ensure(n, s));
+  std::vector<CacheFrame> fr(n);
+  for (int k = 0; k < n; ++k) {
+    uint8_t* raw = c->cache_raw.p + raw_b * k;
+    const void* src[2] = {colors[k], depths[k]};
+    void* dst[2] = {raw, raw + align256(HW * 3)};
+    const size_t sz[2] = {HW * 3, HW * 4};
+    const void* use[2];
+    for (int q = 0; q < 2; ++q) {
+      if (!src[q]) return fail(c, SFB_E_ARG, "null frame plane");
+      cudaPointerAttributes at{};
+      if (cudaPointerGetAttributes(&at, src[q]) == cudaSuccess &&
+          ((at.type == cudaMemoryTypeHost && at.devicePointer != nullptr) ||
+           (at.type == cudaMemoryTypeDevice && at.device == c->device))) {
+        use[q] = at.devicePointer;  // pinned (zero-copy) or device-resident input
+        continue;
+      }
+      cudaGetLastError();
+      CK(c, cudaMemcpyAsync(dst[q], src[q], sz[q], cudaMemcpyHostToDevice, s));
+      use[q] = dst[q];
+    }
+    uint8_t* o = c->cache_out.p + align256(out_b) * k;
+    CacheFrame& f = fr[k];
+    f.color = static_cast<const uint8_t*>(use[0]);
+    f.depth_in = static_cast<const float*>(use[1]);
+    f.intensity = reinterpret_cast<float*>(o);
+    f.depth = reinterpret_cast<float*>(o + 4 * hw);
+    f.points = reinterpret_cast<float*>(o + 8 * hw);
+    f.normals = reinterpret_cast<float*>(o + 20 * hw);
+    f.grad = reinterpret_cast<float*>(o + 32 * hw);
+    f.valid = o + 40 * hw;
+    f.valid_n = o + 41 * hw;
+  }
+  CK(c, cudaMemcpyAsync(c->cache_frames.p, fr.data(), sizeof(CacheFrame) * n, cudaMemcpyHostToDevice, s));
+  CacheArgs ca{c->cache_frames.p, width, height, low_width, low_height, bw, bh,
+               k_low[0], k_low[1], k_low[2], k_low[3], luma_order};
+  CK(c, launch_build_cache(ca, n, s));
+  // the planes become resident frame slots (read in place by the pack kernel)
+  std::vector<sfb_frame_desc> d(n);
+  for (int k = 0; k < n; ++k) {
+    d[k].width = low_width;
+    d[k].height = low_height;
+    d[k].fx = k_low[0];
+    d[k].fy = k_low[1];
+    d[k].cx = k_low[2];
+    d[k].cy = k_low[3];
+    d[k].valid_depth = fr[k].valid;
+    d[k].valid_normal = fr[k].valid_n;
+    d[k].points = fr[k].points;
+    d[k].normals = fr[k].normals;
+    d[k].grad = fr[k].grad;
+  }
+  int rc = sfb_frames_upload(c, n, d.data(), slots_out);
+  if (rc) return rc;
+  // intensity_low for dense_verify, then the host image of every plane
+  for (int k = 0; k < n; ++k) {
+    Slot& sl = c->slots[slots_out[k]];
+    if (!sl.intensity) {
+      void* p = nullptr;
+      CK(c, dev_cache().alloc(&p, hw * sizeof(float)));
+      sl.intensity = static_cast<float*>(p);
+      sl.intensity_bytes = hw * sizeof(float);
+    }
+    CK(c, cudaMemcpyAsync(sl.intensity, fr[k].intensity, hw * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    sl.dev.I = sl.intensity;
+    CK(c, cudaMemcpyAsync(static_cast<uint8_t*>(host_out) + out_b * k, fr[k].intensity, out_b,
+                          cudaMemcpyDeviceToHost, s));
+  }
+  CK(c, cudaStreamSynchronize(s));
   return SFB_OK;
 }
 

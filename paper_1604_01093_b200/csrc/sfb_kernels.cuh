@@ -109,6 +109,25 @@ struct VerifyCfg {
   double depth_max, normal_min, color_max;
 };
 
+// build_cache (frames.py:75-151): per-frame device planes
+struct CacheFrame {
+  const uint8_t* color;   // (H, W, 3)
+  const float* depth_in;  // (H, W)
+  float* intensity;       // (h, w)       -- the host image layout, in order:
+  float* depth;           // (h, w)          intensity, depth, points, normals,
+  float* points;          // (h, w, 3)       grad (f32), valid, valid_n (u8)
+  float* normals;         // (h, w, 3)
+  float* grad;            // (h, w, 2)
+  uint8_t* valid;         // (h, w)
+  uint8_t* valid_n;       // (h, w)
+};
+struct CacheArgs {
+  const CacheFrame* frames;
+  int W, H, low_w, low_h, bw, bh;
+  double fx, fy, cx, cy;  // intrinsics.scaled(low_w, low_h)
+  int luma_order;
+};
+
 // Library-wide kernel launch counter (sfb_launch_count).
 void sfb_count_launch(int n = 1);
 
@@ -140,6 +159,7 @@ void launch_associate(const DenseArgs& a, int src, int dst, int kind, uint8_t* s
 void launch_point_eval(const FrameDev* frames, const PoseDev* poses, int src, int dst, int kind,
                        int64_t m, const double* pts, const double* aux, const double* tgts,
                        double* res, double* jac, cudaStream_t s);
+cudaError_t launch_build_cache(const CacheArgs& a, int n_frames, cudaStream_t s);
 int verify_max_pixels();
 cudaError_t launch_dense_verify(const VerifyItem* items, int n_items, int max_src_hw,
                                 const VerifyCfg& cfg, double* err, long long* cnt, cudaStream_t s);

@@ -111,6 +111,14 @@ class Runtime:
                 self._with_intensity.update(todo)
         return slots
 
+    def adopt(self, caches, slots) -> None:
+        """Register caches whose planes were produced on the device
+        (sfb_build_cache): already resident, intensity included."""
+        with self._lock:
+            for c, s in zip(caches, slots):
+                self._frames[id(c)] = (int(s), c)
+                self._with_intensity.add(int(s))
+
     def clear_frames(self) -> None:
         with self._lock:
             if not self._frames:

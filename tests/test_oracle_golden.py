@@ -135,3 +135,21 @@ def test_oracle_dense_verify_matches_reference_golden():
         assert passed == bool(g["passed"][k])
         assert (n1, n2) == (int(g["count_ij"][k]), int(g["count_ji"][k]))
         assert e1 == g["err_ij"][k] and e2 == g["err_ji"][k]
+
+
+def test_host_build_cache_matches_reference_digests():
+    """This package's NumPy build_cache (the scene generator's producer and the
+    GPU test's diagnostic) is bit-identical to scanfuse.frames.build_cache on
+    every golden input (tests/golden/make_cache_golden.py)."""
+    import json
+    import sys as _sys
+    from golden_io import GOLDEN
+    _sys.path.insert(0, str(GOLDEN))
+    from make_cache_golden import PLANES, cache_inputs, digest
+    from paper_1604_01093_b200 import cache as CA
+    from paper_1604_01093_b200 import se3
+    g = json.loads((GOLDEN / "cache_digests.json").read_text())
+    for name, col, dep, (lw, lh), kk in cache_inputs():
+        c = CA.build_cache(CA.RgbdFrame(0, col, dep), se3.Intrinsics(*kk), lw, lh)
+        for p in PLANES:
+            assert digest(getattr(c, p)) == g[name][p], (name, p)
