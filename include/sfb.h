@@ -213,6 +213,14 @@ int sfb_apply_step(sfb_problem* p, double* step_norm);
 int sfb_gn_step(sfb_problem* p, int32_t pcg_max_it, double pcg_tol, int32_t pcg_restart,
                 const sfb_weights* w, int32_t prev_dense, int32_t relinearize,
                 double w_dense_next, const sfb_config* cfg, double out[10]);
+/* The same split around the sharded exchange (paper_1604_01093_b200.shard):
+ * _begin enqueues everything up to the per-edge sums and reports which
+ * exchange buffers (bit 0: dense edge sums, bit 1: frozen-energy sums) the
+ * caller must sum across ranks on the problem's stream before _end. */
+int sfb_gn_step_begin(sfb_problem* p, int32_t pcg_max_it, double pcg_tol, int32_t pcg_restart,
+                      const sfb_weights* w, int32_t prev_dense, int32_t relinearize,
+                      double w_dense_next, const sfb_config* cfg, int32_t* exchange);
+int sfb_gn_step_end(sfb_problem* p, double out[10]);
 int sfb_energy_frozen(sfb_problem* p, int32_t dense, double energies_out[3]);
 /* E_after of the previous GN iteration and the next linearisation at the
  * same (current) poses in one fused pass (solver.py:662-672 then :630-660):

@@ -282,6 +282,7 @@ struct sfb_problem : Handle {
   // between the two halves of a (possibly sharded) linearisation / energy
   bool pending_dense_on = false;
   int pending_prev_mode = 0;
+  bool pending_gn_relin = false;
   bool pending_energy_dense = false;
   // data-parallel sharding over directed dense edges
   int shard_rank = 0, shard_world = 1;
@@ -1908,17 +1909,18 @@ int sfb_energy_and_linearize_end(sfb_problem* p, double out6[6]) {
 // pcg_solve (solver.py:463-508) -> _apply_step (:674-677, skipped on the
 // device when the PCG diverged) -> the frozen energy of this linearisation at
 // the new poses (:662-672), fused with the next linearisation when
-// `relinearize` (the GN loop evaluates both at identical poses).
+// `relinearize` (the GN loop evaluates both at identical poses).  Sharded
+// problems exchange the buffers flagged by *exchange between _begin and _end
+// (enqueued on the problem's stream; no host sync in between).
 // out[0] PCG iterations, [1] relative residual, [2] 1 if non-finite,
 // [3] step norm, [4..6] energy after (sparse, photo, geo), [7..9] the next
 // linearisation's energies (relinearize only).
-int sfb_gn_step(sfb_problem* p, int32_t max_it, double tol, int32_t restart, const sfb_weights* w,
-                int32_t prev_dense, int32_t relinearize, double w_dense_next,
-                const sfb_config* cfg, double out[10]) {
-  if (!p || !w || !cfg || !out) return fail(p, SFB_E_ARG, "null argument");
+int sfb_gn_step_begin(sfb_problem* p, int32_t max_it, double tol, int32_t restart,
+                      const sfb_weights* w, int32_t prev_dense, int32_t relinearize,
+                      double w_dense_next, const sfb_config* cfg, int32_t* exchange) {
+  if (!p || !w || !cfg || !exchange) return fail(p, SFB_E_ARG, "null argument");
   if (!p->have_system) return fail(p, SFB_E_STATE, "gn_step before linearize");
   if (restart < 1) return fail(p, SFB_E_ARG, "pcg_restart_interval must be >= 1");
-  if (p->shard_world > 1) return fail(p, SFB_E_STATE, "sharded problem: use the _begin/_end forms");
   CK(p, cudaSetDevice(p->ctx->device));
   cudaStream_t s = p->stream;
   if (p->n_blk > 0) {
@@ -1940,16 +1942,28 @@ int sfb_gn_step(sfb_problem* p, int32_t max_it, double tol, int32_t restart, con
     CK(p, cudaMemcpyAsync(p->dscal.p + 8, z, sizeof(z), cudaMemcpyHostToDevice, s));
   }
   p->have_solution = true;
-  int mode = 0;
+  p->pending_gn_relin = relinearize != 0;
   if (relinearize) {
+    int mode = 0;
     int rc = enqueue_linearize(p, w, w_dense_next, cfg, prev_dense ? 1 : 0, &mode);
     if (rc) return rc;
-    rc = enqueue_linearize_end(p);
-    if (rc) return rc;
+    *exchange = (p->pending_dense_on ? 1 : 0) | (mode == 2 ? 2 : 0);
   } else {
-    int rc = enqueue_energy_frozen(p, prev_dense, p->dscal.p + 16);
+    int rc = enqueue_energy_frozen_begin(p, prev_dense);
     if (rc) return rc;
+    *exchange = p->pending_energy_dense ? 2 : 0;
   }
+  return SFB_OK;
+}
+
+int sfb_gn_step_end(sfb_problem* p, double out[10]) {
+  if (!p || !out) return fail(p, SFB_E_ARG, "null argument");
+  CK(p, cudaSetDevice(p->ctx->device));
+  cudaStream_t s = p->stream;
+  const bool relin = p->pending_gn_relin;
+  const int mode = p->pending_prev_mode;
+  int rc = relin ? enqueue_linearize_end(p) : enqueue_energy_frozen_end(p, p->dscal.p + 16);
+  if (rc) return rc;
   CK(p, cudaMemcpyAsync(p->hscal, p->dscal.p, 20 * sizeof(double), cudaMemcpyDeviceToHost, s));
   CK(p, cudaStreamSynchronize(s));
   const double* h = p->hscal;
@@ -1957,7 +1971,7 @@ int sfb_gn_step(sfb_problem* p, int32_t max_it, double tol, int32_t restart, con
   out[1] = p->n_blk > 0 ? h[9] : 0.0;
   out[2] = (p->n_blk > 0 && h[10] != 0.0) ? 1.0 : 0.0;
   out[3] = p->n_blk > 0 ? h[12] : 0.0;
-  if (relinearize) {
+  if (relin) {
     out[4] = h[0];
     out[5] = mode == 1 ? h[3] : (mode == 2 ? h[17] : 0.0);
     out[6] = mode == 1 ? h[4] : (mode == 2 ? h[18] : 0.0);
@@ -1971,6 +1985,16 @@ int sfb_gn_step(sfb_problem* p, int32_t max_it, double tol, int32_t restart, con
     out[7] = out[8] = out[9] = 0.0;
   }
   return SFB_OK;
+}
+
+int sfb_gn_step(sfb_problem* p, int32_t max_it, double tol, int32_t restart, const sfb_weights* w,
+                int32_t prev_dense, int32_t relinearize, double w_dense_next,
+                const sfb_config* cfg, double out[10]) {
+  if (p && p->shard_world > 1) return fail(p, SFB_E_STATE, "sharded problem: use the _begin/_end forms");
+  int32_t ex = 0;
+  int rc = sfb_gn_step_begin(p, max_it, tol, restart, w, prev_dense, relinearize, w_dense_next, cfg, &ex);
+  if (rc) return rc;
+  return sfb_gn_step_end(p, out);
 }
 
 int sfb_energy_and_linearize(sfb_problem* p, const sfb_weights* w, int32_t prev_dense,

@@ -235,15 +235,22 @@ class DeviceProblem:
             self._ck(self.lib.sfb_energy_frozen_end(self.handle, _abi.ptr(e)))
         return e
 
-    def gn_step(self, weights, prev_dense: bool, relinearize: bool, w_dense_next, config):
+    def gn_step(self, weights, prev_dense: bool, relinearize: bool, w_dense_next, config,
+                exchange=None):
         """PCG -> step -> frozen energy (+ next linearisation) in one round trip.
         Returns (pcg_it, pcg_rel, diverged, step_norm, e_after[3], e_next[3])."""
         out = np.zeros(10)
         w, cfg = self._w(weights), self._cfg(config)
-        self._ck(self.lib.sfb_gn_step(
-            self.handle, int(config.pcg_max_iterations), C.c_double(config.pcg_tolerance),
-            int(config.pcg_restart_interval), C.byref(w), 1 if prev_dense else 0,
-            1 if relinearize else 0, C.c_double(w_dense_next), C.byref(cfg), _abi.ptr(out)))
+        args = (self.handle, int(config.pcg_max_iterations), C.c_double(config.pcg_tolerance),
+                int(config.pcg_restart_interval), C.byref(w), 1 if prev_dense else 0,
+                1 if relinearize else 0, C.c_double(w_dense_next), C.byref(cfg))
+        if exchange is None:
+            self._ck(self.lib.sfb_gn_step(*args, _abi.ptr(out)))
+        else:
+            mask = C.c_int32()
+            self._ck(self.lib.sfb_gn_step_begin(*args, C.byref(mask)))
+            self._exchange(exchange, mask.value)
+            self._ck(self.lib.sfb_gn_step_end(self.handle, _abi.ptr(out)))
         if relinearize:
             self.version += 1
         return int(out[0]), float(out[1]), bool(out[2]), float(out[3]), out[4:7], out[7:10]

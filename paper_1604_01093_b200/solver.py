@@ -747,38 +747,19 @@ class AlignmentProblem:
                     it, energy_before, energy_before, w_dense, 0, 0.0, 0.0, True))
                 break
             more = it + 1 < max_iterations
-            if self._xch is None:
-                # PCG -> step -> E_after (+ the next linearisation, at the same
-                # poses) with one host round trip; the step is skipped on the
-                # device when the PCG diverged
-                pcg_it, pcg_rel, diverged, step_norm, ea, e_nx = dp.gn_step(
-                    weights, w_dense > 0.0, more, dense_ramp_weight(weights, it + 1), config)
-                if diverged:
-                    stats.aborted = True
-                    break
-                moved = True
-                if more:
-                    e_next = e_nx
-                tr.mark("pcg+step+energy")
-            else:
-                pcg_it, pcg_rel, status = dp.pcg(config.pcg_max_iterations, config.pcg_tolerance,
-                                                config.pcg_restart_interval)
-                if status == _abi.SFB_E_PCG_NONFINITE:
-                    stats.aborted = True
-                    break
-                tr.mark("pcg")
-                step_norm = dp.apply_step()
-                moved = True
-                tr.mark("step")
-                if more:
-                    # E_after(it) and the linearisation of it+1 happen at the same
-                    # poses: one fused device pass (discarded if the loop stops).
-                    ea, e_next = dp.energy_and_linearize(
-                        weights, w_dense > 0.0, dense_ramp_weight(weights, it + 1), config,
-                        exchange=self._xch)
-                else:
-                    ea = dp.energy_frozen(w_dense > 0.0, exchange=self._xch)
-                tr.mark("energy+lin")
+            # PCG -> step -> E_after (+ the next linearisation, at the same poses)
+            # with one host round trip; the step is skipped on the device when
+            # the PCG diverged (PcgDivergenceError -> aborted, solver.py:717-719)
+            pcg_it, pcg_rel, diverged, step_norm, ea, e_nx = dp.gn_step(
+                weights, w_dense > 0.0, more, dense_ramp_weight(weights, it + 1), config,
+                exchange=self._xch)
+            if diverged:
+                stats.aborted = True
+                break
+            moved = True
+            if more:
+                e_next = e_nx
+            tr.mark("pcg+step+energy")
             energy_after = weights.sparse * float(ea[0])
             if w_dense > 0.0:
                 energy_after += w_dense * (weights.photo * float(ea[1]) + weights.geo * float(ea[2]))
