@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo lets several ranks share one GPU (protocol test only)")
     return ap.parse_args()
 
 
@@ -340,10 +342,15 @@ def main():
         return
     import torch
     import torch.distributed as dist
-    torch.cuda.set_device(local)
-    os.environ["SFB_DEVICE"] = str(local)
+    dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev)
+    os.environ["SFB_DEVICE"] = str(dev)
+    local = dev
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
 
     from paper_1604_01093_b200 import _abi
     from paper_1604_01093_b200 import solver as S
