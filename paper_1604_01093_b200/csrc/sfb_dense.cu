@@ -272,6 +272,19 @@ __device__ __forceinline__ void bilinear_fast(const FrameDev& f, double x, doubl
 
 #define DENSE_MAX_TILES 1024
 
+#ifdef DENSE_COUNT
+// tuning builds only: pixel counters of the fused pass (sfb_debug_dense_count)
+__device__ unsigned long long g_dense_count[8];
+extern "C" int sfb_debug_dense_count(unsigned long long* out, int reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(out, g_dense_count, sizeof(g_dense_count));
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_dense_count, z, sizeof(z));
+  }
+  return (int)e;
+}
+#endif
+
 // Can any point of this tile's bounding sphere (moved by rel) project into
 // the target frustum widened to [-0.5, w-0.5] x [-0.5, h-0.5], z > 0?  The
 // radius carries a 1e-7 m margin (>> rounding of the exact per-pixel path).
@@ -462,6 +475,25 @@ __global__ void __launch_bounds__(DENSE_THREADS, DENSE_MIN_BLOCKS) k_dense_fused
       const unsigned word = __ballot_sync(0xffffffffu, ph_in);
       if (lane == 0) pmask[m >> 5] = word;
     }
+#ifdef DENSE_COUNT
+    {
+      const unsigned b0 = __ballot_sync(0xffffffffu, live && vis);
+      const unsigned b1 = __ballot_sync(0xffffffffu, ph);
+      const unsigned b2 = __ballot_sync(0xffffffffu, ph_in);
+      const unsigned b3 = __ballot_sync(0xffffffffu, ge);
+      const unsigned b4 = __ballot_sync(0xffffffffu, tgt >= 0);
+      const unsigned b5 = __ballot_sync(0xffffffffu, live && (st & 3u));
+      if (lane == 0) {
+        atomicAdd(&g_dense_count[0], (unsigned long long)__popc(b0));
+        atomicAdd(&g_dense_count[1], (unsigned long long)__popc(b1));
+        atomicAdd(&g_dense_count[2], (unsigned long long)__popc(b2));
+        atomicAdd(&g_dense_count[3], (unsigned long long)__popc(b3));
+        atomicAdd(&g_dense_count[4], (unsigned long long)__popc(b4));
+        atomicAdd(&g_dense_count[5], (unsigned long long)__popc(b5));
+        atomicAdd(&g_dense_count[6], 32ull);
+      }
+    }
+#endif
     if (a.do_geo) gtgt[m] = tgt >= 0 ? (uint16_t)tgt : (uint16_t)0xFFFF;
     if (__ballot_sync(0xffffffffu, ph_in || tgt >= 0) && lane == 0) tile_state[t - it.y] |= 4u;
 
