@@ -121,6 +121,39 @@ int sfb_build_cache(sfb_ctx* ctx, int32_t n, int32_t width, int32_t height, int3
                     int32_t low_height, const uint8_t* const* colors, const float* const* depths,
                     const double* k_low, int32_t luma_order, void* host_out, int32_t* slots_out);
 
+/* ---- hashed TSDF volume (tsdf.py:55-267) ------------------------------ */
+/* TsdfVolume(voxel_size, truncation, depth_weighting): 8x8x8-voxel blocks of
+ * float32 accumulators (weight, weight*distance, weight*colour) in a device
+ * pool; the block dictionary (key -> slot, insertion order) is host memory of
+ * the handle.  Synchronous calls on the context's stream. */
+typedef struct sfb_tsdf sfb_tsdf;
+int sfb_tsdf_create(sfb_ctx* ctx, double voxel_size, double truncation, int32_t depth_weighting,
+                    sfb_tsdf** out);
+int sfb_tsdf_destroy(sfb_tsdf* t);
+/* integrate (sign +1) / deintegrate (sign -1) one RGB-D frame (tsdf.py:90-160):
+ * colour (H, W, 3) uint8, depth (H, W) float32, k4 = (fx, fy, cx, cy),
+ * pose = camera -> world (row-major R, t) with pose_ord = NumPy's FMA order of
+ * (m,3) @ R.T for its layout and m = #valid depth pixels; inv_R/inv_t =
+ * pose.inverse() as NumPy computes it (C-ordered, inv_ord); tvals =
+ * np.linspace(0, 1, n_samples) (_touched_blocks, :162-181).  *status: 0 ok,
+ * 1 "frame has no integrated content", 2 "block err_coord missing during
+ * de-integration", 3 "negative weight in block err_coord" - the reference's
+ * DeintegrationMismatchError, raised at the same block with the same partial
+ * update applied before it. */
+int sfb_tsdf_apply(sfb_tsdf* t, int32_t sign, int32_t width, int32_t height, const uint8_t* color,
+                   const float* depth, const double* k4, const double* pose_R, const double* pose_t,
+                   int32_t pose_ord, const double* inv_R, const double* inv_t, int32_t inv_ord,
+                   const double* tvals, int32_t n_samples, int32_t* status, int64_t* err_coord);
+int sfb_tsdf_count(sfb_tsdf* t, int64_t* n_blocks);
+/* all blocks in insertion order: coords (n,3) int64, weight/wdist (n,512), wcolor (n,512,3) */
+int sfb_tsdf_export(sfb_tsdf* t, int64_t n, int64_t* coords, float* weight, float* wdist,
+                    float* wcolor);
+/* insert or overwrite blocks (TsdfVolume.allocate, load_volume) */
+int sfb_tsdf_import(sfb_tsdf* t, int64_t n, const int64_t* coords, const float* weight,
+                    const float* wdist, const float* wcolor);
+int sfb_tsdf_get_block(sfb_tsdf* t, const int64_t* coord, int32_t* found, float* weight,
+                       float* wdist, float* wcolor);
+
 /* ---- dense_verify (filters.py:216-277) --------------------------------- */
 /* Gates of FilterConfig (filters.py:41-43) and NumPy's FMA chain order of
  * (m,3) @ R.T (RigidTransform.apply, geometry.py:139-142) for a C- or

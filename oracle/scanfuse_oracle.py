@@ -582,3 +582,104 @@ def dense_verify(ci, cj, T, depth_max=0.15, normal_min=0.9, color_max=0.1, error
     k = ci.intrinsics_low
     m = min_fraction * k.width * k.height
     return (n1 >= m and n2 >= m and e1 <= error_max and e2 <= error_max), e1, e2, n1, n2
+
+
+# --------------------------------------------------------------------------
+# hashed TSDF integrate / de-integrate (tsdf.py:55-201)
+
+TSDF_B = 8  # voxels per block edge (tsdf.py:21)
+
+
+def _block_offsets():
+    i, j, k = np.meshgrid(np.arange(TSDF_B), np.arange(TSDF_B), np.arange(TSDF_B), indexing="ij")
+    return np.stack([i, j, k], axis=-1).reshape(-1, 3).astype(np.float64)
+
+
+class TsdfOracle:
+    """TsdfVolume restated: blocks = {coord: [weight, wdist, wcolor]} (float32
+    accumulators, insertion order = allocation order).  integrate/deintegrate
+    follow tsdf.py:90-160 step for step; errors raise ValueError."""
+
+    EPS = np.float32(1e-6)
+
+    def __init__(self, voxel_size=0.004, truncation=None, depth_weighting=False):
+        self.vs = float(voxel_size)
+        self.trunc = float(truncation if truncation is not None else max(0.02, 5.0 * voxel_size))
+        self.dw = depth_weighting
+        self.blocks = {}
+
+    @property
+    def extent(self):
+        return self.vs * TSDF_B
+
+    def touched(self, depth_img, K, T):
+        """tsdf.py:162-181: sorted unique block coords the truncation band crosses."""
+        valid = depth_img > 0.0
+        if not np.any(valid):
+            return np.zeros((0, 3), dtype=np.int64)
+        ys, xs = np.nonzero(valid)
+        d = depth_img[ys, xs].astype(np.float64)
+        rays = np.stack([(xs.astype(np.float64) - K.cx) / K.fx * 1.0,
+                         (ys.astype(np.float64) - K.cy) / K.fy * 1.0, np.ones_like(d)], axis=-1)
+        wn = apply(T, rays * np.maximum(d - self.trunc, 1e-3)[:, None])
+        wf = apply(T, rays * (d + self.trunc)[:, None])
+        n = max(2, int(np.ceil(4.0 * self.trunc / self.extent)) + 1)
+        keys = set()
+        allk = []
+        for s in np.linspace(0.0, 1.0, n):
+            c = np.floor((wn + s * (wf - wn)) / self.extent).astype(np.int64)
+            allk.append(c)
+        c = np.unique(np.concatenate(allk), axis=0)
+        del keys
+        return c  # np.unique(axis=0) sorts lexicographically == the packed-key order
+
+    def apply_frame(self, color, depth_img, K, T, sign):
+        tb = self.touched(depth_img, K, T)
+        if tb.shape[0] == 0:
+            if sign < 0:
+                raise ValueError("frame has no integrated content")
+            return
+        cen = (tb[:, None, :] * self.extent + (_block_offsets()[None] + 0.5) * self.vs).reshape(-1, 3)
+        cam = apply(inv(T), cen)
+        u, v, front = project(K, cam)
+        xi, yi = np.round(u).astype(int), np.round(v).astype(int)
+        ins = front & (xi >= 0) & (xi < K.width) & (yi >= 0) & (yi < K.height)
+        xi, yi = np.clip(xi, 0, K.width - 1), np.clip(yi, 0, K.height - 1)
+        d = depth_img[yi, xi].astype(np.float64)
+        sdf = d - cam[:, 2]
+        hit = (ins & (d > 0.0) & (np.abs(sdf) <= self.trunc)).reshape(-1, 512)
+        if self.dw:
+            wgt = np.where(cam[:, 2] > 0.0, 1.0 / np.maximum(cam[:, 2], 1e-6), 0.0)
+        else:
+            wgt = np.ones_like(sdf)
+        col = color[yi, xi].astype(np.float64)
+        wd = (wgt * sdf).reshape(-1, 512).astype(np.float32)
+        w = wgt.reshape(-1, 512).astype(np.float32)
+        wc = (wgt[:, None] * col).reshape(-1, 512, 3).astype(np.float32)
+        s = np.float32(sign)
+        for b, key in enumerate(map(tuple, tb.tolist())):
+            h = hit[b]
+            blk = self.blocks.get(key)
+            if not h.any():
+                if sign < 0 and blk is not None and not blk[0].any():
+                    del self.blocks[key]
+                continue
+            if blk is None:
+                if sign < 0:
+                    raise ValueError(f"block {key} missing")
+                blk = [np.zeros(512, np.float32), np.zeros(512, np.float32),
+                       np.zeros((512, 3), np.float32)]
+                self.blocks[key] = blk
+            blk[0][h] += s * w[b][h]
+            blk[1][h] += s * wd[b][h]
+            blk[2][h] += s * wc[b][h]
+            if sign < 0:
+                if (blk[0] < -self.EPS).any():
+                    raise ValueError(f"negative weight in block {key}")
+                snap = (np.abs(blk[0]) <= self.EPS) & (blk[0] != 0.0)
+                blk[0][snap] = 0.0
+                z = blk[0] == 0.0
+                blk[1][z] = 0.0
+                blk[2][z] = 0.0
+                if not blk[0].any():
+                    del self.blocks[key]

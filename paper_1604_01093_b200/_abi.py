@@ -132,6 +132,14 @@ SIGNATURES = {
     "sfb_gn_step_begin": [_P, _I32, _D, _I32, C.POINTER(Weights), _I32, _I32, _D,
                           C.POINTER(Config), C.POINTER(_I32)],
     "sfb_gn_step_end": [_P, _P],
+    "sfb_tsdf_create": [_P, _D, _D, _I32, C.POINTER(_P)],
+    "sfb_tsdf_destroy": [_P],
+    "sfb_tsdf_apply": [_P, _I32, _I32, _I32, _P, _P, _P, _P, _P, _I32, _P, _P, _I32, _P, _I32,
+                       C.POINTER(_I32), _P],
+    "sfb_tsdf_count": [_P, C.POINTER(_I64)],
+    "sfb_tsdf_export": [_P, _I64, _P, _P, _P, _P],
+    "sfb_tsdf_import": [_P, _I64, _P, _P, _P, _P],
+    "sfb_tsdf_get_block": [_P, _P, C.POINTER(_I32), _P, _P, _P],
     "sfb_build_cache": [_P, _I32, _I32, _I32, _I32, _I32, _P, _P, _P, _I32, _P, _P],
     "sfb_gn_step": [_P, _I32, _D, _I32, C.POINTER(Weights), _I32, _I32, _D, C.POINTER(Config),
                     _P],

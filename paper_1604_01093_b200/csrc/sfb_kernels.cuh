@@ -128,6 +128,39 @@ struct CacheArgs {
   int luma_order;
 };
 
+// hashed TSDF (tsdf.py:55-201)
+struct TsdfTouchArgs {
+  const float* depth;  // (H, W)
+  int W, H;
+  double fx, fy, cx, cy;
+  Xf pose;             // camera -> world
+  int ord;             // NumPy order of (m,3) @ pose.rotation.T
+  double trunc, extent;
+  const double* t;     // np.linspace(0, 1, n_samples), from the host
+  int n_samples;
+  long long* keys;     // W*H*n_samples
+};
+struct TsdfVoxelArgs {
+  const long long* keys;  // sorted unique touched block keys
+  const int* slots;       // pool slot per touched block (-1: skip)
+  const unsigned char* hit;  // EVAL result per touched block
+  unsigned char* flags;   // per touched block: EVAL hit / CHECK negative / COMMIT empty
+  int first;              // first touched block of this launch
+  int snap_end;           // de-integration snaps/clears only touched blocks below this
+  double extent, vs, trunc;
+  Xf inv_pose;            // pose.inverse(), NumPy rounding (host)
+  int ord;
+  double fx, fy, cx, cy;
+  int W, H;
+  const float* depth;
+  const uint8_t* color;   // (H, W, 3)
+  int depth_weighting;
+  float sign;
+  float* weight;          // pool: slot * 512
+  float* wdist;
+  float* wcolor;          // slot * 1536
+};
+
 // Library-wide kernel launch counter (sfb_launch_count).
 void sfb_count_launch(int n = 1);
 
@@ -160,6 +193,13 @@ void launch_point_eval(const FrameDev* frames, const PoseDev* poses, int src, in
                        int64_t m, const double* pts, const double* aux, const double* tgts,
                        double* res, double* jac, cudaStream_t s);
 cudaError_t launch_build_cache(const CacheArgs& a, int n_frames, cudaStream_t s);
+cudaError_t launch_tsdf_touch(const TsdfTouchArgs& a, cudaStream_t s);
+cudaError_t launch_tsdf_zero(const int* slots, int n, float* w, float* d, float* c, cudaStream_t s);
+cudaError_t launch_tsdf_copy(const int* slots, int n, int dir, float* w, float* d, float* c,
+                             float* pw, float* pd, float* pc, cudaStream_t s);
+cudaError_t launch_tsdf_voxels(const TsdfVoxelArgs& a, int mode, int n_blocks, cudaStream_t s);
+cudaError_t tsdf_sort_unique(long long* keys, long long* tmp_keys, int n, void* temp,
+                             size_t* temp_bytes, int* d_count, cudaStream_t s);
 int verify_max_pixels();
 cudaError_t launch_dense_verify(const VerifyItem* items, int n_items, int max_src_hw,
                                 const VerifyCfg& cfg, double* err, long long* cnt, cudaStream_t s);

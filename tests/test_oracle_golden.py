@@ -153,3 +153,32 @@ def test_host_build_cache_matches_reference_digests():
         c = CA.build_cache(CA.RgbdFrame(0, col, dep), se3.Intrinsics(*kk), lw, lh)
         for p in PLANES:
             assert digest(getattr(c, p)) == g[name][p], (name, p)
+
+
+def test_oracle_tsdf_matches_reference_digests():
+    """oracle.TsdfOracle == scanfuse.tsdf.TsdfVolume on the golden scenarios
+    (tests/golden/make_tsdf_golden.py), except the slow 4 mm one."""
+    import json
+    import sys as _sys
+    from golden_io import GOLDEN
+    _sys.path.insert(0, str(GOLDEN))
+    from make_tsdf_golden import SCENARIOS, tsdf_inputs, volume_digest
+    from paper_1604_01093_b200 import se3
+    g = json.loads((GOLDEN / "tsdf_digests.json").read_text())
+    frames, K, truth, noisy = tsdf_inputs()
+    k = se3.Intrinsics(*K)
+    for name, (vs, trunc, dw, steps) in SCENARIOS.items():
+        if name == "vs04":
+            continue
+        o = O.TsdfOracle(vs, trunc, dw)
+        for step, (fi, sign, nz) in enumerate(steps):
+            err = None
+            try:
+                o.apply_frame(frames[fi][0], frames[fi][1], k, (noisy if nz else truth)[fi], sign)
+            except ValueError as e:
+                err = str(e)
+            d = volume_digest(list(o.blocks), {c: tuple(b) for c, b in o.blocks.items()})
+            exp = g[name][step]
+            for key in ("blocks", "occupied", "data", "order"):
+                assert d[key] == exp[key], (name, step, key)
+            assert (err is None) == (exp["error"] is None)

@@ -1,5 +1,2 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 2 --warmup 3 --dist-backend gloo --no-cpu-baseline 2>&1 | tail -3 | cut -c1-1500
-echo rc=$?
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29512 bench.py --impl reference --gpus 2 --steps 1 --warmup 1 2>&1 | tail -2 | cut -c1-300
-echo rc=$?
+timeout 600 python -m pytest tests/test_gpu_tsdf.py -x -q -p no:cacheprovider 2>&1 | tail -30
