@@ -237,6 +237,7 @@ struct sfb_ctx : Handle {
   DBuf<int> counts;
   DBuf<PackArgs> pack_args;
   DBuf<VerifyItem> verify_items;
+  DBuf<CopyJob> copy_jobs;
   DBuf<uint8_t> cache_raw, cache_out;
   DBuf<CacheFrame> cache_frames;
   DBuf<double> verify_err;
@@ -783,6 +784,7 @@ int sfb_ctx_destroy(sfb_ctx* c) {
   for (auto& sl : c->slots)
     if (sl.intensity) dev_cache().release(sl.intensity, sl.intensity_bytes);
   c->verify_items.release();
+  c->copy_jobs.release();
   c->cache_raw.release();
   c->cache_out.release();
   c->cache_frames.release();
@@ -848,6 +850,7 @@ int sfb_frames_upload(sfb_ctx* c, int32_t n, const sfb_frame_desc* d, int32_t* s
   std::vector<PackArgs> pargs(n);
   std::vector<void*> cdst, csrc;
   std::vector<size_t> csz;
+  std::vector<CopyJob> jobs;
   cdst.reserve(5 * (size_t)n);
   csrc.reserve(5 * (size_t)n);
   csz.reserve(5 * (size_t)n);
@@ -880,14 +883,21 @@ int sfb_frames_upload(sfb_ctx* c, int32_t n, const sfb_frame_desc* d, int32_t* s
     const size_t szs[5] = {hw, hw, hw * 12, hw * 12, hw * 8};
     const void* use[5];
     for (int q = 0; q < 5; ++q) {
-      // page-locked host planes are read by the pack kernel in place (UVA
-      // zero-copy over the host link); pageable ones are staged by DMA
+      // device-resident planes (sfb_build_cache) are read in place; page-locked
+      // host planes are pulled by one wide-load copy kernel (16 B per thread,
+      // coalesced over the host link) into staging; pageable ones go by DMA
       cudaPointerAttributes at{};
-      if (cudaPointerGetAttributes(&at, srcs[q]) == cudaSuccess &&
-          ((at.type == cudaMemoryTypeHost && at.devicePointer != nullptr) ||
-           (at.type == cudaMemoryTypeDevice && at.device == c->device))) {
-        use[q] = at.devicePointer;  // device-resident planes (sfb_build_cache) are read in place
-        continue;
+      if (cudaPointerGetAttributes(&at, srcs[q]) == cudaSuccess) {
+        if (at.type == cudaMemoryTypeDevice && at.device == c->device) {
+          use[q] = at.devicePointer;
+          continue;
+        }
+        if (at.type == cudaMemoryTypeHost && at.devicePointer != nullptr) {
+          jobs.push_back(CopyJob{static_cast<const uint8_t*>(at.devicePointer),
+                                 static_cast<uint8_t*>(dsts[q]), szs[q]});
+          use[q] = dsts[q];
+          continue;
+        }
       }
       cudaGetLastError();
       cdst.push_back(dsts[q]);
@@ -913,6 +923,12 @@ int sfb_frames_upload(sfb_ctx* c, int32_t n, const sfb_frame_desc* d, int32_t* s
   // pinned fast path above needs no copies at all)
   for (size_t q = 0; q < cdst.size(); ++q)
     CK(c, cudaMemcpyAsync(cdst[q], csrc[q], csz[q], cudaMemcpyHostToDevice, c->stream));
+  if (!jobs.empty()) {
+    CK(c, c->copy_jobs.ensure(jobs.size(), c->stream));
+    CK(c, cudaMemcpyAsync(c->copy_jobs.p, jobs.data(), sizeof(CopyJob) * jobs.size(),
+                          cudaMemcpyHostToDevice, c->stream));
+    CK(c, launch_stage_copy(c->copy_jobs.p, (int)jobs.size(), c->stream));
+  }
   CK(c, cudaMemcpyAsync(c->pack_args.p, pargs.data(), sizeof(PackArgs) * n, cudaMemcpyHostToDevice,
                         c->stream));
   launch_pack_batch(c->pack_args.p, n, max_hw, max_nt, c->stream);

@@ -352,6 +352,37 @@ __global__ void k_tiles_batch(const PackArgs* args) {
   }
 }
 
+// Pinned host planes -> device staging: one job per plane (blockIdx.y), 16-byte
+// loads when source and destination share their alignment, bytes otherwise.
+__global__ void k_stage_copy(const CopyJob* jobs) {
+  const CopyJob j = jobs[blockIdx.y];
+  const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t nth = (size_t)gridDim.x * blockDim.x;
+  const uintptr_t sa = (uintptr_t)j.src & 15, da = (uintptr_t)j.dst & 15;
+  size_t head = 0, nv = 0;
+  if (sa == da) {
+    head = (16 - sa) & 15;
+    if (head > j.n) head = j.n;
+    nv = (j.n - head) / 16;
+  }
+  const uint4* s4 = reinterpret_cast<const uint4*>(j.src + head);
+  uint4* d4 = reinterpret_cast<uint4*>(j.dst + head);
+  for (size_t i = tid; i < nv; i += nth) d4[i] = s4[i];
+  const size_t done = head + 16 * nv;
+  // head and tail bytes (all bytes when the alignments differ)
+  for (size_t i = tid; i < head; i += nth) j.dst[i] = j.src[i];
+  for (size_t i = done + tid; i < j.n; i += nth) j.dst[i] = j.src[i];
+}
+
+cudaError_t launch_stage_copy(const CopyJob* jobs, int n_jobs, cudaStream_t s) {
+  for (int j0 = 0; j0 < n_jobs; j0 += 65535) {  // gridDim.y limit
+    const int nj = n_jobs - j0 < 65535 ? n_jobs - j0 : 65535;
+    sfb_count_launch();
+    k_stage_copy<<<dim3(16, nj), 256, 0, s>>>(jobs + j0);
+  }
+  return cudaGetLastError();
+}
+
 void launch_pack_batch(const PackArgs* args_dev, int n, int max_hw, int max_tiles, cudaStream_t s) {
   if (n <= 0) return;
   int bx = (max_hw + 255) / 256;

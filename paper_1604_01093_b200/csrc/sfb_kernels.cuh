@@ -161,6 +161,14 @@ struct TsdfVoxelArgs {
   float* wcolor;          // slot * 1536
 };
 
+// one host -> device byte copy (pinned source, read through UVA)
+struct CopyJob {
+  const uint8_t* src;
+  uint8_t* dst;
+  size_t n;
+};
+cudaError_t launch_stage_copy(const CopyJob* jobs, int n_jobs, cudaStream_t s);
+
 // Library-wide kernel launch counter (sfb_launch_count).
 void sfb_count_launch(int n = 1);
 

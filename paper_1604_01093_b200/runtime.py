@@ -26,10 +26,29 @@ def _default_device() -> int:
 
 
 def _plane(a, dtype, shape) -> np.ndarray:
-    arr = np.ascontiguousarray(np.asarray(a), dtype=dtype)
+    if isinstance(a, np.ndarray) and a.dtype == dtype and a.flags.c_contiguous:
+        arr = a  # fast path: already the layout the library reads
+    else:
+        arr = np.ascontiguousarray(np.asarray(a), dtype=dtype)
     if arr.shape != shape:
         raise ValueError(f"cache plane has shape {arr.shape}, expected {shape}")
     return arr
+
+
+# numpy twin of sfb_frame_desc (include/sfb.h), so 500 descriptors fill by column
+_DESC_DTYPE = np.dtype([("width", "<i4"), ("height", "<i4"), ("fx", "<f8"), ("fy", "<f8"),
+                        ("cx", "<f8"), ("cy", "<f8"), ("valid_depth", "<u8"),
+                        ("valid_normal", "<u8"), ("points", "<u8"), ("normals", "<u8"),
+                        ("grad", "<u8")], align=True)
+
+
+def _addr(a: np.ndarray) -> int:
+    """Data pointer of a C-contiguous array (ctypes.c_char.from_buffer is ~2x
+    cheaper than ndarray.ctypes.data; read-only buffers fall back)."""
+    try:
+        return C.addressof(C.c_char.from_buffer(a))
+    except (TypeError, ValueError, BufferError):
+        return a.ctypes.data
 
 
 class Runtime:
@@ -62,11 +81,14 @@ class Runtime:
 
     def _upload(self, caches) -> None:
         n = len(caches)
-        descs = (_abi.FrameDesc * n)()
+        descs = np.zeros(n, dtype=_DESC_DTYPE)  # the sfb_frame_desc array, filled by column
         keep = []
+        dims = np.empty((n, 2), dtype=np.int32)
+        kk = np.empty((n, 4), dtype=np.float64)
+        ptrs = np.empty((n, 5), dtype=np.uint64)
         for k, c in enumerate(caches):
-            vd = np.asarray(c.valid_depth)
-            h, w = vd.shape
+            vd = c.valid_depth
+            h, w = np.shape(vd)
             planes = (
                 _plane(vd, np.bool_, (h, w)).view(np.uint8),
                 _plane(c.valid_normal, np.bool_, (h, w)).view(np.uint8),
@@ -78,14 +100,17 @@ class Runtime:
             k_low = c.intrinsics_low
             if int(k_low.width) != w or int(k_low.height) != h:
                 raise ValueError("intrinsics_low size does not match the cache planes")
-            d = descs[k]
-            d.width, d.height = w, h
-            d.fx, d.fy, d.cx, d.cy = (float(k_low.fx), float(k_low.fy), float(k_low.cx),
-                                      float(k_low.cy))
-            d.valid_depth, d.valid_normal, d.points, d.normals, d.grad = (
-                p.ctypes.data for p in planes)
+            dims[k] = (w, h)
+            kk[k] = (k_low.fx, k_low.fy, k_low.cx, k_low.cy)
+            ptrs[k] = [_addr(p) for p in planes]
+        descs["width"], descs["height"] = dims[:, 0], dims[:, 1]
+        for q, name in enumerate(("fx", "fy", "cx", "cy")):
+            descs[name] = kk[:, q]
+        for q, name in enumerate(("valid_depth", "valid_normal", "points", "normals", "grad")):
+            descs[name] = ptrs[:, q]
         slots = np.zeros(n, dtype=np.int32)
-        _abi.check(self.lib.sfb_frames_upload(self.handle, n, descs, _abi.ptr(slots)), self.handle)
+        _abi.check(self.lib.sfb_frames_upload(self.handle, n, descs.ctypes.data_as(
+            C.POINTER(_abi.FrameDesc)), _abi.ptr(slots)), self.handle)
         for c, s in zip(caches, slots):
             self._frames[id(c)] = (int(s), c)
         del keep

@@ -24,11 +24,13 @@ from __future__ import annotations
 from dataclasses import dataclass, field
 
 import operator
+import threading
 
 import numpy as np
 
 from . import _abi
 from .device_problem import DeviceProblem
+from .runtime import runtime
 from .se3 import RigidTransform
 
 
@@ -647,8 +649,29 @@ class AlignmentProblem:
     def _problem(self) -> DeviceProblem:
         if self._dp is None:
             index = {f: k for k, f in enumerate(self.frame_ids)}
-            frames, off, pi, pj = _set_layout(self.corr_sets, index)
             cl = [self.caches[f] for f in self.frame_ids] if self.caches is not None else None
+            if cl is not None and len(self.corr_sets) > 256:
+                # stack the correspondence sets on a helper thread while the
+                # frame upload runs in the library (ctypes drops the GIL there)
+                box = {}
+
+                def _layout():
+                    try:
+                        box["v"] = _set_layout(self.corr_sets, index)
+                    except BaseException as e:  # re-raised on the caller's thread
+                        box["e"] = e
+
+                th = threading.Thread(target=_layout, daemon=True)
+                th.start()
+                try:
+                    runtime(self._device).slots_for(cl)
+                finally:
+                    th.join()
+                if "e" in box:
+                    raise box["e"]
+                frames, off, pi, pj = box["v"]
+            else:
+                frames, off, pi, pj = _set_layout(self.corr_sets, index)
             self._dp = DeviceProblem(len(self.frame_ids), cl, frames, pi, pj, off,
                                      device=self._device)
             if self._xch is not None:
