@@ -13,9 +13,10 @@
 // accumulators, halves split at n/2 rounded down to a multiple of 8) of the
 // good distances in row-major order, so it is bit-exact too.
 //
-// Layout: the good distances of the CTA's direction are compacted in order
-// into shared memory (<= 24,576 source pixels: 192 KB), then summed by the
-// pairwise tree (leaves in parallel, the combine on one thread).
+// Layout: each warp scans a contiguous pixel segment and appends its good
+// distances in order to its own shared-memory segment (no CTA barrier in the
+// scan); the pairwise tree (leaves in parallel, the combine on one thread)
+// then reads the segments in global order.  <= 25,600 source pixels (200 KB).
 #include "sfb_kernels.cuh"
 
 #define VERIFY_THREADS 512
@@ -41,24 +42,38 @@ __device__ __forceinline__ double bilinear1_exact(const float* img, int w, int h
   return __dadd_rn(__dadd_rn(__dadd_rn(a, b), c), d);
 }
 
+// Sequential reader of the compacted good distances stored as per-warp
+// segments: global index i lives at gd[w*seg + i - off[w]].
+struct SegReader {
+  const double* gd;
+  const int* off;
+  int seg;
+  int i;
+  int w = 0;
+  __device__ __forceinline__ double next() {
+    while (i >= off[w + 1]) ++w;
+    return gd[w * seg + (i++ - off[w])];
+  }
+};
+
 // NumPy pairwise_sum leaf: n < 8 sequential from 0.0; n <= 128 eight strided
 // accumulators, ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the tail.
-__device__ double pairwise_leaf(const double* a, int n) {
+__device__ double pairwise_leaf(SegReader a, int n) {
   if (n < 8) {
     double s = 0.0;
-    for (int i = 0; i < n; ++i) s = __dadd_rn(s, a[i]);
+    for (int i = 0; i < n; ++i) s = __dadd_rn(s, a.next());
     return s;
   }
   double r[8];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) r[j] = a[j];
+  for (int j = 0; j < 8; ++j) r[j] = a.next();
   int i = 8;
   for (; i < n - (n % 8); i += 8)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a.next());
   double s = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
                        __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-  for (; i < n; ++i) s = __dadd_rn(s, a[i]);
+  for (; i < n; ++i) s = __dadd_rn(s, a.next());
   return s;
 }
 
@@ -83,12 +98,16 @@ __global__ void __launch_bounds__(VERIFY_THREADS) k_dense_verify(const VerifyIte
 #pragma unroll
   for (int k = 0; k < 3; ++k) X.t[k] = it.t[k];
   const unsigned both = SFB_FLAG_VD | SFB_FLAG_VN;
-  int base = 0;
-  for (int p0 = 0; p0 < hw; p0 += VERIFY_THREADS) {
-    const int p = p0 + tid;
+  // warp w owns the contiguous pixel segment [w*seg, (w+1)*seg) and appends
+  // its good distances, in order, at gd[w*seg ...]: no CTA barrier in the loop
+  const int seg = ((hw + VERIFY_WARPS - 1) / VERIFY_WARPS + 31) & ~31;
+  const int p_begin = wid * seg, p_end = min(hw, p_begin + seg);
+  int wcount = 0;  // warp-uniform
+  for (int p0 = p_begin; p0 < p_end; p0 += 32) {
+    const int p = p0 + lane;
     bool good = false;
     double dist = 0.0;
-    if (p < hw) {
+    if (p < p_end) {
       const float4 P = __ldg(&S.P[p]);
       if ((__float_as_uint(P.w) & both) == both) {
         double q[3], u, v;
@@ -122,21 +141,23 @@ __global__ void __launch_bounds__(VERIFY_THREADS) k_dense_verify(const VerifyIte
         }
       }
     }
-    // ordered compaction of the good distances
     const unsigned bal = __ballot_sync(0xffffffffu, good);
-    if (lane == 0) warp_cnt[wid] = __popc(bal);
-    __syncthreads();
-    int before = 0, total = 0;
-#pragma unroll
-    for (int w = 0; w < VERIFY_WARPS; ++w) {
-      const int c = warp_cnt[w];
-      before += w < wid ? c : 0;
-      total += c;
-    }
-    if (good) gd[base + before + __popc(bal & ((1u << lane) - 1u))] = dist;
-    base += total;
-    __syncthreads();
+    if (good) gd[p_begin + wcount + __popc(bal & ((1u << lane) - 1u))] = dist;
+    wcount += __popc(bal);
   }
+  if (lane == 0) warp_cnt[wid] = wcount;
+  __syncthreads();
+  __shared__ int seg_off[VERIFY_WARPS + 1];
+  if (tid == 0) {
+    int acc = 0;
+    for (int w = 0; w < VERIFY_WARPS; ++w) {
+      seg_off[w] = acc;
+      acc += warp_cnt[w];
+    }
+    seg_off[VERIFY_WARPS] = acc;
+  }
+  __syncthreads();
+  const int base = seg_off[VERIFY_WARPS];
   const int n = base;
   // numpy pairwise_sum tree over gd[0..n): leaves and post-order ops
   if (tid == 0) {
@@ -169,7 +190,8 @@ __global__ void __launch_bounds__(VERIFY_THREADS) k_dense_verify(const VerifyIte
     n_ops = no;
   }
   __syncthreads();
-  for (int k = tid; k < n_leaves; k += VERIFY_THREADS) leaf_v[k] = pairwise_leaf(gd + leaf_lo[k], leaf_n[k]);
+  for (int k = tid; k < n_leaves; k += VERIFY_THREADS)
+    leaf_v[k] = pairwise_leaf(SegReader{gd, seg_off, seg, leaf_lo[k]}, leaf_n[k]);
   __syncthreads();
   if (tid == 0) {
     double vs[40];
@@ -195,7 +217,9 @@ cudaError_t launch_dense_verify(const VerifyItem* items, int n_items, int max_sr
                                 const VerifyCfg& cfg, double* err, long long* cnt,
                                 cudaStream_t s) {
   if (n_items <= 0) return cudaSuccess;
-  const size_t smem = (size_t)max_src_hw * sizeof(double);
+  // per-warp segments of ceil(hw / warps) rounded up to 32 pixels
+  const int seg = ((max_src_hw + VERIFY_WARPS - 1) / VERIFY_WARPS + 31) & ~31;
+  const size_t smem = (size_t)VERIFY_WARPS * seg * sizeof(double);
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k_dense_verify, cudaFuncAttributeMaxDynamicSharedMemorySize,
