@@ -66,22 +66,36 @@ __device__ __forceinline__ double row_product(const PcgArgs& a, const RowCtx& rc
   double acc = 0.0;
   for (int c0 = e0; c0 < e1; c0 += PCG_GATHER_CAP) {
     const int c1 = min(e1, c0 + PCG_GATHER_CAP);
-    // gather the chunk's neighbour vectors: every load of the chunk in flight
-    for (int k = c0 + lane; k < c1; k += 32) {
-      const int w = rc.cols[k];
-      const double2* pw = reinterpret_cast<const double2*>(pold + 6 * w);
-      double2 x01 = __ldcg(pw), x23 = __ldcg(pw + 1), x45 = __ldcg(pw + 2);
-      if (FOLD) {
-        const double2* zw = reinterpret_cast<const double2*>(z + 6 * w);
-        const double2 z01 = __ldcg(zw), z23 = __ldcg(zw + 1), z45 = __ldcg(zw + 2);
-        x01.x = fma(beta, x01.x, z01.x); x01.y = fma(beta, x01.y, z01.y);
-        x23.x = fma(beta, x23.x, z23.x); x23.y = fma(beta, x23.y, z23.y);
-        x45.x = fma(beta, x45.x, z45.x); x45.y = fma(beta, x45.y, z45.y);
+    // gather the chunk's neighbour vectors: the (up to three) slots of each
+    // lane are loaded before any is stored, so the chunk costs one L2 round trip
+    static_assert(PCG_GATHER_CAP <= 96, "gather unroll covers 3 slots per lane");
+    double2 xa[3], xb[3], xc[3];
+    const int ka = c0 + lane, kb = ka + 32, kc = ka + 64;
+    const bool va = ka < c1, vb = kb < c1, vc = kc < c1;
+    const int wa = va ? rc.cols[ka] : 0, wb = vb ? rc.cols[kb] : 0, wc = vc ? rc.cols[kc] : 0;
+#pragma unroll
+    for (int h = 0; h < 3; ++h) {
+      xa[h] = va ? __ldcg(reinterpret_cast<const double2*>(pold + 6 * wa) + h) : make_double2(0, 0);
+      xb[h] = vb ? __ldcg(reinterpret_cast<const double2*>(pold + 6 * wb) + h) : make_double2(0, 0);
+      xc[h] = vc ? __ldcg(reinterpret_cast<const double2*>(pold + 6 * wc) + h) : make_double2(0, 0);
+    }
+    if (FOLD) {
+#pragma unroll
+      for (int h = 0; h < 3; ++h) {
+        const double2 za = va ? __ldcg(reinterpret_cast<const double2*>(z + 6 * wa) + h) : make_double2(0, 0);
+        const double2 zb = vb ? __ldcg(reinterpret_cast<const double2*>(z + 6 * wb) + h) : make_double2(0, 0);
+        const double2 zc = vc ? __ldcg(reinterpret_cast<const double2*>(z + 6 * wc) + h) : make_double2(0, 0);
+        xa[h].x = fma(beta, xa[h].x, za.x); xa[h].y = fma(beta, xa[h].y, za.y);
+        xb[h].x = fma(beta, xb[h].x, zb.x); xb[h].y = fma(beta, xb[h].y, zb.y);
+        xc[h].x = fma(beta, xc[h].x, zc.x); xc[h].y = fma(beta, xc[h].y, zc.y);
       }
-      double2* gb = reinterpret_cast<double2*>(rc.gbuf + 6 * (k - c0));
-      gb[0] = x01;
-      gb[1] = x23;
-      gb[2] = x45;
+    }
+    double2* gb = reinterpret_cast<double2*>(rc.gbuf);
+#pragma unroll
+    for (int h = 0; h < 3; ++h) {
+      if (va) gb[3 * (ka - c0) + h] = xa[h];
+      if (vb) gb[3 * (kb - c0) + h] = xb[h];
+      if (vc) gb[3 * (kc - c0) + h] = xc[h];
     }
     __syncwarp();
     if (grp < 5) {
@@ -413,7 +427,9 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg(PcgArgs a, Mv mv, int ro
 // neighbours read goes to memory (p every iteration, z every iteration for
 // the folded p = z + beta p, x on restart iterations) and x once at the end;
 // the update phase issues no loads at all.
-#define PCG_RMAX 8
+#ifndef PCG_RMAX
+#define PCG_RMAX 2
+#endif
 
 __device__ __forceinline__ double rsel(const double (&a)[PCG_RMAX], int j) {
   double v = a[0];

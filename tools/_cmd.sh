@@ -1,3 +1,4 @@
 cd $GRAFT_REPO_ROOT
-timeout 600 python -m pytest tests/test_gpu_verify.py tests/test_gpu_cache.py -x -q -p no:cacheprovider 2>&1 | tail -3
-timeout 600 python tools/bench_verify.py --config cfg4 2>&1 | tail -1
+timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_reference_suite.py -x -q -p no:cacheprovider 2>&1 | tail -2
+for v in trace; do echo == $v; SFB_LIB=$GRAFT_REPO_ROOT/variants/$v.so timeout 300 python tools/pcg_trace.py; done
+VARIANTS="cur" bash tools/gpu_variants.sh
