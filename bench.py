@@ -460,8 +460,8 @@ def main():
     if not args.no_cpu_baseline and world == 1:
         edges = [(a, b) for (a, b) in problem.dense_edges]
         # ~10-20 s of single-core oracle work on the GPU box's host
-        cms, sample, spent = cpu_extrapolate(args.config, edges, records, 1, pair_sample=6000,
-                                             edge_sample=600)
+        cms, sample, spent = cpu_extrapolate(args.config, edges, records, 1, pair_sample=8000,
+                                             edge_sample=800)
         cpu = {"value": cms, "unit": "ms", "cores": 1, "kind": "port", "sample": sample,
                "sample_seconds": round(spent, 1)}
     line = {

@@ -26,3 +26,7 @@ timeout 900 $NCU --set full --clock-control none --import-source on -k regex:k_d
 echo profverify rc=$?
 timeout 900 $NCU --set full --clock-control none --import-source on -k regex:k_cache_reduce -c 1 -o gpurun_out/prof_cache python tools/bench_cache.py --frames 64 --reps 1 > gpurun_out/prof_cache.log 2>&1
 echo profcache rc=$?
+timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv --log-file gpurun_out/launches_bench.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/launch_bench_run.log 2>&1
+echo launchbench rc=$?
+timeout 600 python tools/bench_tsdf.py > gpurun_out/bench_tsdf.log 2>&1
+echo tsdf rc=$?
