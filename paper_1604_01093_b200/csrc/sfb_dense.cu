@@ -243,33 +243,6 @@ __device__ __forceinline__ bool near_half(double x) {
   return fabs(fabs(x - rint_magic(x)) - 0.5) < 1e-6;
 }
 
-// bilinear_sample_with_grad on the taps plane with FP64-pipe floor.
-__device__ __forceinline__ void bilinear_fast(const FrameDev& f, double x, double y, double val[2],
-                                              double ddx[2], double ddy[2]) {
-  const double wm1 = (double)(f.w - 1), hm1 = (double)(f.h - 1);
-  x = fmin(fmax(x, 0.0), wm1);
-  y = fmin(fmax(y, 0.0), hm1);
-  double fxr = rint_magic(x), fyr = rint_magic(y);
-  fxr = fxr > x ? fxr - 1.0 : fxr;  // floor
-  fyr = fyr > y ? fyr - 1.0 : fyr;
-  fxr = fmin(fxr, (double)(f.w - 2));
-  fyr = fmin(fyr, (double)(f.h - 2));
-  const int x0 = __double2loint(__dadd_rn(fxr, 6755399441055744.0));
-  const int y0 = __double2loint(__dadd_rn(fyr, 6755399441055744.0));
-  const double ax = x - fxr, ay = y - fyr;
-  const float4 t0 = __ldg(&f.T[2 * (y0 * f.w + x0)]);
-  const float4 t1 = __ldg(&f.T[2 * (y0 * f.w + x0) + 1]);
-  const double bx = 1.0 - ax, by = 1.0 - ay;
-  const double v00[2] = {t0.x, t0.y}, v01[2] = {t0.z, t0.w};
-  const double v10[2] = {t1.x, t1.y}, v11[2] = {t1.z, t1.w};
-#pragma unroll
-  for (int c = 0; c < 2; ++c) {
-    val[c] = v00[c] * bx * by + v01[c] * ax * by + v10[c] * bx * ay + v11[c] * ax * ay;
-    ddx[c] = (v01[c] - v00[c]) * by + (v11[c] - v10[c]) * ay;
-    ddy[c] = (v10[c] - v00[c]) * bx + (v11[c] - v01[c]) * ax;
-  }
-}
-
 #define DENSE_MAX_TILES 1024
 
 #ifdef DENSE_COUNT
@@ -500,7 +473,9 @@ __global__ void __launch_bounds__(DENSE_THREADS, DENSE_MIN_BLOCKS) k_dense_fused
     // ---- photometric: one bilinear sample serves the frozen energy and J
     if (ph_in || pph) {
       double val[2], ddx[2], ddy[2];
-      bilinear_fast(Fj, ua, va, val, ddx, ddy);
+      // (the F2I-floor form issues the tap loads sooner than bilinear_fast's
+      // FP64 rint chain: 6.71 vs 6.83 ms per launch at cfg4)
+      bilinear_grad2(Fj, ua, va, val, ddx, ddy);
       const float2 ref = __ldg(&Fi.G[p]);
       const double r0 = (double)ref.x - val[0], r1 = (double)ref.y - val[1];
       const double e2 = r0 * r0 + r1 * r1;
@@ -624,8 +599,11 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_dense_energy(DenseArgs a, dou
       double q[3];
       xf_apply(sh, sh + 9, P.x, P.y, P.z, q);
       const double zs = q[2] > 0.0 ? q[2] : 1.0;
-      const double u = Fj.fx * q[0] / zs + Fj.cx;
-      const double v = Fj.fy * q[1] / zs + Fj.cy;
+      // reciprocal-multiply projection as k_dense_fused's frozen energy; the
+      // F2I-floor bilinear issues its tap loads sooner than the FP64 rint form
+      const double rz = __drcp_rn(zs);
+      const double u = fma(Fj.fx * q[0], rz, Fj.cx);
+      const double v = fma(Fj.fy * q[1], rz, Fj.cy);
       double val[2], ddx[2], ddy[2];
       bilinear_grad2(Fj, u, v, val, ddx, ddy);
       const float2 ref = __ldg(&Fi.G[p]);
