@@ -430,11 +430,24 @@ int rebuild_structure(sfb_problem* p, int bidir) {
   dc.reserve(2 * (size_t)(p->n_sets + p->n_dir) + 8);
   std::vector<Contrib> bc;  // var = pair id
   bc.reserve((size_t)(p->n_sets + p->n_dir) + 8);
-  std::unordered_map<int64_t, int> pid;
-  pid.reserve(2 * (size_t)(p->n_sets + p->n_dir) + 8);
+  // pair id lookup: a flat nb x nb table while it stays small (<= 64 MB),
+  // a hash map beyond that
   std::vector<int2> pv;
+  const bool flat = (int64_t)nb * nb <= ((int64_t)16 << 20);
+  std::vector<int> pid_flat;
+  std::unordered_map<int64_t, int> pid;
+  if (flat) pid_flat.assign((size_t)nb * nb, -1);
+  else pid.reserve(2 * (size_t)(p->n_sets + p->n_dir) + 8);
   auto pair_of = [&](int a, int b) {
     const int64_t key = (int64_t)a * nb + b;
+    if (flat) {
+      int& slot = pid_flat[key];
+      if (slot < 0) {
+        slot = (int)pv.size();
+        pv.push_back(make_int2(a, b));
+      }
+      return slot;
+    }
     auto ins = pid.emplace(key, (int)pv.size());
     if (ins.second) pv.push_back(make_int2(a, b));
     return ins.first->second;
