@@ -732,26 +732,54 @@ __global__ void k_assemble(AssembleArgs a) {
     const int v = warp;
     double d0 = 0.0, d1 = 0.0, gv = 0.0;
     const int e0 = lane, e1 = lane + 32;  // matrix entries handled by this lane
-    for (int k = a.d_ptr[v]; k < a.d_ptr[v + 1]; ++k) {
-      const int ent = a.d_ent[k];
+    // one contribution's (diagonal entry pair, gradient entry); loads only,
+    // so a batch of them is in flight before the in-order accumulation below
+    auto fetch = [&](int ent, double& x0, double& x1, double& xg) {
       const int kind = ent & 7, id = ent >> 3;
+      x0 = 0.0;
+      x1 = 0.0;
+      xg = 0.0;
       if (kind <= 2) {
         const double* so = a.set_out + (int64_t)id * SFB_SET_STRIDE;
         if (kind == 2) {  // self-set: H_ij + H_ij^T (both cross blocks land on the diagonal)
           const double* h = so + 72;
-          d0 += h[e0] + h[(e0 % 6) * 6 + e0 / 6];
-          if (e1 < 36) d1 += h[e1] + h[(e1 % 6) * 6 + e1 / 6];
+          x0 = h[e0] + h[(e0 % 6) * 6 + e0 / 6];
+          if (e1 < 36) x1 = h[e1] + h[(e1 % 6) * 6 + e1 / 6];
         } else {
           const double* h = so + (kind == 0 ? 0 : 36);
-          d0 += h[e0];
-          if (e1 < 36) d1 += h[e1];
-          if (lane < 6) gv += so[(kind == 0 ? SFB_SET_GI : SFB_SET_GJ) + lane];
+          x0 = h[e0];
+          if (e1 < 36) x1 = h[e1];
+          if (lane < 6) xg = so[(kind == 0 ? SFB_SET_GI : SFB_SET_GJ) + lane];
         }
       } else if (a.dense_on) {
         const double* eo = a.edge_out + (int64_t)id * SFB_ITEM_STRIDE;
-        d0 += sym_full(eo, e0 / 6, e0 % 6);
-        if (e1 < 36) d1 += sym_full(eo, e1 / 6, e1 % 6);
-        if (lane < 6) gv += (kind == 4 ? 1.0 : -1.0) * eo[21 + lane];
+        x0 = sym_full(eo, e0 / 6, e0 % 6);
+        if (e1 < 36) x1 = sym_full(eo, e1 / 6, e1 % 6);
+        if (lane < 6) xg = (kind == 4 ? 1.0 : -1.0) * eo[21 + lane];
+      }
+    };
+    const int k0 = a.d_ptr[v], k1 = a.d_ptr[v + 1];
+    for (int kb = k0; kb < k1; kb += 32) {
+      const int ent_l = kb + lane < k1 ? a.d_ent[kb + lane] : 0;  // 32 list entries at once
+      const int nk = min(32, k1 - kb);
+      int j = 0;
+      for (; j + 4 <= nk; j += 4) {
+        double x0[4], x1[4], xg[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) fetch(__shfl_sync(0xffffffffu, ent_l, j + u), x0[u], x1[u], xg[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {  // list order: the sums are assembled deterministically
+          d0 += x0[u];
+          d1 += x1[u];
+          gv += xg[u];
+        }
+      }
+      for (; j < nk; ++j) {
+        double x0, x1, xg;
+        fetch(__shfl_sync(0xffffffffu, ent_l, j), x0, x1, xg);
+        d0 += x0;
+        d1 += x1;
+        gv += xg;
       }
     }
     double* D = a.D + (int64_t)v * 36;
