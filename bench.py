@@ -156,6 +156,20 @@ def ncu_traffic(config: str):
                                     "dram_gbs": d.get("dram_gbs")}
 
 
+def fp64_model(config: str):
+    """FP64 FLOPs per fused dense launch (SURVEY 8(d) model x the associated
+    pixel-edges counted by tools/dense_count.py) and the measured DFMA peak,
+    from profiles/ (None when absent)."""
+    c = ROOT / "profiles" / f"r01_dense_counts_{config}.json"
+    pk = ROOT / "profiles" / "r01_fp64_peak.json"
+    if not c.exists() or not pk.exists():
+        return None, None
+    d = json.loads(c.read_text())
+    m = d["flop_model"]
+    flops = m["photo_px_edge"] * d["photo_associated"] + m["geo_px_edge"] * d["geo_associated"]
+    return float(flops), float(json.loads(pk.read_text())["dfma_tflops"])
+
+
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -456,6 +470,7 @@ def main():
             dist.destroy_process_group()
         return
     traffic, traffic_src = ncu_traffic(args.config)
+    flops, fp64_peak = fp64_model(args.config)
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         edges = [(a, b) for (a, b) in problem.dense_edges]
@@ -481,6 +496,11 @@ def main():
                      "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": cb["linearize"],
                      "ms_per_launch": lin_per, "launches": lin_n},
+        "roofline_fp64": ({"kernel": "k_dense_fused", "model_flops_per_launch": flops,
+                           "achieved": flops / (lin_per * 1e-3) / 1e12, "peak": fp64_peak,
+                           "unit": "TFLOP/s", "frac": flops / (lin_per * 1e-3) / 1e12 / fp64_peak,
+                           "peak_kind": "measured DFMA (profiles/r01_fp64_peak.json)"}
+                          if flops and lin_n else None),
         "pcg": {"us_per_iteration": pcg_iter_us,
                 "canonical_bytes_per_iteration": cb["pcg_iteration"],
                 "gbs": (cb["pcg_iteration"] / (pcg_iter_us * 1e-6) / 1e9) if pcg_iter_us else None},

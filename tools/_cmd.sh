@@ -1,3 +1,4 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_reference_suite.py tests/test_gpu_fullsize.py -x -q -p no:cacheprovider 2>&1 | tail -2
-VARIANTS="cur" bash tools/gpu_variants.sh
+python tools/build_variant.py count -- -DDENSE_COUNT > /dev/null 2>&1 || true
+SFB_LIB=$GRAFT_REPO_ROOT/variants/count.so timeout 500 python tools/dense_count.py cfg4
+./tools/micro/dmma_rate
