@@ -236,12 +236,7 @@ __device__ __forceinline__ double rint_magic(double x) {
   return __dsub_rn(__dadd_rn(x, M), M);
 }
 
-__device__ __forceinline__ bool near_val(double x, double b) { return fabs(x - b) < 1e-6; }
 
-// |x| < 2^51: is x within 1e-6 of a half-integer (np.round tie region)?
-__device__ __forceinline__ bool near_half(double x) {
-  return fabs(fabs(x - rint_magic(x)) - 0.5) < 1e-6;
-}
 
 #define DENSE_MAX_TILES 1024
 

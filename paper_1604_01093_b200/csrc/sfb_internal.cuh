@@ -173,21 +173,6 @@ __device__ __forceinline__ void bilinear_grad2(const FrameDev& f, double x, doub
   }
 }
 
-// Exact float -> double on the integer pipes (no XU F2F): place the float's
-// exponent and mantissa bits in a double with the unbiased exponent and
-// rescale by 2^896.  Exact for every finite float, including subnormals and
-// signed zero; frame planes are checked finite at upload.
-// (Measured on B200: the XU F2F is faster overall than this 4-op integer
-// form, so SFB_F2D_ALU is off by default.)
-__device__ __forceinline__ double f2d(float f) {
-#ifdef SFB_F2D_ALU
-  const unsigned u = __float_as_uint(f);
-  const unsigned hi = (u & 0x80000000u) | ((u & 0x7fffffffu) >> 3);
-  return __hiloint2double((int)hi, (int)(u << 29)) * 0x1p896;
-#else
-  return (double)f;
-#endif
-}
 
 // Warp-level deterministic butterfly sum (every lane ends with the same bits).
 __device__ __forceinline__ double warp_sum(double v) {
