@@ -307,6 +307,7 @@ struct sfb_problem : Handle {
   DBuf<int2> f_all, f_cand, f_sel;
   DBuf<uint8_t> f_fl, f_pass, f_temp;
   DBuf<int> f_cnt;
+  DBuf<int> f_need;  // [0] queue length, then the undecided candidates (pair filter stage 2)
 };
 
 namespace {
@@ -1699,6 +1700,7 @@ int sfb_problem_destroy(sfb_problem* p) {
   p->f_pass.release();
   p->f_temp.release();
   p->f_cnt.release();
+  p->f_need.release();
   if (p->hscal) pinned_scalars_release(p->hscal);
   if (p->stream) cudaStreamDestroy(p->stream);
   delete p;
@@ -1794,9 +1796,10 @@ int sfb_build_dense_edges_begin(sfb_problem* p, double cos_min) {
     p->n_cand = nc;
     if (nc > 0) {
       CK(p, pass.ensure(nc));
+      CK(p, p->f_need.ensure((size_t)nc + 1, s));
       ProfScope ps(p->prof, 3, s);
       launch_overlap(p->frames.p, p->poses.p, cand.p, nc, p->ctx->rd, 0, pass.p, nullptr, s,
-                     p->shard_rank, p->shard_world);
+                     p->shard_rank, p->shard_world, p->f_need.p + 1, p->f_need.p, p->ctx->n_sm);
       CKL(p);
     }
   }

@@ -4,6 +4,9 @@
 //  k_angle_gate  one thread per pair a<b: clip(z_a . z_b) >= cos_min, the dot
 //                in NumPy's np.dot FMA order.  cos_min is the exact preimage
 //                of `degrees(arccos(c)) < view_angle_max_deg` (host bisection).
+//  k_overlap_prefilter + k_overlap_culled   the solver's path: a thread per
+//                candidate classifies bounding spheres of 16x16 tiles, and only
+//                the undecided pairs get the exact per-point test (queue).
 //  k_overlap     one CTA per candidate pair, both directions; each direction
 //                maps the source's valid points through pose_b^-1 o pose_a
 //                with NumPy's rounding and stops at the first point inside
@@ -11,6 +14,8 @@
 //                __syncthreads_or per 256-pixel chunk.  full_count mode counts
 //                every point instead (frustum_overlap's fraction).
 #include "sfb_kernels.cuh"
+
+#include <algorithm>
 
 __global__ void k_angle_gate(const PoseDev* poses, int n, Rounding rd, double cos_min,
                              uint8_t* flags) {
@@ -122,69 +127,129 @@ __device__ __forceinline__ int classify_tile(const Xf& rel, const double4 s, con
   return all_in ? 1 : 2;
 }
 
+// Stage 1, one thread per candidate: both directions' tiles classified with a
+// plainly rounded relative pose (error ~1e-15 m << the 1e-7 m margin), which
+// settles most pairs for good - every tile of a direction outside the target
+// frustum (no overlap), or a fully-inside tile holding a valid point in both
+// directions (overlap both ways).  The rest are queued for stage 2.
+__global__ void __launch_bounds__(256) k_overlap_prefilter(const FrameDev* frames,
+                                                           const PoseDev* poses, const int2* cand,
+                                                           int n_cand, uint8_t* pass, int* need,
+                                                           int* n_need, int rank, int world) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n_cand) return;
+  if (world > 1 && c % world != rank) {  // another rank's candidate
+    pass[c] = 0;
+    return;
+  }
+  const int2 ab = cand[c];
+  int verdict = 1;  // 1 pass, 0 fail, 2 undecided
+  for (int dir = 0; dir < 2 && verdict != 0; ++dir) {
+    const int sa = dir == 0 ? ab.x : ab.y, sb = dir == 0 ? ab.y : ab.x;
+    const PoseDev& Pa = poses[sa];
+    const PoseDev& Pb = poses[sb];
+    // rel = pose_b^-1 o pose_a, plain rounding
+    Xf rel;
+    double iR[9], it[3];
+    xf_inverse_plain(Pb.R, Pb.t, iR, it);
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+        rel.R[r * 3 + q] = iR[r * 3] * Pa.R[q] + iR[r * 3 + 1] * Pa.R[3 + q] + iR[r * 3 + 2] * Pa.R[6 + q];
+      rel.t[r] = iR[r * 3] * Pa.t[0] + iR[r * 3 + 1] * Pa.t[1] + iR[r * 3 + 2] * Pa.t[2] + it[r];
+    }
+    const FrameDev& Fa = frames[sa];
+    const FrameDev& Fb = frames[sb];
+    const int nt = Fa.tiles_x * Fa.tiles_y;
+    bool in_dir = false, partial = false;
+    for (int t = 0; t < nt && !in_dir; ++t) {
+      const int cls = classify_tile(rel, Fa.tiles[t], Fb);
+      if (cls == 1 && Fa.tile_count[t] > 0) in_dir = true;
+      else if (cls == 2) partial = true;
+    }
+    if (!in_dir) verdict = partial ? 2 : 0;
+  }
+  if (verdict == 2) {
+    need[atomicAdd(n_need, 1)] = c;
+  } else {
+    pass[c] = verdict ? 1 : 0;
+  }
+}
+
+// Stage 2 (persistent CTAs over the queue): the exact per-point test in the
+// partially visible tiles, as frustum_overlap with NumPy's rounding.
 __global__ void __launch_bounds__(256) k_overlap_culled(const FrameDev* frames, const PoseDev* poses,
                                                         const int2* cand, Rounding rd,
-                                                        uint8_t* pass, int rank, int world) {
+                                                        uint8_t* pass, const int* need,
+                                                        const int* n_need) {
   __shared__ Xf rel[2];
   __shared__ int partial[1024];
   __shared__ int n_partial;
-  if (world > 1 && (int)(blockIdx.x % world) != rank) {  // another rank's candidate
-    if (threadIdx.x == 0) pass[blockIdx.x] = 0;
-    return;
-  }
-  const int2 ab = cand[blockIdx.x];
-  if (threadIdx.x < 2) {
-    const int s = threadIdx.x == 0 ? ab.x : ab.y;
-    const int t = threadIdx.x == 0 ? ab.y : ab.x;
-    rel[threadIdx.x] = xf_relative_exact(poses[s], poses[t], rd);
-  }
-  __syncthreads();
-  bool ok = true;
-  for (int dir = 0; dir < 2 && ok; ++dir) {
-    const FrameDev Fa = frames[dir == 0 ? ab.x : ab.y];
-    const FrameDev Fb = frames[dir == 0 ? ab.y : ab.x];
-    const int ord = Fa.n_valid_depth == 1 ? rd.apply_1 : rd.apply_n;
-    const int nt = Fa.tiles_x * Fa.tiles_y;
-    bool found = false;
-    for (int t0 = 0; t0 < nt && !found; t0 += 1024) {
-      if (threadIdx.x == 0) n_partial = 0;
-      __syncthreads();
-      bool any_in = false;
-      for (int t = t0 + threadIdx.x; t < min(nt, t0 + 1024); t += blockDim.x) {
-        const int cls = classify_tile(rel[dir], Fa.tiles[t], Fb);
-        if (cls == 1 && Fa.tile_count[t] > 0) any_in = true;
-        if (cls == 2) partial[atomicAdd(&n_partial, 1)] = t;
-      }
-      if (__syncthreads_or(any_in)) {
-        found = true;
-        break;
-      }
-      const int np = n_partial;
-      for (int k = 0; k < np && !found; ++k) {
-        const int t = partial[k];
-        const int x = (t % Fa.tiles_x) * SFB_TILE + (threadIdx.x % SFB_TILE);
-        const int y = (t / Fa.tiles_x) * SFB_TILE + (threadIdx.x / SFB_TILE);
-        bool in = false;
-        if (x < Fa.w && y < Fa.h) {
-          const float4 P = __ldg(&Fa.P[y * Fa.w + x]);
-          in = (__float_as_uint(P.w) & SFB_FLAG_VD) && point_inside(rel[dir], Fb, P, ord);
-        }
-        if (__syncthreads_or(in)) found = true;
-      }
-      __syncthreads();
+  const int nq = *n_need;
+  for (int k = blockIdx.x; k < nq; k += gridDim.x) {
+    const int c = need[k];
+    const int2 ab = cand[c];
+    if (threadIdx.x < 2) {
+      const int s = threadIdx.x == 0 ? ab.x : ab.y;
+      const int t = threadIdx.x == 0 ? ab.y : ab.x;
+      rel[threadIdx.x] = xf_relative_exact(poses[s], poses[t], rd);
     }
-    ok = found;
+    __syncthreads();
+    bool ok = true;
+    for (int dir = 0; dir < 2 && ok; ++dir) {
+      const FrameDev Fa = frames[dir == 0 ? ab.x : ab.y];
+      const FrameDev Fb = frames[dir == 0 ? ab.y : ab.x];
+      const int ord = Fa.n_valid_depth == 1 ? rd.apply_1 : rd.apply_n;
+      const int nt = Fa.tiles_x * Fa.tiles_y;
+      bool found = false;
+      for (int t0 = 0; t0 < nt && !found; t0 += 1024) {
+        if (threadIdx.x == 0) n_partial = 0;
+        __syncthreads();
+        bool any_in = false;
+        for (int t = t0 + threadIdx.x; t < min(nt, t0 + 1024); t += blockDim.x) {
+          const int cls = classify_tile(rel[dir], Fa.tiles[t], Fb);
+          if (cls == 1 && Fa.tile_count[t] > 0) any_in = true;
+          if (cls == 2) partial[atomicAdd(&n_partial, 1)] = t;
+        }
+        if (__syncthreads_or(any_in)) {
+          found = true;
+          break;
+        }
+        const int np = n_partial;
+        for (int q = 0; q < np && !found; ++q) {
+          const int t = partial[q];
+          const int x = (t % Fa.tiles_x) * SFB_TILE + (threadIdx.x % SFB_TILE);
+          const int y = (t / Fa.tiles_x) * SFB_TILE + (threadIdx.x / SFB_TILE);
+          bool in = false;
+          if (x < Fa.w && y < Fa.h) {
+            const float4 P = __ldg(&Fa.P[y * Fa.w + x]);
+            in = (__float_as_uint(P.w) & SFB_FLAG_VD) && point_inside(rel[dir], Fb, P, ord);
+          }
+          if (__syncthreads_or(in)) found = true;
+        }
+        __syncthreads();
+      }
+      ok = found;
+    }
+    if (threadIdx.x == 0) pass[c] = ok ? 1 : 0;
+    __syncthreads();  // rel / partial are rewritten by the next queued candidate
   }
-  if (threadIdx.x == 0) pass[blockIdx.x] = ok ? 1 : 0;
 }
 
 void launch_overlap(const FrameDev* frames, const PoseDev* poses, const int2* cand, int n_cand,
                     Rounding rd, int full_count, uint8_t* pass, int* counts, cudaStream_t s,
-                    int rank, int world) {
+                    int rank, int world, int* need, int* n_need, int n_sm) {
   if (n_cand <= 0) return;
-  sfb_count_launch();
-  if (full_count)
+  if (full_count) {
+    sfb_count_launch();
     k_overlap<<<n_cand, 256, 0, s>>>(frames, poses, cand, rd, full_count, pass, counts);
-  else
-    k_overlap_culled<<<n_cand, 256, 0, s>>>(frames, poses, cand, rd, pass, rank, world);
+    return;
+  }
+  cudaMemsetAsync(n_need, 0, sizeof(int), s);
+  sfb_count_launch(2);
+  k_overlap_prefilter<<<(n_cand + 255) / 256, 256, 0, s>>>(frames, poses, cand, n_cand, pass, need,
+                                                           n_need, rank, world);
+  const int grid = std::min(n_cand, 8 * n_sm);  // persistent over the (device-sized) queue
+  k_overlap_culled<<<grid, 256, 0, s>>>(frames, poses, cand, rd, pass, need, n_need);
 }

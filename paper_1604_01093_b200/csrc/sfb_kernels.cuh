@@ -194,7 +194,8 @@ void launch_angle_gate(const PoseDev* poses, int n, Rounding rd, double cos_min,
                        cudaStream_t s);
 void launch_overlap(const FrameDev* frames, const PoseDev* poses, const int2* cand, int n_cand,
                     Rounding rd, int full_count, uint8_t* pass, int* counts, cudaStream_t s,
-                    int rank = 0, int world = 1);
+                    int rank = 0, int world = 1, int* need = nullptr, int* n_need = nullptr,
+                    int n_sm = 148);
 void launch_associate(const DenseArgs& a, int src, int dst, int kind, uint8_t* sel, int* tgt,
                       cudaStream_t s);
 void launch_point_eval(const FrameDev* frames, const PoseDev* poses, int src, int dst, int kind,

@@ -1,4 +1,4 @@
 cd $GRAFT_REPO_ROOT
-python tools/build_variant.py count -- -DDENSE_COUNT > /dev/null 2>&1 || true
-SFB_LIB=$GRAFT_REPO_ROOT/variants/count.so timeout 500 python tools/dense_count.py cfg4
-./tools/micro/dmma_rate
+timeout 900 python -m pytest tests -x -q -m gpu -p no:cacheprovider 2>&1 | tail -2
+CFG=cfg5 VARIANTS="cur" bash tools/gpu_variants.sh
+VARIANTS="cur" bash tools/gpu_variants.sh
