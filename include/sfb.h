@@ -104,6 +104,10 @@ int sfb_frames_upload(sfb_ctx* ctx, int32_t n, const sfb_frame_desc* descs,
                       int32_t* slots_out);
 int sfb_frames_release(sfb_ctx* ctx, int32_t n, const int32_t* slots);
 
+/* page-locked host memory (cudaMallocHost) for reusable staging buffers */
+int sfb_host_alloc(int64_t bytes, void** ptr);
+int sfb_host_free(void* ptr);
+
 /* ---- build_cache (frames.py:75-151) on the device ---------------------- */
 /* n RGB-D frames of width x height (colour (H, W, 3) uint8, depth (H, W)
  * float32; host pageable, pinned, or device pointers) -> their CachedFrame

@@ -129,6 +129,8 @@ SIGNATURES = {
     "sfb_profile_read": [_P, _P, _P, _I32],
     "sfb_launch_count": [C.POINTER(_I64)],
     "sfb_frames_set_intensity": [_P, _I32, _P, _P],
+    "sfb_host_alloc": [_I64, C.POINTER(_P)],
+    "sfb_host_free": [_P],
     "sfb_gn_step_begin": [_P, _I32, _D, _I32, C.POINTER(Weights), _I32, _I32, _D,
                           C.POINTER(Config), C.POINTER(_I32)],
     "sfb_gn_step_end": [_P, _P],

@@ -22,6 +22,32 @@ NVCC_FLAGS = [
 ]
 
 
+HOST_SRC = CSRC / "host" / "sfbhost.c"
+
+
+def host_module_path() -> Path:
+    import sysconfig
+    return PKG / ("_sfbhost" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
+def build_host(force: bool = False) -> Path:
+    """The CPython helper module (_sfbhost: correspondence-set stacking) with gcc."""
+    import sysconfig
+    out = host_module_path()
+    if not force and out.exists() and out.stat().st_mtime >= HOST_SRC.stat().st_mtime:
+        return out
+    tmp = out.with_suffix(".tmp")
+    import numpy
+    cmd = [os.environ.get("CC", "gcc"), "-O2", "-shared", "-fPIC", "-Wall",
+           "-I", sysconfig.get_paths()["include"], "-I", numpy.get_include(), str(HOST_SRC),
+           "-o", str(tmp)]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"gcc failed ({res.returncode}):\n{res.stdout}\n{res.stderr}")
+    os.replace(tmp, out)
+    return out
+
+
 def _nvcc() -> str:
     for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", shutil.which("nvcc")):
         if cand and Path(cand).exists():
@@ -45,6 +71,8 @@ def build(force: bool = False, verbose: bool = False, out: Path | None = None,
           extra: list[str] | None = None) -> Path:
     """Compile libsfb.so (or a tuning variant at `out` with `extra` nvcc flags)."""
     lib = Path(out) if out else LIB
+    if out is None:
+        build_host(force)
     if out is None and not force and not needs_rebuild():
         return LIB
     tmp = lib.with_suffix(".so.tmp")

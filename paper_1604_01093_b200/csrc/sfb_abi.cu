@@ -1010,6 +1010,18 @@ int sfb_frames_release(sfb_ctx* c, int32_t n, const int32_t* slots) {
   return SFB_OK;
 }
 
+// Page-locked host staging (reused by the host runtime across calls).
+int sfb_host_alloc(int64_t bytes, void** ptr) {
+  if (!ptr || bytes < 0) return fail(nullptr, SFB_E_ARG, "bad arguments");
+  cudaError_t e = cudaMallocHost(ptr, (size_t)std::max<int64_t>(bytes, 1));
+  if (e != cudaSuccess) return fail(nullptr, SFB_E_OOM, cudaGetErrorString(e));
+  return SFB_OK;
+}
+int sfb_host_free(void* ptr) {
+  if (ptr) cudaFreeHost(ptr);
+  return SFB_OK;
+}
+
 int sfb_frames_set_intensity(sfb_ctx* c, int32_t n, const int32_t* slots,
                              const float* const* intensity) {
   if (!c || n < 0 || (n > 0 && (!slots || !intensity))) return fail(c, SFB_E_ARG, "bad arguments");

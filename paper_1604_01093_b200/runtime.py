@@ -63,6 +63,9 @@ class Runtime:
         _abi.check(self.lib.sfb_ctx_set_rounding(h, C.byref(r)), h)
         self._frames: dict[int, tuple[int, object]] = {}
         self._with_intensity: set[int] = set()  # slots holding intensity_low
+        self._staging: dict = {}
+        self._staging_addr: dict = {}
+        self._staging_ptrs: list = []
         self._lock = threading.Lock()
 
     # -- frame store --------------------------------------------------------
@@ -81,7 +84,19 @@ class Runtime:
 
     def _upload(self, caches) -> None:
         n = len(caches)
-        descs = np.zeros(n, dtype=_DESC_DTYPE)  # the sfb_frame_desc array, filled by column
+        descs = np.zeros(n, dtype=_DESC_DTYPE)  # the sfb_frame_desc array
+        try:
+            from . import _sfbhost
+            native = _sfbhost.fill_frame_descs(caches, descs) is not None
+        except ImportError:
+            native = False
+        if native:  # every plane already in the library's layout: no copies
+            slots = np.zeros(n, dtype=np.int32)
+            _abi.check(self.lib.sfb_frames_upload(self.handle, n, descs.ctypes.data_as(
+                C.POINTER(_abi.FrameDesc)), _abi.ptr(slots)), self.handle)
+            for c, s in zip(caches, slots):
+                self._frames[id(c)] = (int(s), c)
+            return
         keep = []
         dims = np.empty((n, 2), dtype=np.int32)
         kk = np.empty((n, 4), dtype=np.float64)
@@ -136,6 +151,23 @@ class Runtime:
                 self._with_intensity.update(todo)
         return slots
 
+    def staging(self, key: str, nbytes: int) -> np.ndarray:
+        """A reusable page-locked host byte buffer of at least nbytes (grown
+        geometrically); its contents are clobbered by the next caller of the
+        same key, so users consume it before returning."""
+        buf = self._staging.get(key)
+        if buf is None or buf.nbytes < nbytes:
+            size = max(int(nbytes), 2 * (buf.nbytes if buf is not None else 0), 1 << 16)
+            ptr = C.c_void_p()
+            _abi.check(self.lib.sfb_host_alloc(size, C.byref(ptr)))
+            arr = np.ctypeslib.as_array((C.c_uint8 * size).from_address(ptr.value))
+            if buf is not None:
+                self._staging_ptrs.append(self._staging_addr[key])  # freed with the runtime
+            self._staging[key] = arr
+            self._staging_addr[key] = ptr.value
+            buf = arr
+        return buf
+
     def adopt(self, caches, slots) -> None:
         """Register caches whose planes were produced on the device
         (sfb_build_cache): already resident, intensity included."""
@@ -156,6 +188,8 @@ class Runtime:
 
     def __del__(self):
         try:
+            for ptr in list(self._staging_addr.values()) + self._staging_ptrs:
+                self.lib.sfb_host_free(C.c_void_p(ptr))
             self.lib.sfb_ctx_destroy(self.handle)
         except Exception:
             pass

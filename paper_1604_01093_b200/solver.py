@@ -111,13 +111,43 @@ _get_pj = operator.attrgetter("points_j")
 _get_dtype = operator.attrgetter("dtype")
 
 
-def _set_layout(corr_sets, frame_index):
+def _set_layout_native(corr_sets, frame_index, rt):
+    """_set_layout in C (_sfbhost.stack_sets_into) into the runtime's reusable
+    page-locked staging buffers; None when the sets need the NumPy path.  The
+    returned arrays alias staging memory: consume them before the next call."""
+    try:
+        from . import _sfbhost
+    except ImportError:
+        return None
+    n = len(corr_sets)
+    fr = rt.staging("sets_frames", 8 * n).view(np.int32)
+    of = rt.staging("sets_offsets", 8 * (n + 1)).view(np.int64)
+    rows = 1 << 14
+    for _ in range(2):
+        pi = rt.staging("sets_pi", 24 * rows).view(np.float64)
+        pj = rt.staging("sets_pj", 24 * rows).view(np.float64)
+        r = _sfbhost.stack_sets_into(corr_sets, frame_index, fr, of, pi, pj)
+        if r is None:
+            return None
+        if r >= 0:
+            return (fr[:2 * n].reshape(n, 2), of[:n + 1], pi[:3 * r].reshape(r, 3),
+                    pj[:3 * r].reshape(r, 3))
+        rows = -r - 1  # grow to the reported size and redo
+    return None
+
+
+def _set_layout(corr_sets, frame_index, rt=None):
     """(n_sets,2) problem-frame indices, offsets and stacked points for the ABI
-    (build_sparse_term's stacking, solver.py:89-111)."""
+    (build_sparse_term's stacking, solver.py:89-111).  With a runtime `rt`, the
+    C stacker writes into its reusable pinned staging (consume immediately)."""
     n = len(corr_sets)
     if n == 0:
         return (np.zeros((0, 2), dtype=np.int32), np.zeros(1, dtype=np.int64), np.zeros((0, 3)),
                 np.zeros((0, 3)))
+    if rt is not None:
+        lay = _set_layout_native(corr_sets, frame_index, rt)
+        if lay is not None:
+            return lay
     fi = np.fromiter(map(_get_fi, corr_sets), dtype=np.int64, count=n)
     fj = np.fromiter(map(_get_fj, corr_sets), dtype=np.int64, count=n)
     keys = np.fromiter(frame_index.keys(), dtype=np.int64, count=len(frame_index))
@@ -657,21 +687,22 @@ class AlignmentProblem:
 
                 def _layout():
                     try:
-                        box["v"] = _set_layout(self.corr_sets, index)
+                        box["v"] = _set_layout(self.corr_sets, index, rt)
                     except BaseException as e:  # re-raised on the caller's thread
                         box["e"] = e
 
+                rt = runtime(self._device)
                 th = threading.Thread(target=_layout, daemon=True)
                 th.start()
                 try:
-                    runtime(self._device).slots_for(cl)
+                    rt.slots_for(cl)
                 finally:
                     th.join()
                 if "e" in box:
                     raise box["e"]
                 frames, off, pi, pj = box["v"]
             else:
-                frames, off, pi, pj = _set_layout(self.corr_sets, index)
+                frames, off, pi, pj = _set_layout(self.corr_sets, index, runtime(self._device))
             self._dp = DeviceProblem(len(self.frame_ids), cl, frames, pi, pj, off,
                                      device=self._device)
             if self._xch is not None:

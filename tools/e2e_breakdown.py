@@ -21,16 +21,12 @@ for rep in range(4):
     torch.cuda.synchronize()
     t = [time.perf_counter()]
     p = S.AlignmentProblem(sc.frame_ids, sc.init, sc.corr_sets, caches); t.append(time.perf_counter())
-    cl = [caches[f] for f in sc.frame_ids]
-    rt.slots_for(cl); t.append(time.perf_counter())
-    index = {f: k for k, f in enumerate(sc.frame_ids)}
-    lay = S._set_layout(sc.corr_sets, index); t.append(time.perf_counter())
-    p._problem(); t.append(time.perf_counter())
+    p._problem(); t.append(time.perf_counter())  # frame upload || set stacking, problem create
     st = p.solve(W, C); torch.cuda.synchronize(); t.append(time.perf_counter())
     p.close(); t.append(time.perf_counter())
     d = np.diff(t) * 1e3
-    print(f"rep {rep}: init {d[0]:.1f}  frames {d[1]:.1f}  set_layout {d[2]:.1f}  "
-          f"problem(incl. layout) {d[3]:.1f}  solve {d[4]:.1f}  close {d[5]:.1f} ms", flush=True)
+    print(f"rep {rep}: init {d[0]:.1f}  frames+problem {d[1]:.1f}  solve {d[2]:.1f}  close {d[3]:.1f}"
+          f"  total {sum(d):.1f} ms", flush=True)
 
 # raw host->device copy rates for reference
 n = 341 * 1024 * 1024
