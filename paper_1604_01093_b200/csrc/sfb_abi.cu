@@ -308,6 +308,7 @@ struct sfb_problem : Handle {
   DBuf<uint8_t> f_fl, f_pass, f_temp;
   DBuf<int> f_cnt;
   DBuf<int> f_need;  // [0] queue length, then the undecided candidates (pair filter stage 2)
+  std::vector<int> pair_table;  // rebuild_structure's flat pair-id table
 };
 
 namespace {
@@ -435,10 +436,13 @@ int rebuild_structure(sfb_problem* p, int bidir) {
   // a hash map beyond that
   std::vector<int2> pv;
   const bool flat = (int64_t)nb * nb <= ((int64_t)16 << 20);
-  std::vector<int> pid_flat;
+  std::vector<int>& pid_flat = p->pair_table;  // persistent, all -1 between rebuilds
   std::unordered_map<int64_t, int> pid;
-  if (flat) pid_flat.assign((size_t)nb * nb, -1);
-  else pid.reserve(2 * (size_t)(p->n_sets + p->n_dir) + 8);
+  if (flat) {
+    if (pid_flat.size() != (size_t)nb * nb) pid_flat.assign((size_t)nb * nb, -1);
+  } else {
+    pid.reserve(2 * (size_t)(p->n_sets + p->n_dir) + 8);
+  }
   auto pair_of = [&](int a, int b) {
     const int64_t key = (int64_t)a * nb + b;
     if (flat) {
@@ -481,6 +485,8 @@ int rebuild_structure(sfb_problem* p, int bidir) {
   }
   p->n_pairs = (int)pv.size();
   p->pair_vars = pv;
+  if (flat)  // reset only the entries this rebuild touched
+    for (const int2& q : pv) pid_flat[(size_t)q.x * nb + q.y] = -1;
   auto to_csr = [](const std::vector<Contrib>& c, int rows, std::vector<int>& ptr,
                    std::vector<int>& ent) {
     ptr.assign(rows + 1, 0);
