@@ -107,3 +107,60 @@ def test_build_cache_matches_reference_fixture():
     from golden_io import GoldenScene
     s = GoldenScene("cfg2")
     assert s.cache_sha_ok
+
+
+def test_native_set_stacking_matches_numpy_path():
+    """_sfbhost.stack_sets_into == the NumPy stacking (build_sparse_term order),
+    falls back (None) on non-float64 points, and raises like the reference."""
+    import copy
+    from paper_1604_01093_b200 import _build
+    _build.build_host()
+    from paper_1604_01093_b200 import _sfbhost, synth
+    from paper_1604_01093_b200 import solver as S
+    sc = synth.make("cfg3")
+    index = {f: k for k, f in enumerate(sc.frame_ids)}
+    sets = sc.corr_sets
+    n = len(sets)
+    fr = np.empty(2 * n, np.int32)
+    of = np.empty(n + 1, np.int64)
+    small = np.empty(3, np.float64)
+    need = _sfbhost.stack_sets_into(sets, index, fr, of, small, small)
+    rows = -need - 1
+    assert rows == sum(len(s) for s in sets)
+    pi = np.empty(3 * rows)
+    pj = np.empty(3 * rows)
+    assert _sfbhost.stack_sets_into(sets, index, fr, of, pi, pj) == rows
+    ref = S._set_layout(sets, index)
+    assert np.array_equal(fr.reshape(-1, 2), ref[0]) and np.array_equal(of, ref[1])
+    assert np.array_equal(pi.reshape(-1, 3), ref[2]) and np.array_equal(pj.reshape(-1, 3), ref[3])
+    odd = copy.copy(sets[3])
+    odd.points_i = odd.points_i.astype(np.float32)
+    assert _sfbhost.stack_sets_into([sets[0], odd], index, fr, of, pi, pj) is None
+    bad = copy.copy(sets[1])
+    bad.frame_j = 10 ** 7
+    with pytest.raises(KeyError):
+        _sfbhost.stack_sets_into([bad], index, fr, of, pi, pj)
+    short = copy.copy(sets[2])
+    short.points_j = short.points_j[:-1]
+    with pytest.raises(ValueError):
+        _sfbhost.stack_sets_into([short], index, fr, of, pi, pj)
+
+
+def test_native_frame_descriptors():
+    from paper_1604_01093_b200 import _build
+    _build.build_host()
+    from paper_1604_01093_b200 import _sfbhost, synth
+    from paper_1604_01093_b200.runtime import _DESC_DTYPE
+    sc = synth.make("cfg2")
+    caches = [sc.caches[f] for f in sc.frame_ids]
+    d = np.zeros(len(caches), dtype=_DESC_DTYPE)
+    assert _sfbhost.fill_frame_descs(caches, d) is True
+    for k, c in enumerate(caches):
+        assert (d[k]["width"], d[k]["height"]) == c.valid_depth.shape[::-1]
+        assert d[k]["points"] == c.points_low.ctypes.data
+        assert d[k]["grad"] == c.grad_low.ctypes.data
+        assert d[k]["fx"] == c.intrinsics_low.fx and d[k]["cy"] == c.intrinsics_low.cy
+    import copy
+    odd = copy.copy(caches[0])
+    odd.points_low = np.asfortranarray(odd.points_low)
+    assert _sfbhost.fill_frame_descs([odd], d) is None

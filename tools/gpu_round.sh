@@ -30,3 +30,4 @@ timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none -c 4000 -
 echo launchbench rc=$?
 timeout 600 python tools/bench_tsdf.py > gpurun_out/bench_tsdf.log 2>&1
 echo tsdf rc=$?
+for c in cfg3 cfg5; do timeout 900 python bench.py --config $c > gpurun_out/bench_$c.log 2>&1; echo bench$c rc=$?; done
