@@ -496,22 +496,16 @@ __global__ void __launch_bounds__(DENSE_THREADS, DENSE_MIN_BLOCKS) k_dense_fused
     if (tgt >= 0 || (PREV && ptg != 0xFFFF)) {
       if (tgt < 0) N = __ldg(&Fi.N[p]);
       const double n0 = N.x, n1 = N.y, n2 = N.z;
-      if (PREV && ptg != 0xFFFF) {
-        const float4 PT = __ldg(&Fj.P[ptg]);
-        const double t0 = PT.x, t1 = PT.y, t2 = PT.z;
-        const double m0 = ec.back[0] * t0 + ec.back[1] * t1 + ec.back[2] * t2 + ec.back[9];
-        const double m1 = ec.back[3] * t0 + ec.back[4] * t1 + ec.back[5] * t2 + ec.back[10];
-        const double m2 = ec.back[6] * t0 + ec.back[7] * t1 + ec.back[8] * t2 + ec.back[11];
-        const double r = n0 * (d0 - m0) + n1 * (d1 - m1) + n2 * (d2 - m2);
-        eprev_g += r * r;
-      }
+      double r_new = 0.0;
       if (tgt >= 0) {
-        const float4 PT = __ldg(&Fj.P[tgt]);
+        const float4 PT = __ldg(&Fj.P[tgt]);  // (L1 hit; keeping the association's copy
+                                               // live costs more in registers)
         const double t0 = PT.x, t1 = PT.y, t2 = PT.z;
         const double m0 = ec.back[0] * t0 + ec.back[1] * t1 + ec.back[2] * t2 + ec.back[9];
         const double m1 = ec.back[3] * t0 + ec.back[4] * t1 + ec.back[5] * t2 + ec.back[10];
         const double m2 = ec.back[6] * t0 + ec.back[7] * t1 + ec.back[8] * t2 + ec.back[11];
         const double r = n0 * (d0 - m0) + n1 * (d1 - m1) + n2 * (d2 - m2);
+        r_new = r;
         // J_i = M_j v, v = [p_t x n_j ; -n_j], n_j = R_j^T R_i n = rel.R n
         const double nj0 = ec.rel.R[0] * n0 + ec.rel.R[1] * n1 + ec.rel.R[2] * n2;
         const double nj1 = ec.rel.R[3] * n0 + ec.rel.R[4] * n1 + ec.rel.R[5] * n2;
@@ -520,6 +514,20 @@ __global__ void __launch_bounds__(DENSE_THREADS, DENSE_MIN_BLOCKS) k_dense_fused
                              -nj0, -nj1, -nj2};
         accum_row(acc, v, r, a.s_geo);
         acc[28] += r * r;
+      }
+      if (PREV && ptg != 0xFFFF) {
+        if (ptg == tgt) {
+          // the previous pass froze the same target: same residual at these poses
+          eprev_g += r_new * r_new;
+        } else {
+          const float4 PT = __ldg(&Fj.P[ptg]);
+          const double t0 = PT.x, t1 = PT.y, t2 = PT.z;
+          const double m0 = ec.back[0] * t0 + ec.back[1] * t1 + ec.back[2] * t2 + ec.back[9];
+          const double m1 = ec.back[3] * t0 + ec.back[4] * t1 + ec.back[5] * t2 + ec.back[10];
+          const double m2 = ec.back[6] * t0 + ec.back[7] * t1 + ec.back[8] * t2 + ec.back[11];
+          const double r = n0 * (d0 - m0) + n1 * (d1 - m1) + n2 * (d2 - m2);
+          eprev_g += r * r;
+        }
       }
     }
   }
