@@ -830,6 +830,7 @@ int sfb_ctx_set_rounding(sfb_ctx* c, const sfb_rounding* r) {
 int sfb_frames_upload(sfb_ctx* c, int32_t n, const sfb_frame_desc* d, int32_t* slots_out) {
   if (!c || n < 0 || (n > 0 && (!d || !slots_out))) return fail(c, SFB_E_ARG, "bad arguments");
   if (n == 0) return SFB_OK;
+  const auto t_start = std::chrono::steady_clock::now();
   CK(c, cudaSetDevice(c->device));
   size_t total = 0, stage = 0;
   for (int k = 0; k < n; ++k) {
@@ -938,9 +939,9 @@ int sfb_frames_upload(sfb_ctx* c, int32_t n, const sfb_frame_desc* d, int32_t* s
     max_nt = std::max(max_nt, (int)nt);
     devs[k] = f;
   }
-  // one batched H2D for every plane of every frame (CUDA >= 12.8), else a loop
-  // (cudaMemcpyBatchAsync crashed on pageable sources on the 580 driver; the
-  // pinned fast path above needs no copies at all)
+  const auto t_scan = std::chrono::steady_clock::now();
+  // pageable planes by DMA, one call each (cudaMemcpyBatchAsync crashed on
+  // pageable sources on the 580 driver)
   for (size_t q = 0; q < cdst.size(); ++q)
     CK(c, cudaMemcpyAsync(cdst[q], csrc[q], csz[q], cudaMemcpyHostToDevice, c->stream));
   if (!jobs.empty()) {
@@ -956,6 +957,12 @@ int sfb_frames_upload(sfb_ctx* c, int32_t n, const sfb_frame_desc* d, int32_t* s
   std::vector<int> cnt(3 * n);
   CK(c, cudaMemcpyAsync(cnt.data(), c->counts.p, sizeof(int) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
   CK(c, cudaStreamSynchronize(c->stream));
+  if (trace_on()) {
+    const auto t_end = std::chrono::steady_clock::now();
+    fprintf(stderr, "sfb frames_upload: %d frames, scan %.2f ms (pointer checks), copy+pack %.2f ms\n", n,
+            std::chrono::duration<double, std::milli>(t_scan - t_start).count(),
+            std::chrono::duration<double, std::milli>(t_end - t_scan).count());
+  }
   for (int k = 0; k < n; ++k)
     if (cnt[3 * k + 2] != 0) {
       c->free_blocks.emplace(block_bytes, block);
