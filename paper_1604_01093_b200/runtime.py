@@ -69,20 +69,27 @@ class Runtime:
         self._lock = threading.Lock()
 
     # -- frame store --------------------------------------------------------
-    def slots_for(self, caches) -> list[int]:
-        """Slots of the given caches, uploading the ones not yet resident."""
-        with self._lock:
-            missing = []
-            seen = set()
-            for c in caches:
-                if id(c) not in self._frames and id(c) not in seen:
-                    missing.append(c)
-                    seen.add(id(c))
-            if missing:
-                self._upload(missing)
-            return [self._frames[id(c)][0] for c in caches]
+    def slots_for(self, caches, on_submit=None) -> list[int]:
+        """Slots of the given caches, uploading the ones not yet resident.
+        `on_submit()` runs once the upload is about to enter the library (which
+        drops the GIL), or right away when nothing needs uploading."""
+        try:
+            with self._lock:
+                missing = []
+                seen = set()
+                for c in caches:
+                    if id(c) not in self._frames and id(c) not in seen:
+                        missing.append(c)
+                        seen.add(id(c))
+                if missing:
+                    self._upload(missing, on_submit)
+                    on_submit = None
+                return [self._frames[id(c)][0] for c in caches]
+        finally:
+            if on_submit is not None:
+                on_submit()
 
-    def _upload(self, caches) -> None:
+    def _upload(self, caches, on_submit=None) -> None:
         n = len(caches)
         descs = np.zeros(n, dtype=_DESC_DTYPE)  # the sfb_frame_desc array
         try:
@@ -92,6 +99,8 @@ class Runtime:
             native = False
         if native:  # every plane already in the library's layout: no copies
             slots = np.zeros(n, dtype=np.int32)
+            if on_submit is not None:
+                on_submit()
             _abi.check(self.lib.sfb_frames_upload(self.handle, n, descs.ctypes.data_as(
                 C.POINTER(_abi.FrameDesc)), _abi.ptr(slots)), self.handle)
             for c, s in zip(caches, slots):
@@ -124,6 +133,8 @@ class Runtime:
         for q, name in enumerate(("valid_depth", "valid_normal", "points", "normals", "grad")):
             descs[name] = ptrs[:, q]
         slots = np.zeros(n, dtype=np.int32)
+        if on_submit is not None:
+            on_submit()
         _abi.check(self.lib.sfb_frames_upload(self.handle, n, descs.ctypes.data_as(
             C.POINTER(_abi.FrameDesc)), _abi.ptr(slots)), self.handle)
         for c, s in zip(caches, slots):

@@ -681,26 +681,29 @@ class AlignmentProblem:
             index = {f: k for k, f in enumerate(self.frame_ids)}
             cl = [self.caches[f] for f in self.frame_ids] if self.caches is not None else None
             if cl is not None and len(self.corr_sets) > 256:
-                # stack the correspondence sets on a helper thread while the
-                # frame upload runs in the library (ctypes drops the GIL there)
+                # upload the frames on a helper thread and stack the correspondence
+                # sets here as soon as the upload is inside the library (ctypes
+                # drops the GIL there), so the two overlap instead of queueing
+                rt = runtime(self._device)
                 box = {}
+                submitted = threading.Event()
 
-                def _layout():
+                def _upload():
                     try:
-                        box["v"] = _set_layout(self.corr_sets, index, rt)
+                        rt.slots_for(cl, on_submit=submitted.set)
                     except BaseException as e:  # re-raised on the caller's thread
                         box["e"] = e
+                        submitted.set()
 
-                rt = runtime(self._device)
-                th = threading.Thread(target=_layout, daemon=True)
+                th = threading.Thread(target=_upload, daemon=True)
                 th.start()
+                submitted.wait()
                 try:
-                    rt.slots_for(cl)
+                    frames, off, pi, pj = _set_layout(self.corr_sets, index, rt)
                 finally:
                     th.join()
                 if "e" in box:
                     raise box["e"]
-                frames, off, pi, pj = box["v"]
             else:
                 frames, off, pi, pj = _set_layout(self.corr_sets, index, runtime(self._device))
             self._dp = DeviceProblem(len(self.frame_ids), cl, frames, pi, pj, off,
