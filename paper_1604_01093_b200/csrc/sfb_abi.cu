@@ -284,6 +284,13 @@ struct sfb_problem : Handle {
   bool pending_dense_on = false;
   int pending_prev_mode = 0;
   bool pending_gn_relin = false;
+  // speculative PCG of the next GN iteration (sfb_gn_step_end)
+  bool spec_pcg = false;
+  int spec_pcg_args[2] = {0, 0};
+  double spec_pcg_tol = 0.0;
+  int spec_max_it = 0, spec_restart = 1;
+  double spec_tol = 0.0;
+  cudaEvent_t d2h_done = nullptr;
   bool pending_energy_dense = false;
   // data-parallel sharding over directed dense edges
   int shard_rank = 0, shard_world = 1;
@@ -712,6 +719,7 @@ int enqueue_linearize_end(sfb_problem* p) {
   }
   p->dense_active = dense_on;
   p->have_system = true;
+  p->spec_pcg = false;  // a speculative PCG belongs to the previous system
   p->have_solution = false;
   return SFB_OK;
 }
@@ -1727,6 +1735,7 @@ int sfb_problem_destroy(sfb_problem* p) {
   p->f_cnt.release();
   p->f_need.release();
   if (p->hscal) pinned_scalars_release(p->hscal);
+  if (p->d2h_done) cudaEventDestroy(p->d2h_done);
   if (p->stream) cudaStreamDestroy(p->stream);
   delete p;
   return SFB_OK;
@@ -1952,6 +1961,7 @@ int sfb_pcg(sfb_problem* p, int32_t max_it, double tol, int32_t restart, int32_t
   a.restart = restart;
   a.out_scalars = p->dscal.p + 8;
   a.skip = nullptr;
+  p->spec_pcg = false;
   if (p->n_blk > 0) {
     ProfScope ps(p->prof, 2, p->stream);
     CK(p, launch_pcg(a, p->ctx->n_sm, p->stream));
@@ -2375,14 +2385,22 @@ int sfb_gn_step_begin(sfb_problem* p, int32_t max_it, double tol, int32_t restar
   if (restart < 1) return fail(p, SFB_E_ARG, "pcg_restart_interval must be >= 1");
   CK(p, cudaSetDevice(p->ctx->device));
   cudaStream_t s = p->stream;
+  p->spec_max_it = max_it;  // the PCG parameters a speculative PCG will reuse
+  p->spec_tol = tol;
+  p->spec_restart = restart;
   if (p->n_blk > 0) {
-    PcgArgs a = pcg_args(p);
-    a.max_it = max_it;
-    a.tol = tol;
-    a.restart = restart;
-    a.out_scalars = p->dscal.p + 8;
-    a.skip = nullptr;
-    {
+    // the previous _end may already have enqueued this PCG (same system,
+    // same parameters) to run while the host decided to continue
+    const bool have = p->spec_pcg && p->spec_pcg_args[0] == max_it &&
+                      p->spec_pcg_tol == tol && p->spec_pcg_args[1] == restart;
+    p->spec_pcg = false;
+    if (!have) {
+      PcgArgs a = pcg_args(p);
+      a.max_it = max_it;
+      a.tol = tol;
+      a.restart = restart;
+      a.out_scalars = p->dscal.p + 8;
+      a.skip = nullptr;
       ProfScope ps(p->prof, 2, s);
       CK(p, launch_pcg(a, p->ctx->n_sm, s));
     }
@@ -2417,7 +2435,27 @@ int sfb_gn_step_end(sfb_problem* p, double out[10]) {
   int rc = relin ? enqueue_linearize_end(p) : enqueue_energy_frozen_end(p, p->dscal.p + 16);
   if (rc) return rc;
   CK(p, cudaMemcpyAsync(p->hscal, p->dscal.p, 20 * sizeof(double), cudaMemcpyDeviceToHost, s));
-  CK(p, cudaStreamSynchronize(s));
+  if (!p->d2h_done) CK(p, cudaEventCreateWithFlags(&p->d2h_done, cudaEventDisableTiming));
+  CK(p, cudaEventRecord(p->d2h_done, s));
+  if (relin && p->n_blk > 0) {
+    // Speculative next PCG on the system just assembled: it runs while the
+    // host reads these scalars and decides; a stop (converged / aborted /
+    // energy <= 1e-18) simply never consumes it - it only writes the PCG
+    // vectors and status words, which nothing else reads.
+    PcgArgs a = pcg_args(p);
+    a.max_it = p->spec_max_it;
+    a.tol = p->spec_tol;
+    a.restart = p->spec_restart;
+    a.out_scalars = p->dscal.p + 8;
+    a.skip = nullptr;
+    ProfScope ps(p->prof, 2, s);
+    CK(p, launch_pcg(a, p->ctx->n_sm, s));
+    p->spec_pcg = true;
+    p->spec_pcg_args[0] = a.max_it;
+    p->spec_pcg_args[1] = a.restart;
+    p->spec_pcg_tol = a.tol;
+  }
+  CK(p, cudaEventSynchronize(p->d2h_done));
   const double* h = p->hscal;
   out[0] = p->n_blk > 0 ? h[8] : 0.0;
   out[1] = p->n_blk > 0 ? h[9] : 0.0;
