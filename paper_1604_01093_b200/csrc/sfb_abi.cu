@@ -428,6 +428,7 @@ int rebuild_structure(sfb_problem* p, int bidir) {
     gw += (int64_t)nt * 256;
   }
   p->n_items = (int)items.size();
+  const auto t_items = std::chrono::steady_clock::now();
 
   // Contribution lists as CSR, built in two counting passes (entries keep
   // set order then edge order, so every sum is assembled in a fixed order).
@@ -490,6 +491,7 @@ int rebuild_structure(sfb_problem* p, int bidir) {
       bc.push_back({pair_of(a, b), d << 3 | 4});
     }
   }
+  const auto t_pairs = std::chrono::steady_clock::now();
   p->n_pairs = (int)pv.size();
   p->pair_vars = pv;
   if (flat)  // reset only the entries this rebuild touched
@@ -559,6 +561,10 @@ int rebuild_structure(sfb_problem* p, int bidir) {
   CK(p, cudaStreamSynchronize(s));  // host vectors die here
   if (trace_on()) {
     const auto t_end = std::chrono::steady_clock::now();
+    fprintf(stderr, "sfb rebuild_structure: items %.2f ms, pairs %.2f ms, csr+rows %.2f ms; ",
+            std::chrono::duration<double, std::milli>(t_items - t_start).count(),
+            std::chrono::duration<double, std::milli>(t_pairs - t_items).count(),
+            std::chrono::duration<double, std::milli>(t_host - t_pairs).count());
     fprintf(stderr, "sfb rebuild_structure: host %.2f ms, alloc+upload %.2f ms (%d dir edges, %d pairs)\n",
             std::chrono::duration<double, std::milli>(t_host - t_start).count(),
             std::chrono::duration<double, std::milli>(t_end - t_host).count(), p->n_dir, p->n_pairs);
