@@ -92,3 +92,82 @@ def test_dense_verify_on_device_caches_matches_host_caches():
     r_host = F.dense_verify_many([(sc.caches[a], sc.caches[b], T[(a, b)]) for a, b in pairs],
                                  F.FilterConfig())
     assert r_dev == r_host
+
+
+class TestReferenceBuildCache:
+    """test_frames.py:17-80 through build_cache_device (and equal to the host
+    build_cache on each input)."""
+
+    @staticmethod
+    def _k():
+        from paper_1604_01093_b200 import se3
+        return se3.Intrinsics(525.0, 525.0, 319.5, 239.5, 640, 480)
+
+    @staticmethod
+    def _frame(depth_value=2.0, index=0, color=None):
+        from paper_1604_01093_b200.cache import RgbdFrame
+        depth = np.full((480, 640), depth_value, dtype=np.float32)
+        if color is None:
+            rng = np.random.default_rng(index + 1)
+            color = rng.integers(0, 255, size=(480, 640, 3), dtype=np.uint8)
+        return RgbdFrame(index=index, color=color, depth=depth)
+
+    def _dev(self, frame):
+        from paper_1604_01093_b200 import cache as CA
+        c = CA.build_cache_device([frame], self._k())[0]
+        h = CA.build_cache(frame, self._k())
+        for p in PLANES:
+            a, b = np.asarray(getattr(c, p)), np.asarray(getattr(h, p))
+            assert a.dtype == b.dtype and np.array_equal(a, b), p
+        return c
+
+    def test_planar_frame_normals(self):
+        cache = self._dev(self._frame(depth_value=2.0))
+        ok = cache.valid_normal
+        assert np.count_nonzero(ok) > 0.9 * ok.size
+        assert np.allclose(cache.normals_low[ok], [0.0, 0.0, -1.0], atol=1e-3)
+
+    def test_all_invalid_depth(self):
+        frame = self._frame()
+        frame.depth[:] = 0.0
+        cache = self._dev(frame)
+        assert np.count_nonzero(cache.valid_depth) == 0
+        assert np.count_nonzero(cache.valid_normal) == 0
+
+    def test_intensity_ramp_gradient(self):
+        xs = np.arange(640, dtype=np.float32) / 640.0
+        gray = np.tile((xs * 255).astype(np.uint8), (480, 1))
+        cache = self._dev(self._frame(color=np.repeat(gray[..., None], 3, axis=2)))
+        interior = cache.grad_low[5:-5, 5:-5]
+        expected = 1.0 / 80.0
+        assert np.all(np.abs(interior[..., 0] - expected) < 0.05 * expected)
+        assert np.all(np.abs(interior[..., 1]) < 1e-4)
+
+    def test_points_match_unprojection(self):
+        cache = self._dev(self._frame())
+        ys, xs = np.nonzero(cache.valid_depth)
+        pix = np.stack([xs, ys], axis=-1).astype(np.float64)
+        expected = cache.intrinsics_low.unproject(pix, cache.depth_low[ys, xs])
+        assert np.allclose(cache.points_low[ys, xs], expected.astype(np.float32))
+
+    def test_points_reproject_to_pixel_centers(self):
+        frame = self._frame()
+        rng = np.random.default_rng(0)
+        frame.depth += rng.uniform(-0.2, 0.2, size=frame.depth.shape).astype(np.float32)
+        cache = self._dev(frame)
+        ys, xs = np.nonzero(cache.valid_depth)
+        pix, in_front = cache.intrinsics_low.project_many(cache.points_low[ys, xs].astype(np.float64))
+        assert np.all(in_front)
+        assert np.all(np.abs(pix[:, 0] - xs) < 0.5) and np.all(np.abs(pix[:, 1] - ys) < 0.5)
+
+    def test_deterministic(self):
+        frame = self._frame(index=3)
+        a, b = self._dev(frame), self._dev(frame)
+        for p in PLANES:
+            assert np.array_equal(getattr(a, p), getattr(b, p))
+
+    def test_median_ignores_invalid_samples(self):
+        frame = self._frame(depth_value=2.0)
+        frame.depth[0:8, 0:8] = 0.0
+        frame.depth[0, 0] = 2.0
+        assert self._dev(frame).depth_low[0, 0] == np.float32(2.0)
