@@ -25,228 +25,8 @@
 static std::atomic<long long> g_launches{0};
 void sfb_count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
-namespace {
+#include "sfb_host.cuh"
 
-thread_local std::string g_tls_err;
-
-// CUDA-event timing of kernel classes on one stream (enabled per problem).
-struct Prof {
-  bool on = false;
-  double ms[SFB_PROF_CLASSES] = {0};
-  int64_t n[SFB_PROF_CLASSES] = {0};
-  struct Pending {
-    int cls;
-    cudaEvent_t a, b;
-  };
-  std::vector<Pending> pending;
-  std::vector<cudaEvent_t> pool;
-  cudaEvent_t get() {
-    if (pool.empty()) {
-      cudaEvent_t e;
-      cudaEventCreate(&e);
-      return e;
-    }
-    cudaEvent_t e = pool.back();
-    pool.pop_back();
-    return e;
-  }
-  void begin(int cls, cudaStream_t s, Pending* slot) {
-    slot->cls = cls;
-    slot->a = get();
-    slot->b = get();
-    cudaEventRecord(slot->a, s);
-  }
-  void end(const Pending& pd, cudaStream_t s) {
-    cudaEventRecord(pd.b, s);
-    pending.push_back(pd);
-  }
-  // call after a stream sync
-  void drain() {
-    for (auto& pd : pending) {
-      float t = 0.f;
-      if (cudaEventElapsedTime(&t, pd.a, pd.b) == cudaSuccess) {
-        ms[pd.cls] += t;
-        n[pd.cls] += 1;
-      }
-      pool.push_back(pd.a);
-      pool.push_back(pd.b);
-    }
-    pending.clear();
-  }
-  void destroy() {
-    drain();
-    for (auto e : pool) cudaEventDestroy(e);
-    pool.clear();
-  }
-};
-
-// RAII scope: times the kernels enqueued inside it as one class.
-struct ProfScope {
-  Prof* pr;
-  cudaStream_t s;
-  Prof::Pending pd{};
-  ProfScope(Prof& p, int cls, cudaStream_t st) : pr(p.on ? &p : nullptr), s(st) {
-    if (pr) pr->begin(cls, s, &pd);
-  }
-  ~ProfScope() {
-    if (pr) pr->end(pd, s);
-  }
-};
-
-struct Handle {
-  std::string err;
-};
-
-bool trace_on() {
-  static const bool on = getenv("SFB_TRACE") != nullptr;
-  return on;
-}
-
-// Process-wide cache of idle device allocations (per device, keyed by size).
-// Blocks enter it only from DBuf::release(), which callers invoke after the
-// owning stream has been synchronised, so a cached block is never in flight.
-struct DevCache {
-  std::mutex mu;
-  std::map<std::pair<int, size_t>, std::vector<void*>> free;
-  size_t bytes = 0;
-  static constexpr size_t kLimit = (size_t)8 << 30;
-  static size_t round(size_t b) {
-    if (b <= 4096) return 4096;
-    size_t r = 4096;
-    while (r < b && r < ((size_t)1 << 26)) r <<= 1;  // powers of two up to 64 MiB
-    return r < b ? ((b + ((size_t)2 << 20) - 1) & ~(((size_t)2 << 20) - 1)) : r;
-  }
-  cudaError_t alloc(void** p, size_t b) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const size_t rb = round(b);
-    {
-      std::lock_guard<std::mutex> g(mu);
-      auto it = free.find({dev, rb});
-      if (it != free.end() && !it->second.empty()) {
-        *p = it->second.back();
-        it->second.pop_back();
-        bytes -= rb;
-        return cudaSuccess;
-      }
-    }
-    return cudaMalloc(p, rb);
-  }
-  void release(void* p, size_t b) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const size_t rb = round(b);
-    std::lock_guard<std::mutex> g(mu);
-    if (bytes + rb > kLimit) {
-      cudaFree(p);
-      return;
-    }
-    free[{dev, rb}].push_back(p);
-    bytes += rb;
-  }
-};
-DevCache& dev_cache() {
-  static DevCache* c = new DevCache();  // leaked on purpose: outlives static teardown
-  return *c;
-}
-
-// Pinned 64-double scalar mirrors for problem handles, recycled (a fresh
-// cudaMallocHost costs milliseconds).
-std::mutex g_pin_mu;
-std::vector<double*> g_pin_free;
-cudaError_t pinned_scalars(double** out) {
-  {
-    std::lock_guard<std::mutex> g(g_pin_mu);
-    if (!g_pin_free.empty()) {
-      *out = g_pin_free.back();
-      g_pin_free.pop_back();
-      return cudaSuccess;
-    }
-  }
-  return cudaMallocHost(reinterpret_cast<void**>(out), 64 * sizeof(double));
-}
-void pinned_scalars_release(double* p) {
-  std::lock_guard<std::mutex> g(g_pin_mu);
-  g_pin_free.push_back(p);
-}
-
-template <class T>
-struct DBuf {
-  T* p = nullptr;
-  size_t n = 0;
-  // Grow to at least `want` elements.  The old block may still be read by
-  // work in flight: with the owning stream given it is synchronised and the
-  // block recycled through the cache (cudaFree costs milliseconds on this
-  // driver); without one it is freed.
-  cudaError_t ensure(size_t want, cudaStream_t owner = nullptr) {
-    if (want <= n && p) return cudaSuccess;
-    const auto t0 = std::chrono::steady_clock::now();
-    const bool had = p != nullptr;
-    if (p) {
-      if (owner != nullptr && cudaStreamSynchronize(owner) == cudaSuccess)
-        dev_cache().release(p, n * sizeof(T));
-      else
-        cudaFree(p);
-    }
-    p = nullptr;
-    n = 0;
-    const size_t cnt = std::max<size_t>(want, 1);
-    cudaError_t e = dev_cache().alloc(reinterpret_cast<void**>(&p), cnt * sizeof(T));
-    if (e == cudaSuccess) n = cnt;
-    if (trace_on()) {
-      const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-      if (ms > 0.5) fprintf(stderr, "sfb ensure %zu B (%s): %.2f ms\n", cnt * sizeof(T), had ? "grow" : "new", ms);
-    }
-    return e;
-  }
-  void release() {  // caller has synchronised the stream that used the buffer
-    if (p) dev_cache().release(p, n * sizeof(T));
-    p = nullptr;
-    n = 0;
-  }
-};
-
-// Host twin of dot3o (sfb_internal.cuh): NumPy/OpenBLAS 3-term FMA chain
-// fma(a_k b_k, fma(a_j b_j, a_i * b_i)) for permutation code o.
-double host_dot3o(double a0, double a1, double a2, double b0, double b1, double b2, int o) {
-  static const int P[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
-  const double a[3] = {a0, a1, a2}, b[3] = {b0, b1, b2};
-  const int i = P[o][0], j = P[o][1], k = P[o][2];
-  volatile double p = a[i] * b[i];  // rounded product, kept out of the fma
-  return std::fma(a[k], b[k], std::fma(a[j], b[j], (double)p));
-}
-
-struct Slot {
-  FrameDev dev;
-  void* block = nullptr;
-  bool alive = false;
-  float* intensity = nullptr;  // owned (dev_cache), dense_verify only
-  size_t intensity_bytes = 0;
-};
-
-}  // namespace
-
-struct sfb_ctx : Handle {
-  int device = 0;
-  int n_sm = 148;
-  cudaStream_t stream = nullptr;
-  Rounding rd{2, 0, 0, 0, 2, 0};
-  std::vector<Slot> slots;
-  std::map<void*, int> block_refs;
-  DBuf<uint8_t> staging;
-  DBuf<int> counts;
-  DBuf<PackArgs> pack_args;
-  DBuf<VerifyItem> verify_items;
-  DBuf<CopyJob> copy_jobs;
-  DBuf<uint8_t> cache_raw, cache_out;
-  DBuf<CacheFrame> cache_frames;
-  DBuf<double> verify_err;
-  DBuf<long long> verify_cnt;
-  std::map<void*, size_t> block_size;
-  std::multimap<size_t, void*> free_blocks;  // released frame blocks kept for reuse
-  size_t cached_bytes = 0;
-  size_t cache_limit = (size_t)16 << 30;
-};
 
 struct sfb_problem : Handle {
   sfb_ctx* ctx = nullptr;
@@ -320,28 +100,6 @@ struct sfb_problem : Handle {
 
 namespace {
 
-int fail(Handle* h, int code, const std::string& msg) {
-  if (h) h->err = msg;
-  g_tls_err = msg;
-  return code;
-}
-
-#define CK(h, expr)                                                                    \
-  do {                                                                                 \
-    cudaError_t _e = (expr);                                                           \
-    if (_e != cudaSuccess) {                                                           \
-      return fail(h, _e == cudaErrorMemoryAllocation ? SFB_E_OOM : SFB_E_CUDA,         \
-                  std::string(#expr) + ": " + cudaGetErrorString(_e));                 \
-    }                                                                                  \
-  } while (0)
-
-#define CKL(h)                                                                         \
-  do {                                                                                 \
-    cudaError_t _e = cudaGetLastError();                                               \
-    if (_e != cudaSuccess) return fail(h, SFB_E_CUDA, std::string("launch: ") + cudaGetErrorString(_e)); \
-  } while (0)
-
-size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 
 // Stable compaction of flagged elements (cub::DeviceSelect::Flagged).
 template <class T>
@@ -1034,592 +792,6 @@ int sfb_frames_release(sfb_ctx* c, int32_t n, const int32_t* slots) {
     }
     sl.block = nullptr;
   }
-  return SFB_OK;
-}
-
-// Page-locked host staging (reused by the host runtime across calls).
-int sfb_host_alloc(int64_t bytes, void** ptr) {
-  if (!ptr || bytes < 0) return fail(nullptr, SFB_E_ARG, "bad arguments");
-  cudaError_t e = cudaMallocHost(ptr, (size_t)std::max<int64_t>(bytes, 1));
-  if (e != cudaSuccess) return fail(nullptr, SFB_E_OOM, cudaGetErrorString(e));
-  return SFB_OK;
-}
-int sfb_host_free(void* ptr) {
-  if (ptr) cudaFreeHost(ptr);
-  return SFB_OK;
-}
-
-int sfb_frames_set_intensity(sfb_ctx* c, int32_t n, const int32_t* slots,
-                             const float* const* intensity) {
-  if (!c || n < 0 || (n > 0 && (!slots || !intensity))) return fail(c, SFB_E_ARG, "bad arguments");
-  CK(c, cudaSetDevice(c->device));
-  for (int k = 0; k < n; ++k) {
-    const int s = slots[k];
-    if (s < 0 || s >= (int)c->slots.size() || !c->slots[s].alive)
-      return fail(c, SFB_E_ARG, "slot " + std::to_string(s) + " is not resident");
-    if (!intensity[k]) return fail(c, SFB_E_ARG, "null intensity plane");
-    Slot& sl = c->slots[s];
-    const size_t bytes = (size_t)sl.dev.w * sl.dev.h * sizeof(float);
-    if (!sl.intensity) {
-      void* p = nullptr;
-      CK(c, dev_cache().alloc(&p, bytes));
-      sl.intensity = static_cast<float*>(p);
-      sl.intensity_bytes = bytes;
-    }
-    CK(c, cudaMemcpyAsync(sl.intensity, intensity[k], bytes, cudaMemcpyHostToDevice, c->stream));
-    sl.dev.I = sl.intensity;
-  }
-  CK(c, cudaStreamSynchronize(c->stream));  // host planes are borrowed for the call only
-  return SFB_OK;
-}
-
-int sfb_dense_verify(sfb_ctx* c, int32_t n_items, const int32_t* src_slots,
-                     const int32_t* dst_slots, const double* R9, const double* t3,
-                     const uint8_t* flags, const sfb_verify_config* cfg,
-                     double* err_out, int64_t* count_out) {
-  if (!c || n_items < 0 || !cfg) return fail(c, SFB_E_ARG, "bad arguments");
-  if (n_items == 0) return SFB_OK;
-  if (!src_slots || !dst_slots || !R9 || !t3 || !flags || !err_out || !count_out)
-    return fail(c, SFB_E_ARG, "null argument");
-  for (int32_t o : {cfg->apply_n, cfg->apply_1, cfg->apply_nf, cfg->apply_1f})
-    if (o < 0 || o > 5) return fail(c, SFB_E_ARG, "rounding code out of range");
-  CK(c, cudaSetDevice(c->device));
-  std::vector<VerifyItem> items(n_items);
-  int max_hw = 1;
-  for (int k = 0; k < n_items; ++k) {
-    const int ss = src_slots[k], ds = dst_slots[k];
-    for (int s : {ss, ds}) {
-      if (s < 0 || s >= (int)c->slots.size() || !c->slots[s].alive)
-        return fail(c, SFB_E_ARG, "slot " + std::to_string(s) + " is not resident");
-      if (!c->slots[s].intensity)
-        return fail(c, SFB_E_ARG, "slot " + std::to_string(s) + " has no intensity plane");
-    }
-    VerifyItem& it = items[k];
-    it.src = c->slots[ss].dev;
-    it.dst = c->slots[ds].dev;
-    const bool inv = flags[k] & 1, f_ord = flags[k] & 2;
-    const double* R = R9 + 9 * (size_t)k;
-    const double* t = t3 + 3 * (size_t)k;
-    if (inv) {
-      // RigidTransform.inverse (geometry.py:135-137): R.T.copy() (C-ordered)
-      // and -(R.T) @ t with NumPy's gemv order for R.T's memory layout
-      const int mv = f_ord ? c->rd.mv_c : c->rd.mv_f;
-      for (int r = 0; r < 3; ++r)
-        for (int q = 0; q < 3; ++q) it.R[r * 3 + q] = R[q * 3 + r];
-      for (int r = 0; r < 3; ++r)
-        it.t[r] = -host_dot3o(it.R[r * 3 + 0], it.R[r * 3 + 1], it.R[r * 3 + 2], t[0], t[1], t[2], mv);
-      it.ord_n = cfg->apply_n;
-      it.ord_1 = cfg->apply_1;
-    } else {
-      for (int q = 0; q < 9; ++q) it.R[q] = R[q];
-      for (int q = 0; q < 3; ++q) it.t[q] = t[q];
-      it.ord_n = f_ord ? cfg->apply_nf : cfg->apply_n;
-      it.ord_1 = f_ord ? cfg->apply_1f : cfg->apply_1;
-    }
-    max_hw = std::max(max_hw, it.src.w * it.src.h);
-  }
-  if (max_hw > verify_max_pixels())
-    return fail(c, SFB_E_ARG, "dense_verify supports frames of at most " +
-                                  std::to_string(verify_max_pixels()) + " pixels");
-  CK(c, c->verify_items.ensure(n_items));
-  CK(c, c->verify_err.ensure(n_items));
-  CK(c, c->verify_cnt.ensure(n_items));
-  CK(c, cudaMemcpyAsync(c->verify_items.p, items.data(), sizeof(VerifyItem) * n_items,
-                        cudaMemcpyHostToDevice, c->stream));
-  const VerifyCfg vc{cfg->depth_max, cfg->normal_min, cfg->color_max};
-  CK(c, launch_dense_verify(c->verify_items.p, n_items, max_hw, vc, c->verify_err.p,
-                            c->verify_cnt.p, c->stream));
-  CK(c, cudaMemcpyAsync(err_out, c->verify_err.p, sizeof(double) * n_items, cudaMemcpyDeviceToHost,
-                        c->stream));
-  std::vector<long long> cnt(n_items);
-  CK(c, cudaMemcpyAsync(cnt.data(), c->verify_cnt.p, sizeof(long long) * n_items,
-                        cudaMemcpyDeviceToHost, c->stream));
-  CK(c, cudaStreamSynchronize(c->stream));
-  for (int k = 0; k < n_items; ++k) count_out[k] = cnt[k];
-  return SFB_OK;
-}
-
-int sfb_build_cache(sfb_ctx* c, int32_t n, int32_t width, int32_t height, int32_t low_width,
-                    int32_t low_height, const uint8_t* const* colors, const float* const* depths,
-                    const double* k_low, int32_t luma_order, void* host_out, int32_t* slots_out) {
-  if (!c || n < 0 || (n > 0 && (!colors || !depths || !k_low || !host_out || !slots_out)))
-    return fail(c, SFB_E_ARG, "bad arguments");
-  if (n == 0) return SFB_OK;
-  if (low_width < 2 || low_height < 2 || width % low_width || height % low_height)
-    return fail(c, SFB_E_ARG, "frame does not divide into low_width x low_height blocks");
-  if (luma_order < 0 || luma_order > 5) return fail(c, SFB_E_ARG, "rounding code out of range");
-  const int bw = width / low_width, bh = height / low_height;
-  if (bw * bh > 64) return fail(c, SFB_E_ARG, "blocks of more than 64 samples are not supported");
-  CK(c, cudaSetDevice(c->device));
-  cudaStream_t s = c->stream;
-  const size_t HW = (size_t)width * height, hw = (size_t)low_width * low_height;
-  const size_t raw_b = align256(HW * 3) + align256(HW * 4), out_b = 42 * hw;
-  CK(c, c->cache_raw.ensure(raw_b * n, s));
-  CK(c, c->cache_out.ensure(align256(out_b) * n, s));
-  CK(c, c->cache_frames.ensure(n, s));
-  std::vector<CacheFrame> fr(n);
-  for (int k = 0; k < n; ++k) {
-    uint8_t* raw = c->cache_raw.p + raw_b * k;
-    const void* src[2] = {colors[k], depths[k]};
-    void* dst[2] = {raw, raw + align256(HW * 3)};
-    const size_t sz[2] = {HW * 3, HW * 4};
-    const void* use[2];
-    for (int q = 0; q < 2; ++q) {
-      if (!src[q]) return fail(c, SFB_E_ARG, "null frame plane");
-      cudaPointerAttributes at{};
-      if (cudaPointerGetAttributes(&at, src[q]) == cudaSuccess &&
-          ((at.type == cudaMemoryTypeHost && at.devicePointer != nullptr) ||
-           (at.type == cudaMemoryTypeDevice && at.device == c->device))) {
-        use[q] = at.devicePointer;  // pinned (zero-copy) or device-resident input
-        continue;
-      }
-      cudaGetLastError();
-      CK(c, cudaMemcpyAsync(dst[q], src[q], sz[q], cudaMemcpyHostToDevice, s));
-      use[q] = dst[q];
-    }
-    uint8_t* o = c->cache_out.p + align256(out_b) * k;
-    CacheFrame& f = fr[k];
-    f.color = static_cast<const uint8_t*>(use[0]);
-    f.depth_in = static_cast<const float*>(use[1]);
-    f.intensity = reinterpret_cast<float*>(o);
-    f.depth = reinterpret_cast<float*>(o + 4 * hw);
-    f.points = reinterpret_cast<float*>(o + 8 * hw);
-    f.normals = reinterpret_cast<float*>(o + 20 * hw);
-    f.grad = reinterpret_cast<float*>(o + 32 * hw);
-    f.valid = o + 40 * hw;
-    f.valid_n = o + 41 * hw;
-  }
-  CK(c, cudaMemcpyAsync(c->cache_frames.p, fr.data(), sizeof(CacheFrame) * n, cudaMemcpyHostToDevice, s));
-  CacheArgs ca{c->cache_frames.p, width, height, low_width, low_height, bw, bh,
-               k_low[0], k_low[1], k_low[2], k_low[3], luma_order};
-  CK(c, launch_build_cache(ca, n, s));
-  // the planes become resident frame slots (read in place by the pack kernel)
-  std::vector<sfb_frame_desc> d(n);
-  for (int k = 0; k < n; ++k) {
-    d[k].width = low_width;
-    d[k].height = low_height;
-    d[k].fx = k_low[0];
-    d[k].fy = k_low[1];
-    d[k].cx = k_low[2];
-    d[k].cy = k_low[3];
-    d[k].valid_depth = fr[k].valid;
-    d[k].valid_normal = fr[k].valid_n;
-    d[k].points = fr[k].points;
-    d[k].normals = fr[k].normals;
-    d[k].grad = fr[k].grad;
-  }
-  int rc = sfb_frames_upload(c, n, d.data(), slots_out);
-  if (rc) return rc;
-  // intensity_low for dense_verify, then the host image of every plane
-  for (int k = 0; k < n; ++k) {
-    Slot& sl = c->slots[slots_out[k]];
-    if (!sl.intensity) {
-      void* p = nullptr;
-      CK(c, dev_cache().alloc(&p, hw * sizeof(float)));
-      sl.intensity = static_cast<float*>(p);
-      sl.intensity_bytes = hw * sizeof(float);
-    }
-    CK(c, cudaMemcpyAsync(sl.intensity, fr[k].intensity, hw * sizeof(float), cudaMemcpyDeviceToDevice, s));
-    sl.dev.I = sl.intensity;
-    CK(c, cudaMemcpyAsync(static_cast<uint8_t*>(host_out) + out_b * k, fr[k].intensity, out_b,
-                          cudaMemcpyDeviceToHost, s));
-  }
-  CK(c, cudaStreamSynchronize(s));
-  return SFB_OK;
-}
-
-// ---- hashed TSDF volume (tsdf.py:55-267) ---------------------------------
-}  // extern "C"
-
-struct sfb_tsdf : Handle {
-  sfb_ctx* ctx = nullptr;
-  double vs = 0.004, trunc = 0.02, extent = 0.032;
-  int dw = 0;
-  // block dictionary: key -> pool slot, insertion order with tombstones
-  std::unordered_map<long long, int> map;
-  std::vector<long long> order;
-  std::unordered_map<long long, size_t> pos;
-  size_t dead = 0;
-  std::vector<int> free_slots;
-  int cap = 0, used = 0;
-  float *weight = nullptr, *wdist = nullptr, *wcolor = nullptr;
-  DBuf<long long> keys, tmp;
-  DBuf<uint8_t> temp, color;
-  DBuf<int> cnt, slots, aux;
-  DBuf<unsigned char> hit, flags;
-  DBuf<double> tvals;
-  DBuf<float> depth, pack;
-};
-
-namespace {
-
-long long tsdf_decode(long long key, int k) {
-  const long long m = (1LL << 21) - 1, S = 1LL << 20;
-  return (k == 0 ? ((key >> 42) & m) : k == 1 ? ((key >> 21) & m) : (key & m)) - S;
-}
-
-long long tsdf_encode(const int64_t* c) {
-  const long long S = 1LL << 20;
-  return (long long)((((unsigned long long)(c[0] + S)) << 42) |
-                     (((unsigned long long)(c[1] + S)) << 21) | ((unsigned long long)(c[2] + S)));
-}
-
-int tsdf_grow(sfb_tsdf* t, int need) {
-  if (need <= t->cap) return SFB_OK;
-  int nc = std::max(need, std::max(1024, 2 * t->cap));
-  float *w = nullptr, *d = nullptr, *c = nullptr;
-  if (cudaMalloc(&w, sizeof(float) * 512 * (size_t)nc) != cudaSuccess ||
-      cudaMalloc(&d, sizeof(float) * 512 * (size_t)nc) != cudaSuccess ||
-      cudaMalloc(&c, sizeof(float) * 1536 * (size_t)nc) != cudaSuccess) {
-    cudaFree(w);
-    cudaFree(d);
-    cudaFree(c);
-    return fail(t, SFB_E_OOM, "TSDF block pool");
-  }
-  cudaStream_t s = t->ctx->stream;
-  CK(t, cudaMemsetAsync(w, 0, sizeof(float) * 512 * (size_t)nc, s));
-  CK(t, cudaMemsetAsync(d, 0, sizeof(float) * 512 * (size_t)nc, s));
-  CK(t, cudaMemsetAsync(c, 0, sizeof(float) * 1536 * (size_t)nc, s));
-  if (t->cap > 0) {
-    CK(t, cudaMemcpyAsync(w, t->weight, sizeof(float) * 512 * (size_t)t->cap, cudaMemcpyDeviceToDevice, s));
-    CK(t, cudaMemcpyAsync(d, t->wdist, sizeof(float) * 512 * (size_t)t->cap, cudaMemcpyDeviceToDevice, s));
-    CK(t, cudaMemcpyAsync(c, t->wcolor, sizeof(float) * 1536 * (size_t)t->cap, cudaMemcpyDeviceToDevice, s));
-    CK(t, cudaStreamSynchronize(s));
-    cudaFree(t->weight);
-    cudaFree(t->wdist);
-    cudaFree(t->wcolor);
-  }
-  t->weight = w;
-  t->wdist = d;
-  t->wcolor = c;
-  t->cap = nc;
-  return SFB_OK;
-}
-
-int tsdf_new_slot(sfb_tsdf* t, long long key) {
-  int sl;
-  if (!t->free_slots.empty()) {
-    sl = t->free_slots.back();
-    t->free_slots.pop_back();
-  } else {
-    sl = t->used++;
-  }
-  t->map[key] = sl;
-  t->pos[key] = t->order.size();
-  t->order.push_back(key);
-  return sl;
-}
-
-void tsdf_drop(sfb_tsdf* t, long long key, std::vector<int>& freed) {
-  auto it = t->map.find(key);
-  if (it == t->map.end()) return;
-  freed.push_back(it->second);
-  t->free_slots.push_back(it->second);
-  t->map.erase(it);
-  auto p = t->pos.find(key);
-  t->order[p->second] = LLONG_MIN;  // tombstone
-  t->pos.erase(p);
-  if (++t->dead > 1024 && t->dead * 2 > t->order.size()) {  // compact
-    std::vector<long long> o;
-    o.reserve(t->map.size());
-    for (long long k : t->order)
-      if (k != LLONG_MIN) {
-        t->pos[k] = o.size();
-        o.push_back(k);
-      }
-    t->order.swap(o);
-    t->dead = 0;
-  }
-}
-
-int tsdf_zero_slots(sfb_tsdf* t, const std::vector<int>& sl) {
-  if (sl.empty()) return SFB_OK;
-  cudaStream_t s = t->ctx->stream;
-  CK(t, t->aux.ensure(sl.size(), s));
-  CK(t, cudaMemcpyAsync(t->aux.p, sl.data(), sizeof(int) * sl.size(), cudaMemcpyHostToDevice, s));
-  CK(t, launch_tsdf_zero(t->aux.p, (int)sl.size(), t->weight, t->wdist, t->wcolor, s));
-  CK(t, cudaStreamSynchronize(s));
-  return SFB_OK;
-}
-
-}  // namespace
-
-extern "C" {
-
-int sfb_tsdf_create(sfb_ctx* c, double voxel_size, double truncation, int32_t depth_weighting,
-                    sfb_tsdf** out) {
-  if (!c || !out || !(voxel_size > 0.0) || !(truncation > 0.0))
-    return fail(c, SFB_E_ARG, "bad arguments");
-  sfb_tsdf* t = new sfb_tsdf();
-  t->ctx = c;
-  t->vs = voxel_size;
-  t->trunc = truncation;
-  t->extent = voxel_size * 8;  // TsdfVolume.block_extent (tsdf.py:83-85)
-  t->dw = depth_weighting ? 1 : 0;
-  *out = t;
-  return SFB_OK;
-}
-
-int sfb_tsdf_destroy(sfb_tsdf* t) {
-  if (!t) return SFB_OK;
-  cudaSetDevice(t->ctx->device);
-  cudaStreamSynchronize(t->ctx->stream);
-  cudaFree(t->weight);
-  cudaFree(t->wdist);
-  cudaFree(t->wcolor);
-  DBuf<long long>* kb[] = {&t->keys, &t->tmp};
-  for (auto* b : kb) b->release();
-  t->temp.release();
-  t->color.release();
-  t->cnt.release();
-  t->slots.release();
-  t->aux.release();
-  t->hit.release();
-  t->flags.release();
-  t->tvals.release();
-  t->depth.release();
-  t->pack.release();
-  delete t;
-  return SFB_OK;
-}
-
-int sfb_tsdf_apply(sfb_tsdf* t, int32_t sign, int32_t width, int32_t height, const uint8_t* color,
-                   const float* depth, const double* k4, const double* pose_R, const double* pose_t,
-                   int32_t pose_ord, const double* inv_R, const double* inv_t, int32_t inv_ord,
-                   const double* tvals, int32_t n_samples, int32_t* status, int64_t* err_coord) {
-  if (!t || !color || !depth || !k4 || !pose_R || !pose_t || !inv_R || !inv_t || !tvals || !status ||
-      !err_coord || width < 1 || height < 1 || n_samples < 1 || (sign != 1 && sign != -1))
-    return fail(t, SFB_E_ARG, "bad arguments");
-  if (pose_ord < 0 || pose_ord > 5 || inv_ord < 0 || inv_ord > 5)
-    return fail(t, SFB_E_ARG, "rounding code out of range");
-  *status = 0;
-  CK(t, cudaSetDevice(t->ctx->device));
-  cudaStream_t s = t->ctx->stream;
-  const size_t hw = (size_t)width * height;
-  CK(t, t->depth.ensure(hw, s));
-  CK(t, t->color.ensure(hw * 3, s));
-  CK(t, t->tvals.ensure(n_samples, s));
-  CK(t, cudaMemcpyAsync(t->depth.p, depth, sizeof(float) * hw, cudaMemcpyHostToDevice, s));
-  CK(t, cudaMemcpyAsync(t->color.p, color, hw * 3, cudaMemcpyHostToDevice, s));
-  CK(t, cudaMemcpyAsync(t->tvals.p, tvals, sizeof(double) * n_samples, cudaMemcpyHostToDevice, s));
-  // touched blocks: ray samples -> keys -> sorted unique (np.unique)
-  const size_t nk = hw * n_samples;
-  if (nk > (size_t)INT32_MAX) return fail(t, SFB_E_ARG, "frame too large");
-  CK(t, t->keys.ensure(nk, s));
-  CK(t, t->tmp.ensure(nk, s));
-  CK(t, t->cnt.ensure(1, s));
-  TsdfTouchArgs ta{};
-  ta.depth = t->depth.p;
-  ta.W = width;
-  ta.H = height;
-  ta.fx = k4[0]; ta.fy = k4[1]; ta.cx = k4[2]; ta.cy = k4[3];
-  for (int q = 0; q < 9; ++q) ta.pose.R[q] = pose_R[q];
-  for (int q = 0; q < 3; ++q) ta.pose.t[q] = pose_t[q];
-  ta.ord = pose_ord;
-  ta.trunc = t->trunc;
-  ta.extent = t->extent;
-  ta.t = t->tvals.p;
-  ta.n_samples = n_samples;
-  ta.keys = t->keys.p;
-  CK(t, launch_tsdf_touch(ta, s));
-  size_t tb = 0;
-  CK(t, tsdf_sort_unique(t->keys.p, t->tmp.p, (int)nk, nullptr, &tb, t->cnt.p, s));
-  CK(t, t->temp.ensure(std::max<size_t>(tb, 1), s));
-  CK(t, tsdf_sort_unique(t->keys.p, t->tmp.p, (int)nk, t->temp.p, &tb, t->cnt.p, s));
-  int nu = 0;
-  CK(t, cudaMemcpyAsync(&nu, t->cnt.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-  CK(t, cudaStreamSynchronize(s));
-  std::vector<long long> keys(nu);
-  if (nu > 0)
-    CK(t, cudaMemcpyAsync(keys.data(), t->keys.p, sizeof(long long) * nu, cudaMemcpyDeviceToHost, s));
-  CK(t, cudaStreamSynchronize(s));
-  int n = nu;
-  if (n > 0 && keys[n - 1] == LLONG_MAX) --n;  // invalid pixels' sentinel
-  if (n == 0) {
-    if (sign < 0) *status = 1;  // "frame has no integrated content"
-    return SFB_OK;
-  }
-  // EVAL: which touched blocks receive a hit
-  TsdfVoxelArgs va{};
-  va.keys = t->keys.p;
-  va.extent = t->extent;
-  va.vs = t->vs;
-  va.trunc = t->trunc;
-  for (int q = 0; q < 9; ++q) va.inv_pose.R[q] = inv_R[q];
-  for (int q = 0; q < 3; ++q) va.inv_pose.t[q] = inv_t[q];
-  va.ord = inv_ord;
-  va.fx = k4[0]; va.fy = k4[1]; va.cx = k4[2]; va.cy = k4[3];
-  va.W = width;
-  va.H = height;
-  va.depth = t->depth.p;
-  va.color = t->color.p;
-  va.depth_weighting = t->dw;
-  va.sign = (float)sign;
-  va.snap_end = n;
-  CK(t, t->hit.ensure(n, s));
-  CK(t, t->flags.ensure(n, s));
-  CK(t, t->slots.ensure(n, s));
-  va.flags = t->hit.p;
-  va.slots = nullptr;
-  CK(t, launch_tsdf_voxels(va, 0, n, s));
-  std::vector<unsigned char> hit(n);
-  CK(t, cudaMemcpyAsync(hit.data(), t->hit.p, n, cudaMemcpyDeviceToHost, s));
-  CK(t, cudaStreamSynchronize(s));
-  // the reference's block loop, in touched (sorted key) order (tsdf.py:130-156)
-  std::vector<int> slot(n, -1);
-  int limit = n;
-  if (sign > 0) {
-    int need = t->used;
-    for (int b = 0; b < n; ++b)
-      if (hit[b] && !t->map.count(keys[b])) ++need;
-    int rc = tsdf_grow(t, need);
-    if (rc) return rc;
-    for (int b = 0; b < n; ++b) {
-      if (!hit[b]) continue;
-      auto it = t->map.find(keys[b]);
-      slot[b] = it != t->map.end() ? it->second : tsdf_new_slot(t, keys[b]);
-    }
-  } else {
-    for (int b = 0; b < n; ++b) {
-      auto it = t->map.find(keys[b]);
-      if (hit[b] && it == t->map.end()) {  // "block ... missing during de-integration"
-        limit = b;
-        *status = 2;
-        for (int k = 0; k < 3; ++k) err_coord[k] = tsdf_decode(keys[b], k);
-        break;
-      }
-      slot[b] = it != t->map.end() ? it->second : -1;
-    }
-  }
-  CK(t, cudaMemcpyAsync(t->slots.p, slot.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s));
-  va.slots = t->slots.p;
-  va.hit = t->hit.p;
-  va.weight = t->weight;  // (the pool may have grown above)
-  va.wdist = t->wdist;
-  va.wcolor = t->wcolor;
-  int k2 = -1;
-  if (sign < 0 && limit > 0) {  // CHECK: the first block whose weight would go negative
-    va.flags = t->flags.p;
-    CK(t, launch_tsdf_voxels(va, 1, limit, s));
-    std::vector<unsigned char> neg(limit);
-    CK(t, cudaMemcpyAsync(neg.data(), t->flags.p, limit, cudaMemcpyDeviceToHost, s));
-    CK(t, cudaStreamSynchronize(s));
-    for (int b = 0; b < limit; ++b)
-      if (slot[b] >= 0 && hit[b] && neg[b]) {
-        k2 = b;
-        break;
-      }
-    if (k2 >= 0) {
-      limit = k2 + 1;     // that block's update lands, then the error (tsdf.py:146-150)
-      va.snap_end = k2;   // ... before its snap / clear / drop
-      *status = 3;
-      for (int k = 0; k < 3; ++k) err_coord[k] = tsdf_decode(keys[k2], k);
-    }
-  }
-  if (limit > 0) {  // COMMIT
-    va.flags = t->flags.p;
-    CK(t, launch_tsdf_voxels(va, 2, limit, s));
-  }
-  if (sign < 0 && limit > 0) {  // drop blocks left empty (tsdf.py:156-160)
-    std::vector<unsigned char> empty(limit);
-    CK(t, cudaMemcpyAsync(empty.data(), t->flags.p, limit, cudaMemcpyDeviceToHost, s));
-    CK(t, cudaStreamSynchronize(s));
-    std::vector<int> freed;
-    for (int b = 0; b < limit; ++b)
-      if (slot[b] >= 0 && empty[b] && b != k2) tsdf_drop(t, keys[b], freed);
-    int rc = tsdf_zero_slots(t, freed);
-    if (rc) return rc;
-  }
-  CK(t, cudaStreamSynchronize(s));
-  return SFB_OK;
-}
-
-int sfb_tsdf_count(sfb_tsdf* t, int64_t* n_blocks) {
-  if (!t || !n_blocks) return fail(t, SFB_E_ARG, "null argument");
-  *n_blocks = (int64_t)t->map.size();
-  return SFB_OK;
-}
-
-// Blocks in insertion order (the reference's dict order): coords (n, 3) and
-// weight (n, 512), wdist (n, 512), wcolor (n, 512, 3); any output may be NULL.
-int sfb_tsdf_export(sfb_tsdf* t, int64_t n, int64_t* coords, float* weight, float* wdist,
-                    float* wcolor) {
-  if (!t || n != (int64_t)t->map.size()) return fail(t, SFB_E_ARG, "n must equal the block count");
-  CK(t, cudaSetDevice(t->ctx->device));
-  cudaStream_t s = t->ctx->stream;
-  std::vector<int> sl;
-  sl.reserve(n);
-  int64_t k = 0;
-  for (long long key : t->order) {
-    if (key == LLONG_MIN) continue;
-    if (coords)
-      for (int q = 0; q < 3; ++q) coords[3 * k + q] = tsdf_decode(key, q);
-    sl.push_back(t->map[key]);
-    ++k;
-  }
-  if (n == 0 || (!weight && !wdist && !wcolor)) return SFB_OK;
-  CK(t, t->aux.ensure(n, s));
-  CK(t, t->pack.ensure((size_t)n * 2560, s));
-  CK(t, cudaMemcpyAsync(t->aux.p, sl.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s));
-  float* pw = t->pack.p;
-  float* pd = pw + (size_t)n * 512;
-  float* pc = pd + (size_t)n * 512;
-  CK(t, launch_tsdf_copy(t->aux.p, (int)n, 0, t->weight, t->wdist, t->wcolor, pw, pd, pc, s));
-  if (weight) CK(t, cudaMemcpyAsync(weight, pw, sizeof(float) * 512 * n, cudaMemcpyDeviceToHost, s));
-  if (wdist) CK(t, cudaMemcpyAsync(wdist, pd, sizeof(float) * 512 * n, cudaMemcpyDeviceToHost, s));
-  if (wcolor) CK(t, cudaMemcpyAsync(wcolor, pc, sizeof(float) * 1536 * n, cudaMemcpyDeviceToHost, s));
-  CK(t, cudaStreamSynchronize(s));
-  return SFB_OK;
-}
-
-// Insert (or overwrite) blocks with the given accumulators; new keys append
-// to the insertion order (TsdfVolume.allocate / load_volume, tsdf.py:75-81,260-267).
-int sfb_tsdf_import(sfb_tsdf* t, int64_t n, const int64_t* coords, const float* weight,
-                    const float* wdist, const float* wcolor) {
-  if (!t || n < 0 || (n > 0 && (!coords || !weight || !wdist || !wcolor)))
-    return fail(t, SFB_E_ARG, "bad arguments");
-  if (n == 0) return SFB_OK;
-  CK(t, cudaSetDevice(t->ctx->device));
-  cudaStream_t s = t->ctx->stream;
-  int need = t->used;
-  for (int64_t b = 0; b < n; ++b)
-    if (!t->map.count(tsdf_encode(coords + 3 * b))) ++need;
-  int rc = tsdf_grow(t, need);
-  if (rc) return rc;
-  std::vector<int> sl(n);
-  for (int64_t b = 0; b < n; ++b) {
-    const long long key = tsdf_encode(coords + 3 * b);
-    auto it = t->map.find(key);
-    sl[b] = it != t->map.end() ? it->second : tsdf_new_slot(t, key);
-  }
-  CK(t, t->aux.ensure(n, s));
-  CK(t, t->pack.ensure((size_t)n * 2560, s));
-  float* pw = t->pack.p;
-  float* pd = pw + (size_t)n * 512;
-  float* pc = pd + (size_t)n * 512;
-  CK(t, cudaMemcpyAsync(t->aux.p, sl.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s));
-  CK(t, cudaMemcpyAsync(pw, weight, sizeof(float) * 512 * n, cudaMemcpyHostToDevice, s));
-  CK(t, cudaMemcpyAsync(pd, wdist, sizeof(float) * 512 * n, cudaMemcpyHostToDevice, s));
-  CK(t, cudaMemcpyAsync(pc, wcolor, sizeof(float) * 1536 * n, cudaMemcpyHostToDevice, s));
-  CK(t, launch_tsdf_copy(t->aux.p, (int)n, 1, t->weight, t->wdist, t->wcolor, pw, pd, pc, s));
-  CK(t, cudaStreamSynchronize(s));
-  return SFB_OK;
-}
-
-// One block's accumulators (found = 0 when absent): TsdfVolume.block / voxel_state.
-int sfb_tsdf_get_block(sfb_tsdf* t, const int64_t* coord, int32_t* found, float* weight,
-                       float* wdist, float* wcolor) {
-  if (!t || !coord || !found) return fail(t, SFB_E_ARG, "null argument");
-  auto it = t->map.find(tsdf_encode(coord));
-  *found = it != t->map.end() ? 1 : 0;
-  if (!*found) return SFB_OK;
-  CK(t, cudaSetDevice(t->ctx->device));
-  cudaStream_t s = t->ctx->stream;
-  const size_t sl = it->second;
-  if (weight) CK(t, cudaMemcpyAsync(weight, t->weight + sl * 512, 2048, cudaMemcpyDeviceToHost, s));
-  if (wdist) CK(t, cudaMemcpyAsync(wdist, t->wdist + sl * 512, 2048, cudaMemcpyDeviceToHost, s));
-  if (wcolor) CK(t, cudaMemcpyAsync(wcolor, t->wcolor + sl * 1536, 6144, cudaMemcpyDeviceToHost, s));
-  CK(t, cudaStreamSynchronize(s));
   return SFB_OK;
 }
 
