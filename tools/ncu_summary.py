@@ -36,6 +36,29 @@ def _csv(args):
     return list(csv.reader(io.StringIO(out)))
 
 
+def _stall_lines(rep, top=12):
+    """Warp-stall samples per CUDA source line (needs -lineinfo), top lines."""
+    rows = _csv([rep, "--page", "source", "--csv", "--print-source", "cuda,sass"])
+    agg, fname, tot = collections.Counter(), "", 0
+    text = {}
+    for r in rows:
+        if r and r[0] in ("File Path", "File Name"):
+            fname = r[1].split("/")[-1]
+            continue
+        if len(r) < 6 or not r[0] or r[0] == "Line No":
+            continue
+        try:
+            v = int(r[4])
+        except ValueError:
+            continue
+        key = f"{fname}:{r[0]}"
+        agg[key] += v
+        text[key] = r[1].strip()[:80]
+        tot += v
+    tot = tot or 1
+    return [{"line": k, "pct": round(100 * v / tot, 1), "source": text[k]} for k, v in agg.most_common(top)]
+
+
 def main():
     rep, dst = sys.argv[1], sys.argv[2]
     label = sys.argv[sys.argv.index("--label") + 1] if "--label" in sys.argv else ""
@@ -83,6 +106,7 @@ def main():
     st = sum(stalls.values()) or 1.0
     res["stall_pct"] = {k: round(100 * v / st, 1) for k, v in stalls.most_common(8)}
     res["inst_mix_pct"] = {k: round(100 * v / tot, 1) for k, v in mix.most_common(10)}
+    res["stall_lines_pct"] = _stall_lines(rep)
     with open(dst, "w") as f:
         json.dump(res, f, indent=1)
     print(json.dumps(res, indent=1))
