@@ -264,7 +264,128 @@ done:
   return res;
 }
 
+/* ---- poses (solver._push_poses / _pull_poses) ---------------------------- */
+static PyObject *s_rotation, *s_translation;
+
+/* float64 ndarray of `n` elements in any layout -> out (C order) */
+static int copy_f64(PyObject* o, int nd, const npy_intp* dims, double* out) {
+  if (!PyArray_Check(o)) return 0;
+  PyArrayObject* a = (PyArrayObject*)o;
+  if (PyArray_TYPE(a) != NPY_DOUBLE || !PyArray_ISNOTSWAPPED(a)) return 0;
+  if (nd == 2) {
+    if (PyArray_NDIM(a) != 2 || PyArray_DIM(a, 0) != dims[0] || PyArray_DIM(a, 1) != dims[1]) return 0;
+    for (npy_intp r = 0; r < dims[0]; ++r)
+      for (npy_intp c = 0; c < dims[1]; ++c) memcpy(out++, PyArray_GETPTR2(a, r, c), 8);
+    return 1;
+  }
+  /* translation: any shape holding dims[0] elements (np.reshape(3)) */
+  if (PyArray_SIZE(a) != dims[0]) return 0;
+  if (PyArray_NDIM(a) == 1) {
+    for (npy_intp k = 0; k < dims[0]; ++k) memcpy(out++, PyArray_GETPTR1(a, k), 8);
+    return 1;
+  }
+  if (!PyArray_ISCARRAY_RO(a)) return 0;
+  memcpy(out, PyArray_DATA(a), 8 * (size_t)dims[0]);
+  return 1;
+}
+
+static int out_array(PyObject* o, int typenum, npy_intp n, char** data) {
+  if (!PyArray_Check(o)) return 0;
+  PyArrayObject* a = (PyArrayObject*)o;
+  if (PyArray_TYPE(a) != typenum || !PyArray_ISCARRAY(a) || PyArray_SIZE(a) != n) return 0;
+  *data = (char*)PyArray_DATA(a);
+  return 1;
+}
+
+/* pack_poses(poses, R, t, fl) -> True | None.  R (n,3,3), t (n,3) float64 and
+ * fl (n,) uint8 C arrays; fl[k] = rotation F-ordered (not C), the BLAS
+ * operand-order flag of device_problem._pose_arrays.  None: an entry is not a
+ * float64 ndarray pair (the caller takes the NumPy path). */
+static PyObject* pack_poses(PyObject* self, PyObject* args) {
+  PyObject *poses, *Ro, *to, *flo;
+  if (!PyArg_ParseTuple(args, "OOOO", &poses, &Ro, &to, &flo)) return NULL;
+  PyObject* seq = PySequence_Fast(poses, "poses must be a sequence");
+  if (!seq) return NULL;
+  const Py_ssize_t n = PySequence_Fast_GET_SIZE(seq);
+  char *R, *t, *fl;
+  PyObject* res = NULL;
+  if (!out_array(Ro, NPY_DOUBLE, 9 * n, &R) || !out_array(to, NPY_DOUBLE, 3 * n, &t) ||
+      !out_array(flo, NPY_UINT8, n, &fl)) {
+    PyErr_SetString(PyExc_ValueError, "pack_poses: bad output arrays");
+    goto done;
+  }
+  static const npy_intp d33[2] = {3, 3}, d3[1] = {3};
+  for (Py_ssize_t k = 0; k < n; ++k) {
+    PyObject* p = PySequence_Fast_GET_ITEM(seq, k);
+    PyObject* rot = PyObject_GetAttr(p, s_rotation);
+    if (!rot) goto done;
+    PyObject* tr = PyObject_GetAttr(p, s_translation);
+    if (!tr) {
+      Py_DECREF(rot);
+      goto done;
+    }
+    const int ok = copy_f64(rot, 2, d33, (double*)R + 9 * k) && copy_f64(tr, 1, d3, (double*)t + 3 * k);
+    if (ok) {
+      PyArrayObject* a = (PyArrayObject*)rot;
+      fl[k] = (PyArray_IS_F_CONTIGUOUS(a) && !PyArray_IS_C_CONTIGUOUS(a)) ? 1 : 0;
+    }
+    Py_DECREF(rot);
+    Py_DECREF(tr);
+    if (!ok) {
+      res = Py_NewRef(Py_None);
+      goto done;
+    }
+  }
+  res = Py_NewRef(Py_True);
+done:
+  Py_DECREF(seq);
+  return res;
+}
+
+/* make_poses(poses, frame_ids, R, t, cls, first) -> None: for k >= first,
+ * poses[frame_ids[k]] = cls(R[k].copy(), t[k].copy()). */
+static PyObject* make_poses(PyObject* self, PyObject* args) {
+  PyObject *poses, *ids, *Ro, *to, *cls;
+  Py_ssize_t first;
+  if (!PyArg_ParseTuple(args, "O!OOOOn", &PyDict_Type, &poses, &ids, &Ro, &to, &cls, &first))
+    return NULL;
+  PyObject* seq = PySequence_Fast(ids, "frame_ids must be a sequence");
+  if (!seq) return NULL;
+  const Py_ssize_t n = PySequence_Fast_GET_SIZE(seq);
+  char *R, *t;
+  PyObject* res = NULL;
+  if (!out_array(Ro, NPY_DOUBLE, 9 * n, &R) || !out_array(to, NPY_DOUBLE, 3 * n, &t)) {
+    PyErr_SetString(PyExc_ValueError, "make_poses: bad input arrays");
+    goto done;
+  }
+  for (Py_ssize_t k = first; k < n; ++k) {
+    npy_intp d33[2] = {3, 3}, d3[1] = {3};
+    PyObject* rk = PyArray_SimpleNew(2, d33, NPY_DOUBLE);
+    PyObject* tk = rk ? PyArray_SimpleNew(1, d3, NPY_DOUBLE) : NULL;
+    if (!tk) {
+      Py_XDECREF(rk);
+      goto done;
+    }
+    memcpy(PyArray_DATA((PyArrayObject*)rk), R + 72 * k, 72);
+    memcpy(PyArray_DATA((PyArrayObject*)tk), t + 24 * k, 24);
+    PyObject* obj = PyObject_CallFunctionObjArgs(cls, rk, tk, NULL);
+    Py_DECREF(rk);
+    Py_DECREF(tk);
+    if (!obj) goto done;
+    const int rc = PyDict_SetItem(poses, PySequence_Fast_GET_ITEM(seq, k), obj);
+    Py_DECREF(obj);
+    if (rc) goto done;
+  }
+  res = Py_NewRef(Py_None);
+done:
+  Py_DECREF(seq);
+  return res;
+}
+
 static PyMethodDef methods[] = {
+    {"pack_poses", pack_poses, METH_VARARGS, "pack_poses(poses, R, t, fl) -> True | None"},
+    {"make_poses", make_poses, METH_VARARGS,
+     "make_poses(poses, frame_ids, R, t, cls, first) -> None"},
     {"fill_frame_descs", fill_frame_descs, METH_VARARGS,
      "fill_frame_descs(caches, descs) -> True | None"},
     {"stack_sets_into", stack_sets_into, METH_VARARGS,
@@ -281,6 +402,9 @@ PyMODINIT_FUNC PyInit__sfbhost(void) {
   s_points_i = PyUnicode_InternFromString("points_i");
   s_points_j = PyUnicode_InternFromString("points_j");
   if (!s_frame_i || !s_frame_j || !s_points_i || !s_points_j) return NULL;
+  s_rotation = PyUnicode_InternFromString("rotation");
+  s_translation = PyUnicode_InternFromString("translation");
+  if (!s_rotation || !s_translation) return NULL;
   s_vd = PyUnicode_InternFromString("valid_depth");
   s_vn = PyUnicode_InternFromString("valid_normal");
   s_pts = PyUnicode_InternFromString("points_low");

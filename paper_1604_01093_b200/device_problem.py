@@ -17,12 +17,25 @@ def _pose_arrays(poses: list):
     R = np.empty((n, 3, 3), dtype=np.float64)
     t = np.empty((n, 3), dtype=np.float64)
     fl = np.zeros(n, dtype=np.uint8)
+    host = _host_module()
+    if host is not None and host.pack_poses(poses, R, t, fl) is not None:
+        return R, t, fl
     for k, p in enumerate(poses):
         rot = np.asarray(p.rotation)
         R[k] = rot
         t[k] = np.asarray(p.translation, dtype=np.float64).reshape(3)
         fl[k] = 1 if (rot.flags.f_contiguous and not rot.flags.c_contiguous) else 0
     return R, t, fl
+
+
+@functools.lru_cache(maxsize=1)
+def _host_module():
+    """The native host helpers (_sfbhost), or None when not built."""
+    try:
+        from . import _sfbhost
+    except ImportError:
+        return None
+    return _sfbhost
 
 
 @functools.lru_cache(maxsize=64)

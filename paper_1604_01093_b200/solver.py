@@ -29,7 +29,7 @@ import threading
 import numpy as np
 
 from . import _abi
-from .device_problem import DeviceProblem
+from .device_problem import DeviceProblem, _host_module
 from .runtime import runtime
 from .se3 import RigidTransform
 
@@ -717,6 +717,10 @@ class AlignmentProblem:
 
     def _pull_poses(self):
         R, t = self._dp.get_poses()
+        host = _host_module()
+        if host is not None and type(self.poses) is dict:
+            host.make_poses(self.poses, self.frame_ids, R, t, RigidTransform, 1)
+            return
         for k, f in enumerate(self.frame_ids[1:], start=1):
             self.poses[f] = RigidTransform(R[k].copy(), t[k].copy())
 

@@ -164,3 +164,53 @@ def test_native_frame_descriptors():
     odd = copy.copy(caches[0])
     odd.points_low = np.asfortranarray(odd.points_low)
     assert _sfbhost.fill_frame_descs([odd], d) is None
+
+
+def _py_pose_arrays(poses):
+    """device_problem._pose_arrays' NumPy loop, restated as the checker."""
+    n = len(poses)
+    R, t, fl = np.empty((n, 3, 3)), np.empty((n, 3)), np.zeros(n, np.uint8)
+    for k, p in enumerate(poses):
+        rot = np.asarray(p.rotation)
+        R[k] = rot
+        t[k] = np.asarray(p.translation, dtype=np.float64).reshape(3)
+        fl[k] = 1 if (rot.flags.f_contiguous and not rot.flags.c_contiguous) else 0
+    return R, t, fl
+
+
+def test_native_pose_packing_matches_numpy_path():
+    """_sfbhost.pack_poses / make_poses == the NumPy pose push / pull, including
+    F-ordered and strided rotations (the BLAS-order flag) and the fallback."""
+    from paper_1604_01093_b200 import _build
+    _build.build_host()
+    from paper_1604_01093_b200 import _sfbhost
+    from paper_1604_01093_b200.device_problem import _pose_arrays
+    from paper_1604_01093_b200.solver import RigidTransform
+    rng = np.random.default_rng(3)
+    poses = [RigidTransform(rng.standard_normal((3, 3)), rng.standard_normal(3)) for _ in range(40)]
+    poses[2] = RigidTransform(np.asfortranarray(poses[2].rotation), poses[2].translation.reshape(3, 1).copy())
+    poses[3] = RigidTransform(rng.standard_normal((3, 5))[:, 1:4], rng.standard_normal((3, 2))[:, 1])
+    n = len(poses)
+    R, t, fl = np.empty((n, 3, 3)), np.empty((n, 3)), np.zeros(n, np.uint8)
+    assert _sfbhost.pack_poses(poses, R, t, fl) is True
+    for got, want in zip((R, t, fl), _py_pose_arrays(poses)):
+        assert np.array_equal(got, want)
+    assert fl[2] == 1 and fl[3] == 0
+    # non-float64 / non-array entries: None, and _pose_arrays falls back
+    odd = list(poses)
+    odd[5] = RigidTransform([[1, 0, 0], [0, 1, 0], [0, 0, 1]], [1, 2, 3])
+    assert _sfbhost.pack_poses(odd, R, t, fl) is None
+    for got, want in zip(_pose_arrays(odd), _py_pose_arrays(odd)):
+        assert np.array_equal(got, want)
+    with pytest.raises(ValueError):
+        _sfbhost.pack_poses(poses, R[:3], t, fl)
+    # pull: fresh C-contiguous owned copies, frame 0 untouched
+    ids = [10 * k for k in range(n)]
+    d = {f: None for f in ids}
+    assert _sfbhost.make_poses(d, ids, R, t, RigidTransform, 1) is None
+    assert d[0] is None
+    for k in range(1, n):
+        p = d[ids[k]]
+        assert type(p) is RigidTransform
+        assert np.array_equal(p.rotation, R[k]) and np.array_equal(p.translation, t[k])
+        assert p.rotation.flags.c_contiguous and p.rotation.flags.owndata
