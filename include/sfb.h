@@ -197,6 +197,11 @@ int sfb_problem_create(sfb_ctx* ctx, int32_t n_frames, const int32_t* slots,
                        const int32_t* set_frame_j, const int64_t* set_offsets,
                        const double* points_i, const double* points_j,
                        sfb_problem** out);
+/* Attach the frames to a problem created with slots == NULL (the caller
+ * builds the problem while the frames upload is still in flight; the same
+ * state as passing the slots to sfb_problem_create).  Once only, before any
+ * dense call. */
+int sfb_problem_attach_frames(sfb_problem* p, const int32_t* slots);
 int sfb_problem_destroy(sfb_problem* p);
 int sfb_problem_stream(sfb_problem* p, void** stream_out);
 

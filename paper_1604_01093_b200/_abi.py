@@ -84,6 +84,7 @@ SIGNATURES = {
     "sfb_frames_upload": [_P, _I32, C.POINTER(FrameDesc), _P],
     "sfb_frames_release": [_P, _I32, _P],
     "sfb_problem_create": [_P, _I32, _P, _I32, _P, _P, _P, _P, _P, C.POINTER(_P)],
+    "sfb_problem_attach_frames": [_P, _P],
     "sfb_problem_destroy": [_P],
     "sfb_problem_stream": [_P, C.POINTER(_P)],
     "sfb_set_poses": [_P, _P, _P, _P],

@@ -40,7 +40,7 @@ def build_host(force: bool = False) -> Path:
     import numpy
     cmd = [os.environ.get("CC", "gcc"), "-O2", "-shared", "-fPIC", "-Wall",
            "-I", sysconfig.get_paths()["include"], "-I", numpy.get_include(), str(HOST_SRC),
-           "-o", str(tmp)]
+           "-o", str(tmp), "-lpthread"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"gcc failed ({res.returncode}):\n{res.stdout}\n{res.stderr}")

@@ -12,6 +12,7 @@
 #include <Python.h>
 #define NPY_NO_DEPRECATED_API NPY_1_7_API_VERSION
 #include <numpy/arrayobject.h>
+#include <pthread.h>
 #include <stdint.h>
 #include <string.h>
 
@@ -32,6 +33,27 @@ static int get_f64_rows(PyObject* arr, const char** data, Py_ssize_t* rows) {
   *data = (const char*)PyArray_DATA(a);
   *rows = PyArray_DIM(a, 0);
   return 1;
+}
+
+/* set range [s0, s1) of the stacked copy */
+#define COPY_THREADS 6
+typedef struct {
+  const SetBufs* b;
+  const int64_t* of;
+  char *di, *dj;
+  Py_ssize_t s0, s1;
+} CopyTask;
+
+static void* copy_task(void* arg) {
+  const CopyTask* t = (const CopyTask*)arg;
+  for (Py_ssize_t s = t->s0; s < t->s1; ++s) {
+    const size_t nb = (size_t)(t->of[s + 1] - t->of[s]) * 24;
+    if (nb) {
+      memcpy(t->di + t->of[s] * 24, t->b[s].pi, nb);
+      memcpy(t->dj + t->of[s] * 24, t->b[s].pj, nb);
+    }
+  }
+  return NULL;
 }
 
 /* interned attribute names (PyObject_GetAttrString would build a str per call) */
@@ -138,15 +160,35 @@ static PyObject* stack_sets_into(PyObject* self, PyObject* args) {
   }
   if (hi == 0 || hj == 0) goto done;
   {
-    char* di = (char*)vi.buf;
-    char* dj = (char*)vj.buf;
-    for (Py_ssize_t s = 0; s < n; ++s) {
-      const size_t nb = (size_t)(of[s + 1] - of[s]) * 24;
-      if (nb) {
-        memcpy(di + of[s] * 24, b[s].pi, nb);
-        memcpy(dj + of[s] * 24, b[s].pj, nb);
-      }
+    /* the copies need no Python objects (b[] holds the references): release
+     * the GIL - the frames-upload thread can finish meanwhile - and split
+     * large stacks over a few threads by set range */
+    CopyTask t[COPY_THREADS];
+    const int64_t bytes = total * 48;
+    int nt = bytes >= ((int64_t)4 << 20) ? COPY_THREADS : 1;
+    if (nt > n) nt = n > 0 ? (int)n : 1;
+    Py_BEGIN_ALLOW_THREADS
+    pthread_t th[COPY_THREADS];
+    int started[COPY_THREADS] = {0};
+    for (int k = 0; k < nt; ++k) {
+      /* balance by rows: task k copies the sets whose first row lies in its share */
+      t[k] = (CopyTask){b, of, (char*)vi.buf, (char*)vj.buf, 0, 0};
+      const int64_t lo = total * k / nt, hi = total * (k + 1) / nt;
+      Py_ssize_t s0 = 0, s1 = n;
+      { Py_ssize_t a = 0, z = n; while (a < z) { Py_ssize_t m = (a + z) / 2; if (of[m] < lo) a = m + 1; else z = m; } s0 = a; }
+      { Py_ssize_t a = 0, z = n; while (a < z) { Py_ssize_t m = (a + z) / 2; if (of[m] < hi) a = m + 1; else z = m; } s1 = a; }
+      if (k == nt - 1) s1 = n;
+      if (k == 0) s0 = 0;
+      t[k].s0 = s0;
+      t[k].s1 = s1;
     }
+    for (int k = 1; k < nt; ++k) started[k] = pthread_create(&th[k], NULL, copy_task, &t[k]) == 0;
+    copy_task(&t[0]);
+    for (int k = 1; k < nt; ++k) {
+      if (started[k]) pthread_join(th[k], NULL);
+      else copy_task(&t[k]);
+    }
+    Py_END_ALLOW_THREADS
   }
   res = PyLong_FromLongLong((long long)total);
 done:

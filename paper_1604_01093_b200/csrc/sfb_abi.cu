@@ -95,7 +95,6 @@ struct sfb_problem : Handle {
   DBuf<uint8_t> f_fl, f_pass, f_temp;
   DBuf<int> f_cnt;
   DBuf<int> f_need;  // [0] queue length, then the undecided candidates (pair filter stage 2)
-  std::vector<int> pair_table;  // rebuild_structure's flat pair-id table
 };
 
 namespace {
@@ -202,10 +201,13 @@ int rebuild_structure(sfb_problem* p, int bidir) {
   // a hash map beyond that
   std::vector<int2> pv;
   const bool flat = (int64_t)nb * nb <= ((int64_t)16 << 20);
-  std::vector<int>& pid_flat = p->pair_table;  // persistent, all -1 between rebuilds
+  // persistent per host thread (a 16 MB table costs ~3 ms of page faults to
+  // create), all -1 between rebuilds
+  static thread_local std::vector<int> pair_table;
+  std::vector<int>& pid_flat = pair_table;
   std::unordered_map<int64_t, int> pid;
   if (flat) {
-    if (pid_flat.size() != (size_t)nb * nb) pid_flat.assign((size_t)nb * nb, -1);
+    if (pid_flat.size() < (size_t)nb * nb) pid_flat.resize((size_t)nb * nb, -1);
   } else {
     pid.reserve(2 * (size_t)(p->n_sets + p->n_dir) + 8);
   }
@@ -792,6 +794,26 @@ int sfb_frames_release(sfb_ctx* c, int32_t n, const int32_t* slots) {
     }
     sl.block = nullptr;
   }
+  return SFB_OK;
+}
+
+int sfb_problem_attach_frames(sfb_problem* p, const int32_t* slots) {
+  if (!p || !slots) return fail(p, SFB_E_ARG, "bad arguments");
+  if (p->has_frames) return fail(p, SFB_E_ARG, "frames already attached");
+  sfb_ctx* c = p->ctx;
+  CK(p, cudaSetDevice(c->device));
+  std::vector<FrameDev> fr(p->n);
+  for (int k = 0; k < p->n; ++k) {
+    const int sl = slots[k];
+    if (sl < 0 || sl >= (int)c->slots.size() || !c->slots[sl].alive)
+      return fail(p, SFB_E_ARG, "frame slot not uploaded");
+    fr[k] = c->slots[sl].dev;
+  }
+  CK(p, upload_vec(p->frames, fr, p->stream));
+  CK(p, cudaStreamSynchronize(p->stream));  // fr dies here
+  p->frames_h.swap(fr);
+  p->slots.assign(slots, slots + p->n);
+  p->has_frames = true;
   return SFB_OK;
 }
 

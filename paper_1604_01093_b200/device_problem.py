@@ -101,6 +101,12 @@ class DeviceProblem:
         self.n_vars = 6 * (n_frames - 1)
         self.version = 0
 
+    def attach_frames(self, caches_in_order, slots) -> None:
+        """Frames for a problem created without them (uploaded meanwhile)."""
+        slots = np.ascontiguousarray(slots, dtype=np.int32)
+        self._ck(self.lib.sfb_problem_attach_frames(self.handle, _abi.ptr(slots)))
+        self._caches = caches_in_order
+
     def close(self):
         if getattr(self, "handle", None) is not None:
             self.lib.sfb_problem_destroy(self.handle)

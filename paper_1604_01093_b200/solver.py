@@ -690,7 +690,7 @@ class AlignmentProblem:
 
                 def _upload():
                     try:
-                        rt.slots_for(cl, on_submit=submitted.set)
+                        box["slots"] = rt.slots_for(cl, on_submit=submitted.set)
                     except BaseException as e:  # re-raised on the caller's thread
                         box["e"] = e
                         submitted.set()
@@ -698,16 +698,26 @@ class AlignmentProblem:
                 th = threading.Thread(target=_upload, daemon=True)
                 th.start()
                 submitted.wait()
+                dp = None
                 try:
+                    # the sparse problem is built while the frames are in flight
                     frames, off, pi, pj = _set_layout(self.corr_sets, index, rt)
+                    dp = DeviceProblem(len(self.frame_ids), None, frames, pi, pj, off,
+                                       device=self._device)
                 finally:
                     th.join()
-                if "e" in box:
-                    raise box["e"]
+                try:
+                    if "e" in box:
+                        raise box["e"]
+                    dp.attach_frames(cl, box["slots"])
+                except BaseException:
+                    dp.close()
+                    raise
+                self._dp = dp
             else:
                 frames, off, pi, pj = _set_layout(self.corr_sets, index, runtime(self._device))
-            self._dp = DeviceProblem(len(self.frame_ids), cl, frames, pi, pj, off,
-                                     device=self._device)
+                self._dp = DeviceProblem(len(self.frame_ids), cl, frames, pi, pj, off,
+                                         device=self._device)
             if self._xch is not None:
                 self._dp.set_shard(self._xch.rank, self._xch.world)
         return self._dp

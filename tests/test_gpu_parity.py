@@ -194,3 +194,31 @@ def test_solve_is_bit_reproducible():
         out.append((np.stack([p.poses[f].rotation for f in s.ids]),
                     [r.energy_after for r in st.iterations]))
     assert np.array_equal(out[0][0], out[1][0]) and out[0][1] == out[1][1]
+
+
+def test_overlapped_setup_matches_direct_setup():
+    """cfg3 (> 256 sets) builds the sparse problem while the frames upload
+    (sfb_problem_attach_frames); the direct construction with the slots must
+    give the bit-identical solve, and attaching twice is an error."""
+    from paper_1604_01093_b200.device_problem import DeviceProblem
+    from paper_1604_01093_b200.runtime import runtime
+    s = GoldenScene("cfg3")
+    assert len(s.corr_sets) > 256
+    W, C = s.weights_obj(S), s.config_obj(S)
+    p1 = S.AlignmentProblem(s.ids, s.init, s.corr_sets, s.caches)
+    st1 = p1.solve(W, C, 3)
+    p2 = S.AlignmentProblem(s.ids, s.init, s.corr_sets, s.caches)
+    index = {f: k for k, f in enumerate(s.ids)}
+    cl = [s.caches[f] for f in s.ids]
+    frames, off, pi, pj = S._set_layout(s.corr_sets, index)
+    p2._dp = DeviceProblem(len(s.ids), cl, frames, pi, pj, off)
+    st2 = p2.solve(W, C, 3)
+    assert [r.energy_after for r in st1.iterations] == [r.energy_after for r in st2.iterations]
+    for f in s.ids:
+        assert np.array_equal(p1.poses[f].rotation, p2.poses[f].rotation)
+        assert np.array_equal(p1.poses[f].translation, p2.poses[f].translation)
+    slots = runtime(0).slots_for(cl)
+    with pytest.raises(Exception, match="already attached"):
+        p1._dp.attach_frames(cl, slots)
+    p1.close()
+    p2.close()
