@@ -274,18 +274,128 @@ __device__ __forceinline__ unsigned char tile_maybe_visible(const Xf& rel, const
   return 1;
 }
 
+#ifndef DENSE_TMEM
+#define DENSE_TMEM 1
+#endif
+#if DENSE_TMEM
+// Tensor-memory accumulators: the 27 H/g sums of each thread live in TMEM (54
+// 32-bit columns of its lane; warp w uses lanes 32(w%4).. and columns
+// 64(w/4)..), read-modify-written once per tile by the warp (tcgen05.ld/st,
+// warp-converged), so registers hold only the tile's Jacobian rows: 80
+// registers, 3 CTAs (24 warps) per SM instead of 128 registers and 2 CTAs
+// (6.61 -> 6.32 ms per launch at cfg4).  The per-entry FMA order (photo row
+// 0, photo row 1, geo row) is the register path's.  -DDENSE_TMEM=0 builds
+// the register-accumulator kernel.
+#define TM_LD16(addr, u)                                                                        \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" \
+               : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]),      \
+                 "=r"(u[6]), "=r"(u[7]), "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]),    \
+                 "=r"(u[12]), "=r"(u[13]), "=r"(u[14]), "=r"(u[15])                            \
+               : "r"(addr))
+#define TM_ST16(addr, u)                                                                        \
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" \
+               ::"r"(addr), "r"(u[0]), "r"(u[1]), "r"(u[2]), "r"(u[3]), "r"(u[4]), "r"(u[5]), \
+                 "r"(u[6]), "r"(u[7]), "r"(u[8]), "r"(u[9]), "r"(u[10]), "r"(u[11]),           \
+                 "r"(u[12]), "r"(u[13]), "r"(u[14]), "r"(u[15])                                \
+               : "memory")
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ double tm_d(const uint32_t* u, int k) {
+  return __hiloint2double((int)u[2 * k + 1], (int)u[2 * k]);
+}
+__device__ __forceinline__ void tm_set(uint32_t* u, int k, double v) {
+  u[2 * k] = (uint32_t)__double2loint(v);
+  u[2 * k + 1] = (uint32_t)__double2hiint(v);
+}
+// entry E of the 27 (21 packed H, then 6 g): photo rows 0, 1 then the geo row,
+// the order of the register path's accum_row calls (compile-time indices)
+__host__ __device__ constexpr int sym6_row(int e) {
+  int r = 0;
+  while (e >= 6 - r) { e -= 6 - r; ++r; }
+  return r;
+}
+__host__ __device__ constexpr int sym6_col(int e) {
+  int r = 0;
+  while (e >= 6 - r) { e -= 6 - r; ++r; }
+  return e + r;
+}
+template <int E>
+__device__ __forceinline__ double tm_update(double acc, const double (&jp)[2][6],
+                                            const double (&rp)[2], const double (&jg)[6],
+                                            double rg, double sp, double sg) {
+  if constexpr (E < 21) {
+    constexpr int r = sym6_row(E), c = sym6_col(E);
+    acc = fma(sp * jp[0][r], jp[0][c], acc);
+    acc = fma(sp * jp[1][r], jp[1][c], acc);
+    return fma(sg * jg[r], jg[c], acc);
+  } else {
+    constexpr int r = E - 21;
+    acc = fma(sp * jp[0][r], rp[0], acc);
+    acc = fma(sp * jp[1][r], rp[1], acc);
+    return fma(sg * jg[r], rg, acc);
+  }
+}
+template <int Q>
+__device__ __forceinline__ void tm_chunk(uint32_t tm, const double (&jp)[2][6], const double (&rp)[2],
+                                         const double (&jg)[6], double rg, double sp, double sg) {
+  uint32_t u[16];
+  TM_LD16(tm + 16 * Q, u);
+  tm_wait_ld();
+  tm_set(u, 0, tm_update<8 * Q + 0>(tm_d(u, 0), jp, rp, jg, rg, sp, sg));
+  tm_set(u, 1, tm_update<8 * Q + 1>(tm_d(u, 1), jp, rp, jg, rg, sp, sg));
+  tm_set(u, 2, tm_update<8 * Q + 2>(tm_d(u, 2), jp, rp, jg, rg, sp, sg));
+  if constexpr (8 * Q + 3 < 27) {
+    tm_set(u, 3, tm_update<8 * Q + 3>(tm_d(u, 3), jp, rp, jg, rg, sp, sg));
+    tm_set(u, 4, tm_update<8 * Q + 4>(tm_d(u, 4), jp, rp, jg, rg, sp, sg));
+    tm_set(u, 5, tm_update<8 * Q + 5>(tm_d(u, 5), jp, rp, jg, rg, sp, sg));
+    tm_set(u, 6, tm_update<8 * Q + 6>(tm_d(u, 6), jp, rp, jg, rg, sp, sg));
+    tm_set(u, 7, tm_update<8 * Q + 7>(tm_d(u, 7), jp, rp, jg, rg, sp, sg));
+  }
+  TM_ST16(tm + 16 * Q, u);
+}
+#ifndef DENSE_TMEM_BLOCKS
+#define DENSE_TMEM_BLOCKS 3
+#endif
+#define DENSE_BLOCKS_EFF DENSE_TMEM_BLOCKS
+#else
+#define DENSE_BLOCKS_EFF DENSE_MIN_BLOCKS
+#endif
+
 template <bool STD, bool PREV>
 #ifndef DENSE_MIN_BLOCKS
 #define DENSE_MIN_BLOCKS 2
 #endif
-__global__ void __launch_bounds__(DENSE_THREADS, DENSE_MIN_BLOCKS) k_dense_fused(DenseArgs a) {
+__global__ void __launch_bounds__(DENSE_THREADS, DENSE_BLOCKS_EFF) k_dense_fused(DenseArgs a) {
   __shared__ FusedCtx ec;
   const int4 it = a.items[blockIdx.x];
   const int2 de = a.dir_edges[it.x];
   if (threadIdx.x == 0) load_fused_ctx(&ec, a.poses[de.x], a.poses[de.y], a.rd);
   const FrameDev Fi = a.frames[de.x];
   const FrameDev Fj = a.frames[de.y];
+#if DENSE_TMEM
+  __shared__ uint32_t tm_base;
+  if ((threadIdx.x >> 5) == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&tm_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  // warp w: lanes 32*(w%4).., columns 64*(w/4) .. +56
+  const uint32_t tm = tm_base + ((uint32_t)(((threadIdx.x >> 5) & 3) * 32) << 16) +
+                      (uint32_t)((threadIdx.x >> 7) * 64);
+  {
+    uint32_t z[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) z[k] = 0u;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) TM_ST16(tm + 16 * q, z);
+    tm_wait_st();
+  }
+#else
+  __syncthreads();
+#endif
   const int ord_ph = (Fi.n_valid_depth == 1) ? a.rd.apply_1 : a.rd.apply_n;
   const int ord_ge = (Fi.n_valid_geo == 1) ? a.rd.apply_1 : a.rd.apply_n;
   const int lane = threadIdx.x & 31;
@@ -312,9 +422,13 @@ __global__ void __launch_bounds__(DENSE_THREADS, DENSE_MIN_BLOCKS) k_dense_fused
   }
   __syncthreads();
 
+#if DENSE_TMEM
+  double acc27 = 0.0, acc28 = 0.0;
+#else
   double acc[29];
 #pragma unroll
   for (int k = 0; k < 29; ++k) acc[k] = 0.0;
+#endif
   double eprev_p = 0.0, eprev_g = 0.0;
 
   // pixels in tile-major order: slot m = tile * 256 + threadIdx.x (the frozen
@@ -465,6 +579,11 @@ __global__ void __launch_bounds__(DENSE_THREADS, DENSE_MIN_BLOCKS) k_dense_fused
     if (a.do_geo) gtgt[m] = tgt >= 0 ? (uint16_t)tgt : (uint16_t)0xFFFF;
     if (__ballot_sync(0xffffffffu, ph_in || tgt >= 0) && lane == 0) tile_state[t - it.y] |= 4u;
 
+#if DENSE_TMEM
+    double jp[2][6], rp[2] = {0.0, 0.0}, jg[6], rg = 0.0;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) jp[0][k] = jp[1][k] = jg[k] = 0.0;
+#endif
     // ---- photometric: one bilinear sample serves the frozen energy and J
     if (ph_in || pph) {
       double val[2], ddx[2], ddy[2];
@@ -479,6 +598,24 @@ __global__ void __launch_bounds__(DENSE_THREADS, DENSE_MIN_BLOCKS) k_dense_fused
         // J_i = M_j v with M_j = [[R_j, -[t_j]x R_j], [0, -R_j]] (per edge) and
         // v = [dq x q ; dq] in camera-j coordinates (dq = d value / d q):
         // accumulate v v^T here, apply M_j once per edge (k_edge_reduce).
+#if DENSE_TMEM
+        acc27 += e2;
+        const double a_ = Fj.fx * rz, b_ = Fj.fy * rz;
+        rp[0] = r0;
+        rp[1] = r1;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const double dq0 = ddx[c] * a_, dq1 = ddy[c] * b_;
+          const double dq2 = -(dq0 * q0 + dq1 * q1) * rz;
+          jp[c][0] = dq1 * q2 - dq2 * q1;
+          jp[c][1] = dq2 * q0 - dq0 * q2;
+          jp[c][2] = dq0 * q1 - dq1 * q0;
+          jp[c][3] = dq0;
+          jp[c][4] = dq1;
+          jp[c][5] = dq2;
+        }
+      }
+#else
         acc[27] += e2;
         const double a_ = Fj.fx * rz, b_ = Fj.fy * rz;
         const double res[2] = {r0, r1};
@@ -491,6 +628,7 @@ __global__ void __launch_bounds__(DENSE_THREADS, DENSE_MIN_BLOCKS) k_dense_fused
           accum_row(acc, v, res[c], a.s_photo);
         }
       }
+#endif
     }
     // ---- point-to-plane: new association and/or frozen target
     if (tgt >= 0 || (PREV && ptg != 0xFFFF)) {
@@ -510,10 +648,21 @@ __global__ void __launch_bounds__(DENSE_THREADS, DENSE_MIN_BLOCKS) k_dense_fused
         const double nj0 = ec.rel.R[0] * n0 + ec.rel.R[1] * n1 + ec.rel.R[2] * n2;
         const double nj1 = ec.rel.R[3] * n0 + ec.rel.R[4] * n1 + ec.rel.R[5] * n2;
         const double nj2 = ec.rel.R[6] * n0 + ec.rel.R[7] * n1 + ec.rel.R[8] * n2;
+#if DENSE_TMEM
+        jg[0] = t1 * nj2 - t2 * nj1;
+        jg[1] = t2 * nj0 - t0 * nj2;
+        jg[2] = t0 * nj1 - t1 * nj0;
+        jg[3] = -nj0;
+        jg[4] = -nj1;
+        jg[5] = -nj2;
+        rg = r;
+        acc28 += r * r;
+#else
         const double v[6] = {t1 * nj2 - t2 * nj1, t2 * nj0 - t0 * nj2, t0 * nj1 - t1 * nj0,
                              -nj0, -nj1, -nj2};
         accum_row(acc, v, r, a.s_geo);
         acc[28] += r * r;
+#endif
       }
       if (PREV && ptg != 0xFFFF) {
         if (ptg == tgt) {
@@ -530,7 +679,32 @@ __global__ void __launch_bounds__(DENSE_THREADS, DENSE_MIN_BLOCKS) k_dense_fused
         }
       }
     }
+#if DENSE_TMEM
+    __syncwarp();
+    if (__any_sync(0xffffffffu, ph_in || tgt >= 0)) {
+      const double sp = a.s_photo, sg = a.s_geo;
+      tm_chunk<0>(tm, jp, rp, jg, rg, sp, sg);
+      tm_chunk<1>(tm, jp, rp, jg, rg, sp, sg);
+      tm_chunk<2>(tm, jp, rp, jg, rg, sp, sg);
+      tm_chunk<3>(tm, jp, rp, jg, rg, sp, sg);
+      tm_wait_st();
+    }
+#endif
   }
+#if DENSE_TMEM
+  double acc[29];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint32_t u[16];
+    TM_LD16(tm + 16 * q, u);
+    tm_wait_ld();
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (8 * q + k < 27) acc[8 * q + k] = tm_d(u, k);
+  }
+  acc[27] = acc27;
+  acc[28] = acc28;
+#endif
   double* out = a.item_out + (int64_t)blockIdx.x * SFB_ITEM_STRIDE;
   if (PREV) {
     double tail[31];
@@ -546,6 +720,13 @@ __global__ void __launch_bounds__(DENSE_THREADS, DENSE_MIN_BLOCKS) k_dense_fused
   // (block_reduce_store synchronised the CTA: tile_state bit2 is final)
   for (int t = it.y + threadIdx.x; t < it.z; t += blockDim.x)
     a.tile_any[toff + t] = (tile_state[t - it.y] & 4u) ? 1 : 0;
+#if DENSE_TMEM
+  // every warp's last TMEM read completed (wait::ld) before block_reduce_store's barrier
+  if ((threadIdx.x >> 5) == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tm_base));
+  }
+#endif
 }
 
 void launch_dense_linearize(const DenseArgs& a, cudaStream_t s) {
