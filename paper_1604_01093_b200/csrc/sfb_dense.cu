@@ -577,7 +577,10 @@ __global__ void __launch_bounds__(DENSE_THREADS, DENSE_BLOCKS_EFF) k_dense_fused
     }
 #endif
     if (a.do_geo) gtgt[m] = tgt >= 0 ? (uint16_t)tgt : (uint16_t)0xFFFF;
-    if (__ballot_sync(0xffffffffu, ph_in || tgt >= 0) && lane == 0) tile_state[t - it.y] |= 4u;
+    // every warp that freezes an association in this tile stores the same
+    // byte (bits 0-1 are constant after the barrier above): no read-modify-write
+    if (__ballot_sync(0xffffffffu, ph_in || tgt >= 0) && lane == 0)
+      tile_state[t - it.y] = (unsigned char)(st | 4u);
 
 #if DENSE_TMEM
     double jp[2][6], rp[2] = {0.0, 0.0}, jg[6], rg = 0.0;
