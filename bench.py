@@ -319,36 +319,129 @@ def cpu_extrapolate(scene_name, edges_undirected, records, workers: int, pair_sa
 # ---------------------------------------------------------------------------
 
 
+def _filter_chunk(args):
+    """Worker: the oracle pair filter (solver.py:130-148) over a chunk of pairs."""
+    scene_name, pairs = args
+    from oracle import scanfuse_oracle as O
+    scene = _scene_cache(scene_name)
+    poses = {f: O.pose_of(p) for f, p in scene.init.items()}
+    out = []
+    for (a, b) in pairs:
+        if O.view_angle_deg(poses[a], poses[b]) >= 60.0:
+            continue
+        if O.frustum_overlap(scene.caches[a], poses[a], scene.caches[b], poses[b]) <= 0.0:
+            continue
+        if O.frustum_overlap(scene.caches[b], poses[b], scene.caches[a], poses[a]) <= 0.0:
+            continue
+        out.append((a, b))
+    return out
+
+
+def reference_step(pool, workers, scene_name, frac=1.0, seed=0):
+    """One reference-arm step on the host cores: the oracle pair filter over
+    ALL n(n-1)/2 frame pairs, then ONE complete dense GN linearisation
+    (associate + linearise + accumulate + frozen energy, solver.py:582-672)
+    over every accepted edge, one sparse linearisation and one full matvec.
+    Returns (seconds per phase, edges).  `frac` < 1 samples (warm-up only)."""
+    from oracle import scanfuse_oracle as O
+    scene = _scene_cache(scene_name)
+    ids = scene.frame_ids
+    n = len(ids)
+    pairs = [(ids[a], ids[b]) for a in range(n) for b in range(a + 1, n)]
+    if frac < 1.0:
+        rng = np.random.default_rng(seed)
+        pairs = [pairs[k] for k in sorted(rng.choice(len(pairs), max(1, int(frac * len(pairs))),
+                                                       replace=False))]
+    chunks = [pairs[k::workers * 4] for k in range(workers * 4)]
+    t0 = time.perf_counter()
+    outs = pool.map(_filter_chunk, [(scene_name, c) for c in chunks if c])
+    t_filter = time.perf_counter() - t0
+    edges = sorted(e for o in outs for e in o)
+    echunks = [edges[k::workers * 4] for k in range(workers * 4)]
+    t0 = time.perf_counter()
+    pool.map(_time_edges, [(scene_name, c) for c in echunks if c])
+    t_gn = time.perf_counter() - t0
+    prob = O.Problem(ids, {f: O.pose_of(p) for f, p in scene.init.items()}, scene.corr_sets, None)
+    t0 = time.perf_counter()
+    S_, _, _ = prob.linearize(O.DEFAULT_W, 0.0, O.DEFAULT_CFG)
+    t_sparse = time.perf_counter() - t0
+    S_.dense = np.zeros((prob.n_vars, prob.n_vars))
+    x = np.random.default_rng(seed).normal(size=prob.n_vars)
+    t0 = time.perf_counter()
+    S_.apply(x)
+    t_mv = time.perf_counter() - t0
+    return {"filter": t_filter, "dense_gn": t_gn, "sparse": t_sparse, "matvec": t_mv}, edges
+
+
 def run_reference(args, rank):
+    """--impl reference: the oracle port (NumPy restatement of the reference,
+    oracle/scanfuse_oracle.py) on all host cores.  Each timed step measures
+    the FULL pair filter and ONE COMPLETE dense GN iteration of the workload
+    (every accepted edge, no sampling) and reports the full-solve time they
+    imply for the default schedule (10 GN, 9 of them dense, 10 x (50 + 2)
+    matvecs; the cfg4 solve runs exactly that)."""
     if rank != 0:
         return
+    import multiprocessing as mp
     workers = os.cpu_count() or 1
     scene = _scene_cache(args.config)
-    vals = []
+    pool = mp.get_context("fork").Pool(workers)  # forked with the scene loaded
+    pool.map(_noop, range(workers))
+    n_gn, n_dense, n_mv = 10, 9, 10 * (50 + 2)
+    vals, phases, n_edges = [], [], 0
     for k in range(args.warmup + args.steps):
-        ms, sample, _ = cpu_extrapolate(args.config, None, None, workers,
-                                        pair_sample=120 * workers, edge_sample=12 * workers,
-                                        seed=k)
-        if k >= args.warmup:
-            vals.append(ms)
+        timed = k >= args.warmup
+        ph, edges = reference_step(pool, workers, args.config, 1.0 if timed else 0.01, seed=k)
+        if timed:
+            total = ph["filter"] + n_dense * ph["dense_gn"] + 2 * n_gn * ph["sparse"] + n_mv * ph["matvec"]
+            vals.append(1e3 * total)
+            phases.append(ph)
+            n_edges = len(edges)
+    pool.close()
+    pool.join()
     v = float(np.median(vals))
+    med = {key: float(np.median([p[key] for p in phases])) for key in phases[0]}
+    sample = (f"per step: full oracle pair filter ({len(scene.frame_ids) * (len(scene.frame_ids) - 1) // 2}"
+              f" pairs -> {n_edges} edges) + one complete dense GN iteration over all {n_edges} "
+              f"edges on {workers} processes, then x{n_dense} dense GN + {n_mv} matvecs "
+              f"(measured: filter {med['filter']:.2f} s, dense GN iteration {med['dense_gn']:.2f} s, "
+              f"sparse lin {med['sparse']:.3f} s, matvec {1e3 * med['matvec']:.2f} ms)")
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "ms", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOADS[args.config], "name": args.config,
-                   "frames": len(scene.frame_ids)},
+                   "frames": len(scene.frame_ids), "dense_edges": n_edges},
         "cpu_baseline": {"value": v, "unit": "ms", "cores": workers, "kind": "port",
-                         "sample": sample},
+                         "sample": sample, "s_per_dense_gn_iteration": med["dense_gn"],
+                         "s_pair_filter": med["filter"], "steps_ms": [round(x, 1) for x in vals]},
         "e2e": {"value": v, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+def self_launch(args) -> int:
+    """`--gpus N` (N > 1) without a torchrun environment: launch N ranks, one
+    per GPU, through torch.distributed.run on this node and return its exit
+    code (rank 0 prints the JSON line)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
 def main():
     args = parse()
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(self_launch(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":

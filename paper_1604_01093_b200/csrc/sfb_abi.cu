@@ -58,6 +58,8 @@ struct sfb_problem : Handle {
   DBuf<uint8_t> tile_any[2];     // per (edge, source tile): any frozen association
   int cur = 0;                   // buffer holding the latest linearisation
   DBuf<double> item_out, edge_out, item_e2;
+  DBuf<int2> stride_counts;      // per frame source counts on the stride grid
+  int stride_counts_for = 0;     // stride they were computed for (0: none)
   DBuf<double> edge_e2;          // frozen-energy sums per directed edge (2 each)
   bool dense_active = false;
   // between the two halves of a (possibly sharded) linearisation / energy
@@ -353,6 +355,21 @@ DenseArgs dense_args(sfb_problem* p) {
   return a;
 }
 
+// Per-frame source-pixel counts on a stride grid (> 1), computed once per stride.
+int ensure_stride_counts(sfb_problem* p, int stride, DenseArgs* a) {
+  a->stride = stride;
+  a->stride_counts = nullptr;
+  if (stride <= 1 || !p->has_frames) return SFB_OK;
+  if (p->stride_counts_for != stride) {
+    CK(p, p->stride_counts.ensure(p->n, p->stream));
+    launch_stride_counts(p->frames.p, p->n, stride, p->stride_counts.p, p->stream);
+    CKL(p);
+    p->stride_counts_for = stride;
+  }
+  a->stride_counts = p->stride_counts.p;
+  return SFB_OK;
+}
+
 SparseArgs sparse_args(sfb_problem* p) {
   SparseArgs a{};
   a.poses = p->poses.p;
@@ -411,7 +428,10 @@ int enqueue_linearize(sfb_problem* p, const sfb_weights* w, double w_dense, cons
     da.s_geo = w_dense * w->geo;
     da.geo_dmax = cfg->geo_distance_max;
     da.geo_nmin = cfg->geo_normal_min;
-    da.stride = cfg->dense_pixel_stride;
+    {
+      int rc = ensure_stride_counts(p, cfg->dense_pixel_stride, &da);
+      if (rc) return rc;
+    }
     if (lin) {
       const int nxt = 1 - p->cur;
       da.photo_mask = p->photo_mask[nxt].p;
@@ -594,6 +614,7 @@ int sfb_ctx_destroy(sfb_ctx* c) {
 
 int sfb_ctx_set_rounding(sfb_ctx* c, const sfb_rounding* r) {
   if (!c || !r) return fail(c, SFB_E_ARG, "null argument");
+  std::lock_guard<std::recursive_mutex> lk(c->mu);
   const int32_t v[6] = {r->matvec_c, r->matvec_f, r->gemm33, r->apply_n, r->apply_1, r->dot3};
   for (int k = 0; k < 6; ++k)
     if (v[k] < 0 || v[k] > 5) return fail(c, SFB_E_ARG, "rounding code out of range");
@@ -603,6 +624,7 @@ int sfb_ctx_set_rounding(sfb_ctx* c, const sfb_rounding* r) {
 
 int sfb_frames_upload(sfb_ctx* c, int32_t n, const sfb_frame_desc* d, int32_t* slots_out) {
   if (!c || n < 0 || (n > 0 && (!d || !slots_out))) return fail(c, SFB_E_ARG, "bad arguments");
+  std::lock_guard<std::recursive_mutex> lk(c->mu);
   if (n == 0) return SFB_OK;
   const auto t_start = std::chrono::steady_clock::now();
   CK(c, cudaSetDevice(c->device));
@@ -762,6 +784,7 @@ int sfb_frames_upload(sfb_ctx* c, int32_t n, const sfb_frame_desc* d, int32_t* s
 
 int sfb_frames_release(sfb_ctx* c, int32_t n, const int32_t* slots) {
   if (!c || (n > 0 && !slots)) return fail(c, SFB_E_ARG, "bad arguments");
+  std::lock_guard<std::recursive_mutex> lk(c->mu);
   cudaSetDevice(c->device);
   for (int k = 0; k < n; ++k) {
     const int s = slots[k];
@@ -803,12 +826,14 @@ int sfb_problem_attach_frames(sfb_problem* p, const int32_t* slots) {
   sfb_ctx* c = p->ctx;
   CK(p, cudaSetDevice(c->device));
   std::vector<FrameDev> fr(p->n);
+  std::unique_lock<std::recursive_mutex> lk(c->mu);  // slots may grow on another thread
   for (int k = 0; k < p->n; ++k) {
     const int sl = slots[k];
     if (sl < 0 || sl >= (int)c->slots.size() || !c->slots[sl].alive)
       return fail(p, SFB_E_ARG, "frame slot not uploaded");
     fr[k] = c->slots[sl].dev;
   }
+  lk.unlock();
   CK(p, upload_vec(p->frames, fr, p->stream));
   CK(p, cudaStreamSynchronize(p->stream));  // fr dies here
   p->frames_h.swap(fr);
@@ -838,6 +863,7 @@ int sfb_problem_create(sfb_ctx* c, int32_t n_frames, const int32_t* slots, int32
   if (slots) {
     p->has_frames = true;
     p->slots.assign(slots, slots + n_frames);
+    std::lock_guard<std::recursive_mutex> lk(c->mu);  // slots may grow on another thread
     for (int k = 0; k < n_frames; ++k) {
       const int sl = slots[k];
       if (sl < 0 || sl >= (int)c->slots.size() || !c->slots[sl].alive)
@@ -886,6 +912,9 @@ int sfb_problem_create(sfb_ctx* c, int32_t n_frames, const int32_t* slots, int32
       p->part.ensure(4 * 1024) || p->flags.ensure(64) || p->dscal.ensure(64))
     return bail(SFB_E_OOM, "vectors");
   if (pinned_scalars(&p->hscal) != cudaSuccess) return bail(SFB_E_OOM, "pinned");
+  // host arrays are borrowed for the call only: the async copies above must
+  // have landed before returning (they may come from reusable staging)
+  if (p->n_corr > 0 && cudaStreamSynchronize(s) != cudaSuccess) return bail(SFB_E_CUDA, "points upload");
   int rc = rebuild_structure(p, 0);
   if (rc) {
     std::string m = p->err;
@@ -910,6 +939,7 @@ int sfb_problem_destroy(sfb_problem* p) {
                         &p->dscal};
   for (auto* b : db) b->release();
   p->frames.release();
+  p->stride_counts.release();
   p->poses.release();
   p->best.release();
   p->set_off.release();
@@ -1192,6 +1222,7 @@ int sfb_pcg_dense(sfb_ctx* c, int32_t n, const double* A, const double* rhs, con
                   double* rel, int32_t* status) {
   if (!c || n < 0 || (n > 0 && (!A || !rhs || !diag || !x_out)) || !iters || !rel || !status)
     return fail(c, SFB_E_ARG, "bad arguments");
+  std::lock_guard<std::recursive_mutex> lk(c->mu);
   if (restart < 1) return fail(c, SFB_E_ARG, "restart_interval must be >= 1");
   if (n == 0) {
     *iters = 0;
@@ -1453,7 +1484,10 @@ int sfb_associate(sfb_problem* p, int32_t fi, int32_t fj, int32_t kind, const sf
   DenseArgs a = dense_args(p);
   a.geo_dmax = cfg->geo_distance_max;
   a.geo_nmin = cfg->geo_normal_min;
-  a.stride = cfg->dense_pixel_stride;
+  {
+    int rc = ensure_stride_counts(p, cfg->dense_pixel_stride, &a);
+    if (rc) return rc;
+  }
   launch_associate(a, fi, fj, kind, ds.p, dt.p, p->stream);
   CKL(p);
   CK(p, cudaMemcpyAsync(sel, ds.p, hw, cudaMemcpyDeviceToHost, p->stream));

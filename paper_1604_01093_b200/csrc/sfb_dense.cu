@@ -184,6 +184,47 @@ __device__ __forceinline__ bool stride_ok(int p, int w, int stride) {
   return (y % stride) == 0 && (x % stride) == 0;
 }
 
+// Source-pixel counts of _source_pixel_data (solver.py:158-167) for frame f:
+// (valid_depth, valid_depth & valid_normal) on the stride grid.  NumPy's
+// rounding of relative.apply differs when exactly one pixel is selected.
+__device__ __forceinline__ int2 src_counts(const DenseArgs& a, const FrameDev& F, int f) {
+  if (a.stride > 1 && a.stride_counts) return a.stride_counts[f];
+  return make_int2(F.n_valid_depth, F.n_valid_geo);
+}
+
+__global__ void k_stride_counts(const FrameDev* frames, int stride, int2* out) {
+  const FrameDev F = frames[blockIdx.x];
+  int cd = 0, cg = 0;
+  for (int p = threadIdx.x; p < F.w * F.h; p += blockDim.x) {
+    if (!stride_ok(p, F.w, stride)) continue;
+    const unsigned fl = __float_as_uint(__ldg(&F.P[p]).w);
+    cd += (fl & SFB_FLAG_VD) ? 1 : 0;
+    cg += ((fl & SFB_FLAG_VD) && (fl & SFB_FLAG_VN)) ? 1 : 0;
+  }
+  cd = __reduce_add_sync(0xffffffffu, cd);
+  cg = __reduce_add_sync(0xffffffffu, cg);
+  __shared__ int sh[2][8];
+  if ((threadIdx.x & 31) == 0) {
+    sh[0][threadIdx.x >> 5] = cd;
+    sh[1][threadIdx.x >> 5] = cg;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int a0 = 0, a1 = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      a0 += sh[0][w];
+      a1 += sh[1][w];
+    }
+    out[blockIdx.x] = make_int2(a0, a1);
+  }
+}
+
+void launch_stride_counts(const FrameDev* frames, int n, int stride, int2* out, cudaStream_t s) {
+  if (n <= 0) return;
+  sfb_count_launch();
+  k_stride_counts<<<n, 256, 0, s>>>(frames, stride, out);
+}
+
 // ---------------------------------------------------------------------------
 // Fused dense pass.  For each (directed edge, pixel tile) item, at the current
 // poses, one thread per source pixel:
@@ -396,8 +437,9 @@ __global__ void __launch_bounds__(DENSE_THREADS, DENSE_BLOCKS_EFF) k_dense_fused
 #else
   __syncthreads();
 #endif
-  const int ord_ph = (Fi.n_valid_depth == 1) ? a.rd.apply_1 : a.rd.apply_n;
-  const int ord_ge = (Fi.n_valid_geo == 1) ? a.rd.apply_1 : a.rd.apply_n;
+  const int2 nsrc = src_counts(a, Fi, de.x);
+  const int ord_ph = (nsrc.x == 1) ? a.rd.apply_1 : a.rd.apply_n;
+  const int ord_ge = (nsrc.y == 1) ? a.rd.apply_1 : a.rd.apply_n;
   const int lane = threadIdx.x & 31;
   uint32_t* pmask = a.photo_mask + a.photo_off[it.x];
   uint16_t* gtgt = a.geo_tgt + a.geo_off[it.x];
@@ -1078,8 +1120,9 @@ __global__ void k_associate(DenseArgs a, int src, int dst, int kind, uint8_t* se
   const FrameDev Fj = a.frames[dst];
   __syncthreads();
   const int hw = Fi.w * Fi.h;
-  const int ord_ph = (Fi.n_valid_depth == 1) ? a.rd.apply_1 : a.rd.apply_n;
-  const int ord_ge = (Fi.n_valid_geo == 1) ? a.rd.apply_1 : a.rd.apply_n;
+  const int2 nsrc = src_counts(a, Fi, src);
+  const int ord_ph = (nsrc.x == 1) ? a.rd.apply_1 : a.rd.apply_n;
+  const int ord_ge = (nsrc.y == 1) ? a.rd.apply_1 : a.rd.apply_n;
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < hw; p += gridDim.x * blockDim.x) {
     const float4 P = Fi.P[p];
     const unsigned fl = __float_as_uint(P.w);
@@ -1087,7 +1130,6 @@ __global__ void k_associate(DenseArgs a, int src, int dst, int kind, uint8_t* se
     const bool ph = kind == 0 && sok && (fl & SFB_FLAG_VD);
     const bool ge = kind == 1 && sok && (fl & SFB_FLAG_VD) && (fl & SFB_FLAG_VN);
     const float4 N = ge ? Fi.N[p] : make_float4(0.f, 0.f, 0.f, 0.f);
-    // a single-pixel stride selection is not tracked here (m == 1 order)
     const AssocOut ao = associate_pixel(ec, Fj, P, N, ph, ge, ord_ph, ord_ge, a.rd, a.geo_dmax,
                                         a.geo_nmin);
     sel[p] = kind == 0 ? (uint8_t)ao.photo : (uint8_t)(ao.tgt >= 0);

@@ -248,6 +248,12 @@ inline size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 using namespace sfbh;
 
 struct sfb_ctx : Handle {
+  // Serialises every call that touches the frame-store slots or the shared
+  // per-context buffers / stream below (frames upload / release, problem
+  // creation from slots, dense_verify, build_cache, the dense PCG): distinct
+  // problems may be solved concurrently (reference solver.py:551-552), and
+  // they share this context.
+  std::recursive_mutex mu;
   int device = 0;
   int n_sm = 148;
   cudaStream_t stream = nullptr;

@@ -54,6 +54,9 @@ struct DenseArgs {
   int do_photo, do_geo;
   double geo_dmax, geo_nmin;
   int stride;
+  // per frame, valid_depth / geo pixel counts on the stride grid (stride > 1;
+  // the m == 1 NumPy rounding case of _source_pixel_data, solver.py:158-167)
+  const int2* stride_counts;
   int n_items;
 };
 
@@ -176,6 +179,7 @@ void sfb_count_launch(int n = 1);
 void launch_pack_batch(const PackArgs* args_dev, int n, int max_hw, int max_tiles, cudaStream_t s);
 void launch_sparse(const SparseArgs& a, cudaStream_t s);
 void launch_dense_linearize(const DenseArgs& a, cudaStream_t s);
+void launch_stride_counts(const FrameDev* frames, int n, int stride, int2* out, cudaStream_t s);
 void launch_dense_energy(const DenseArgs& a, double* item_e2, cudaStream_t s);
 void launch_edge_reduce2(const int* edge_item_ptr, const double* item_e2, double* edge_e2, int n_dir,
                          cudaStream_t s);

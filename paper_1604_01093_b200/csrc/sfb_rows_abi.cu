@@ -20,6 +20,7 @@ int sfb_host_free(void* ptr) {
 int sfb_frames_set_intensity(sfb_ctx* c, int32_t n, const int32_t* slots,
                              const float* const* intensity) {
   if (!c || n < 0 || (n > 0 && (!slots || !intensity))) return fail(c, SFB_E_ARG, "bad arguments");
+  std::lock_guard<std::recursive_mutex> lk(c->mu);
   CK(c, cudaSetDevice(c->device));
   for (int k = 0; k < n; ++k) {
     const int s = slots[k];
@@ -51,6 +52,7 @@ int sfb_dense_verify(sfb_ctx* c, int32_t n_items, const int32_t* src_slots,
     return fail(c, SFB_E_ARG, "null argument");
   for (int32_t o : {cfg->apply_n, cfg->apply_1, cfg->apply_nf, cfg->apply_1f})
     if (o < 0 || o > 5) return fail(c, SFB_E_ARG, "rounding code out of range");
+  std::lock_guard<std::recursive_mutex> lk(c->mu);
   CK(c, cudaSetDevice(c->device));
   std::vector<VerifyItem> items(n_items);
   int max_hw = 1;
@@ -118,6 +120,7 @@ int sfb_build_cache(sfb_ctx* c, int32_t n, int32_t width, int32_t height, int32_
   if (luma_order < 0 || luma_order > 5) return fail(c, SFB_E_ARG, "rounding code out of range");
   const int bw = width / low_width, bh = height / low_height;
   if (bw * bh > 64) return fail(c, SFB_E_ARG, "blocks of more than 64 samples are not supported");
+  std::lock_guard<std::recursive_mutex> lk(c->mu);
   CK(c, cudaSetDevice(c->device));
   cudaStream_t s = c->stream;
   const size_t HW = (size_t)width * height, hw = (size_t)low_width * low_height;

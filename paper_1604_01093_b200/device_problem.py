@@ -78,8 +78,11 @@ class DeviceProblem:
         self.lib = self.rt.lib
         self.n = n_frames
         slots = None
+        self._slots = None
         if caches_in_order is not None:
             slots = np.asarray(self.rt.slots_for(caches_in_order), dtype=np.int32)
+            self.rt.acquire(slots)
+            self._slots = slots
         self._caches = caches_in_order
         if set_frames is None:
             set_frames = np.zeros((0, 2), dtype=np.int32)
@@ -92,9 +95,15 @@ class DeviceProblem:
         pi = np.ascontiguousarray(pts_i if pts_i is not None else np.zeros((0, 3)), dtype=np.float64)
         pj = np.ascontiguousarray(pts_j if pts_j is not None else np.zeros((0, 3)), dtype=np.float64)
         h = C.c_void_p()
-        _abi.check(self.lib.sfb_problem_create(
-            self.rt.handle, n_frames, _abi.ptr(slots), n_sets, _abi.ptr(fi), _abi.ptr(fj),
-            _abi.ptr(off), _abi.ptr(pi), _abi.ptr(pj), C.byref(h)), self.rt.handle)
+        try:
+            _abi.check(self.lib.sfb_problem_create(
+                self.rt.handle, n_frames, _abi.ptr(slots), n_sets, _abi.ptr(fi), _abi.ptr(fj),
+                _abi.ptr(off), _abi.ptr(pi), _abi.ptr(pj), C.byref(h)), self.rt.handle)
+        except BaseException:
+            if self._slots is not None:
+                self.rt.release_users(self._slots)
+                self._slots = None
+            raise
         self.handle = h
         self.n_sets = n_sets
         self.n_corr = int(off[-1]) if n_sets else 0
@@ -104,13 +113,22 @@ class DeviceProblem:
     def attach_frames(self, caches_in_order, slots) -> None:
         """Frames for a problem created without them (uploaded meanwhile)."""
         slots = np.ascontiguousarray(slots, dtype=np.int32)
-        self._ck(self.lib.sfb_problem_attach_frames(self.handle, _abi.ptr(slots)))
+        self.rt.acquire(slots)
+        try:
+            self._ck(self.lib.sfb_problem_attach_frames(self.handle, _abi.ptr(slots)))
+        except BaseException:
+            self.rt.release_users(slots)
+            raise
+        self._slots = slots
         self._caches = caches_in_order
 
     def close(self):
         if getattr(self, "handle", None) is not None:
             self.lib.sfb_problem_destroy(self.handle)
             self.handle = None
+            if getattr(self, "_slots", None) is not None:
+                self.rt.release_users(self._slots)
+                self._slots = None
 
     def __del__(self):
         try:

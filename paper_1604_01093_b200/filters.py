@@ -106,10 +106,11 @@ def dense_verify_many(pairs, config: FilterConfig, error_max: float | None = Non
                             pr["apply_nf"], pr["apply_1f"])
     err = np.zeros(2 * n, dtype=np.float64)
     cnt = np.zeros(2 * n, dtype=np.int64)
-    _abi.check(rt.lib.sfb_dense_verify(rt.handle, 2 * n, _abi.ptr(src), _abi.ptr(dst),
-                                       _abi.ptr(R9), _abi.ptr(t3), _abi.ptr(flags),
-                                       _abi.C.byref(cfg), _abi.ptr(err), _abi.ptr(cnt)),
-               rt.handle)
+    with rt.using(src):  # no concurrent clear_frames() may release them mid-call
+        _abi.check(rt.lib.sfb_dense_verify(rt.handle, 2 * n, _abi.ptr(src), _abi.ptr(dst),
+                                           _abi.ptr(R9), _abi.ptr(t3), _abi.ptr(flags),
+                                           _abi.C.byref(cfg), _abi.ptr(err), _abi.ptr(cnt)),
+                   rt.handle)
     out = []
     for k, (ci, _, _) in enumerate(pairs):
         err_ij, err_ji = float(err[2 * k]), float(err[2 * k + 1])

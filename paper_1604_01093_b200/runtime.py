@@ -2,15 +2,22 @@
 
 A `CachedFrame` is immutable after construction (reference frames.py:8-9),
 so its planes are uploaded once per context and addressed by slot.  The
-store keys frames by object identity and holds a strong reference so an id
-cannot be recycled while its slot is alive; `clear_frames()` drops them.
+store keys frames by object identity and holds only a weak reference: when
+the caller drops a cache, its slot (and device block) is released as soon
+as no live device problem still uses it.  Problems register the slots they
+read (`acquire` / `release_users`); `clear_frames()` forgets every mapping
+and releases the slots nobody uses, deferring the rest to the last user.
+Caches that cannot be weakly referenced are held strongly until
+`clear_frames()`.
 """
 
 from __future__ import annotations
 
 import ctypes as C
 import os
+import contextlib
 import threading
+import weakref
 
 import numpy as np
 
@@ -61,12 +68,21 @@ class Runtime:
         pr = probe()
         r = _abi.Rounding(**{k: pr[k] for k, _ in _abi.Rounding._fields_})
         _abi.check(self.lib.sfb_ctx_set_rounding(h, C.byref(r)), h)
+        # id(cache) -> (slot, weakref to the cache, or the cache itself)
         self._frames: dict[int, tuple[int, object]] = {}
         self._with_intensity: set[int] = set()  # slots holding intensity_low
+        self._users: dict[int, int] = {}        # slot -> live users (problems, calls)
+        self._orphans: set[int] = set()         # unmapped slots waiting for their last user
+        self._dead: list = []                   # ids of collected caches (finalizer-appended)
         self._staging: dict = {}
         self._staging_addr: dict = {}
         self._staging_ptrs: list = []
-        self._lock = threading.Lock()
+        # RLock: a cache finalizer never takes it (it only appends to _dead),
+        # but slot bookkeeping may be re-entered from one call chain
+        self._lock = threading.RLock()
+        # held from stacking correspondence sets into the shared pinned
+        # staging until sfb_problem_create has copied them
+        self.stage_lock = threading.Lock()
 
     # -- frame store --------------------------------------------------------
     def slots_for(self, caches, on_submit=None) -> list[int]:
@@ -75,10 +91,11 @@ class Runtime:
         drops the GIL), or right away when nothing needs uploading."""
         try:
             with self._lock:
+                self._reap()
                 missing = []
                 seen = set()
                 for c in caches:
-                    if id(c) not in self._frames and id(c) not in seen:
+                    if self._lookup(c) is None and id(c) not in seen:
                         missing.append(c)
                         seen.add(id(c))
                 if missing:
@@ -104,7 +121,7 @@ class Runtime:
             _abi.check(self.lib.sfb_frames_upload(self.handle, n, descs.ctypes.data_as(
                 C.POINTER(_abi.FrameDesc)), _abi.ptr(slots)), self.handle)
             for c, s in zip(caches, slots):
-                self._frames[id(c)] = (int(s), c)
+                self._register(c, int(s))
             return
         keep = []
         dims = np.empty((n, 2), dtype=np.int32)
@@ -138,7 +155,7 @@ class Runtime:
         _abi.check(self.lib.sfb_frames_upload(self.handle, n, descs.ctypes.data_as(
             C.POINTER(_abi.FrameDesc)), _abi.ptr(slots)), self.handle)
         for c, s in zip(caches, slots):
-            self._frames[id(c)] = (int(s), c)
+            self._register(c, int(s))
         del keep
 
     def intensity_slots_for(self, caches) -> list[int]:
@@ -183,19 +200,89 @@ class Runtime:
         """Register caches whose planes were produced on the device
         (sfb_build_cache): already resident, intensity included."""
         with self._lock:
+            self._reap()
             for c, s in zip(caches, slots):
-                self._frames[id(c)] = (int(s), c)
+                self._register(c, int(s))
                 self._with_intensity.add(int(s))
 
-    def clear_frames(self) -> None:
-        with self._lock:
-            if not self._frames:
-                return
-            slots = np.array([s for s, _ in self._frames.values()], dtype=np.int32)
-            _abi.check(self.lib.sfb_frames_release(self.handle, len(slots), _abi.ptr(slots)),
+    # -- slot lifetime ----------------------------------------------------------
+    def _register(self, cache, slot: int) -> None:
+        try:
+            ref = weakref.ref(cache)
+            weakref.finalize(cache, self._dead.append, id(cache))
+        except TypeError:  # not weakly referenceable: held until clear_frames()
+            ref = cache
+        self._frames[id(cache)] = (slot, ref)
+
+    def _lookup(self, cache):
+        ent = self._frames.get(id(cache))
+        if ent is None:
+            return None
+        ref = ent[1]
+        alive = ref() if isinstance(ref, weakref.ref) else ref
+        if alive is not cache:  # a recycled id: the old cache is gone
+            self._forget(id(cache))
+            return None
+        return ent[0]
+
+    def _forget(self, key) -> None:
+        ent = self._frames.pop(key, None)
+        if ent is not None:
+            self._orphans.add(ent[0])
+
+    def _reap(self) -> None:
+        """Unmap collected caches; release unmapped slots nobody uses."""
+        while self._dead:
+            key = self._dead.pop()
+            ent = self._frames.get(key)
+            if ent is not None and isinstance(ent[1], weakref.ref) and ent[1]() is None:
+                self._forget(key)
+        free = [s for s in self._orphans if self._users.get(s, 0) == 0]
+        if free:
+            arr = np.array(sorted(free), dtype=np.int32)
+            _abi.check(self.lib.sfb_frames_release(self.handle, len(arr), _abi.ptr(arr)),
                        self.handle)
-            self._frames.clear()
-            self._with_intensity.clear()
+            self._orphans.difference_update(free)
+            self._with_intensity.difference_update(free)
+
+    def acquire(self, slots) -> None:
+        """Register a user (a device problem) of these slots."""
+        with self._lock:
+            for s in set(int(x) for x in slots):
+                self._users[s] = self._users.get(s, 0) + 1
+
+    def release_users(self, slots) -> None:
+        with self._lock:
+            for s in set(int(x) for x in slots):
+                n = self._users.get(s, 0) - 1
+                if n <= 0:
+                    self._users.pop(s, None)
+                else:
+                    self._users[s] = n
+            self._reap()
+
+    @contextlib.contextmanager
+    def using(self, slots):
+        """Keep the slots alive for the duration of one library call."""
+        self.acquire(slots)
+        try:
+            yield
+        finally:
+            self.release_users(slots)
+
+    def resident_frames(self) -> int:
+        """Slots currently held (mapped or awaiting their last user)."""
+        with self._lock:
+            self._reap()
+            return len(self._frames) + len(self._orphans)
+
+    def clear_frames(self) -> None:
+        """Forget every cache mapping; slots still used by live problems are
+        released when their last user closes."""
+        with self._lock:
+            for key in list(self._frames):
+                self._forget(key)
+            self._reap()
 
     def __del__(self):
         try:

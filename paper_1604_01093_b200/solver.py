@@ -700,10 +700,13 @@ class AlignmentProblem:
                 submitted.wait()
                 dp = None
                 try:
-                    # the sparse problem is built while the frames are in flight
-                    frames, off, pi, pj = _set_layout(self.corr_sets, index, rt)
-                    dp = DeviceProblem(len(self.frame_ids), None, frames, pi, pj, off,
-                                       device=self._device)
+                    # the sparse problem is built while the frames are in flight;
+                    # the stacked sets live in the runtime's shared pinned staging
+                    # until sfb_problem_create has copied them
+                    with rt.stage_lock:
+                        frames, off, pi, pj = _set_layout(self.corr_sets, index, rt)
+                        dp = DeviceProblem(len(self.frame_ids), None, frames, pi, pj, off,
+                                           device=self._device)
                 finally:
                     th.join()
                 try:
@@ -715,9 +718,13 @@ class AlignmentProblem:
                     raise
                 self._dp = dp
             else:
-                frames, off, pi, pj = _set_layout(self.corr_sets, index, runtime(self._device))
-                self._dp = DeviceProblem(len(self.frame_ids), cl, frames, pi, pj, off,
-                                         device=self._device)
+                rt = runtime(self._device)
+                if cl is not None:
+                    rt.slots_for(cl)  # upload outside the staging lock
+                with rt.stage_lock:
+                    frames, off, pi, pj = _set_layout(self.corr_sets, index, rt)
+                    self._dp = DeviceProblem(len(self.frame_ids), cl, frames, pi, pj, off,
+                                             device=self._device)
             if self._xch is not None:
                 self._dp.set_shard(self._xch.rank, self._xch.world)
         return self._dp
