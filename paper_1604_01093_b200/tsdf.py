@@ -14,13 +14,20 @@ Every voxel decision and every float32 accumulation reproduces the
 reference's NumPy arithmetic, so the volume is bit-identical (including the
 dict's insertion order and the DeintegrationMismatchError behaviour).
 
-`blocks` and `block()` return host snapshots: mutating their arrays does not
-write back (use `allocate` + `load_volume`-style imports to seed data).
+`blocks` is a live mapping view of the device volume, in the reference
+dict's insertion order: `blocks[coord]` fetches one block (cached until the
+next integrate / deintegrate / assignment), `blocks[coord] = VoxelBlock(...)`
+writes through to the device (how the reference's `load_volume` seeds a
+volume, tsdf.py:260-267), iteration yields coordinates, and `items()` /
+`values()` export the whole volume once.  Blocks handed out (`blocks[c]`,
+`block()`, `allocate()`) are read-only host copies: writing into their
+arrays raises instead of being silently lost.
 """
 
 from __future__ import annotations
 
 import ctypes as C
+from collections.abc import MutableMapping
 from dataclasses import dataclass
 
 import numpy as np
@@ -33,6 +40,7 @@ BLOCK_SIZE = 8
 BLOCK_VOXELS = BLOCK_SIZE ** 3
 
 __all__ = ["BLOCK_SIZE", "BLOCK_VOXELS", "DeintegrationMismatchError", "VoxelBlock", "TsdfVolume",
+           "BlockView",
            "default_truncation", "volumes_equal", "save_volume", "load_volume"]
 
 
@@ -92,30 +100,42 @@ class TsdfVolume:
         _abi.check(self._rt.lib.sfb_tsdf_count(self._h, C.byref(n)), self._h)
         return n.value
 
-    def block(self, coord):
-        """Snapshot of the block at `coord`, or None (tsdf.py:70-71)."""
-        c = np.asarray([int(x) for x in coord], dtype=np.int64)
+    def _key(self, coord) -> tuple:
+        return tuple(int(x) for x in coord)
+
+    def _fetch(self, key):
+        """One block from the device (read-only host copy), or None."""
+        c = np.asarray(key, dtype=np.int64)
         found = C.c_int32()
         b = VoxelBlock.empty()
         _abi.check(self._rt.lib.sfb_tsdf_get_block(self._h, _abi.ptr(c), C.byref(found),
                                                    _abi.ptr(b.weight), _abi.ptr(b.wdist),
                                                    _abi.ptr(b.wcolor)), self._h)
-        return b if found.value else None
+        return _readonly(b) if found.value else None
+
+    def block(self, coord):
+        """The block at `coord`, or None (tsdf.py:70-71)."""
+        return self.blocks.get(self._key(coord))
 
     def allocate(self, coord) -> VoxelBlock:
         """Existing block, or a new empty one appended to the dict (tsdf.py:73-80)."""
-        b = self.block(coord)
+        key = self._key(coord)
+        b = self.blocks.get(key)
         if b is not None:
             return b
-        c = np.asarray([[int(x) for x in coord]], dtype=np.int64)
-        e = VoxelBlock.empty()
-        _abi.check(self._rt.lib.sfb_tsdf_import(self._h, 1, _abi.ptr(c), _abi.ptr(e.weight),
-                                                _abi.ptr(e.wdist), _abi.ptr(e.wcolor)), self._h)
-        return e
+        self.blocks[key] = VoxelBlock.empty()
+        return self.blocks[key]
 
     @property
-    def blocks(self) -> dict:
-        """{coord: VoxelBlock} in the reference dict's insertion order (a snapshot)."""
+    def blocks(self) -> "BlockView":
+        """{coord: VoxelBlock} view in the reference dict's insertion order."""
+        view = getattr(self, "_view", None)
+        if view is None:
+            view = self._view = BlockView(self)
+        return view
+
+    def snapshot(self) -> dict:
+        """Every block at once, {coord: VoxelBlock} (one export)."""
         n = len(self)
         coords = np.zeros((n, 3), dtype=np.int64)
         w = np.zeros((n, BLOCK_VOXELS), dtype=np.float32)
@@ -123,6 +143,8 @@ class TsdfVolume:
         col = np.zeros((n, BLOCK_VOXELS, 3), dtype=np.float32)
         _abi.check(self._rt.lib.sfb_tsdf_export(self._h, n, _abi.ptr(coords), _abi.ptr(w),
                                                 _abi.ptr(d), _abi.ptr(col)), self._h)
+        for a in (w, d, col):
+            a.flags.writeable = False
         return {tuple(int(x) for x in coords[k]): VoxelBlock(w[k], d[k], col[k]) for k in range(n)}
 
     def _coords(self) -> list:
@@ -149,6 +171,7 @@ class TsdfVolume:
         self._apply(frame, intrinsics, pose, -1)
 
     def _apply(self, frame, intrinsics, pose, sign):
+        self._version = getattr(self, "_version", 0) + 1
         depth = np.ascontiguousarray(frame.depth, dtype=np.float32)
         color = np.ascontiguousarray(frame.color, dtype=np.uint8)
         H, W = depth.shape
@@ -208,6 +231,7 @@ class TsdfVolume:
         return sum(int(np.count_nonzero(b.weight)) for b in self.blocks.values())
 
     def _import(self, coords, weight, wdist, wcolor):
+        self._version = getattr(self, "_version", 0) + 1
         n = len(coords)
         c = np.ascontiguousarray(np.asarray(coords, dtype=np.int64).reshape(n, 3))
         w = np.ascontiguousarray(np.asarray(weight, dtype=np.float32).reshape(n, BLOCK_VOXELS))
@@ -217,10 +241,94 @@ class TsdfVolume:
                                                 _abi.ptr(col)), self._h)
 
 
+def _readonly(b: VoxelBlock) -> VoxelBlock:
+    for a in (b.weight, b.wdist, b.wcolor):
+        a.flags.writeable = False
+    return b
+
+
+class BlockView(MutableMapping):
+    """Live {coord: VoxelBlock} view of a device TsdfVolume (the reference's
+    `TsdfVolume.blocks` dict, tsdf.py:65)."""
+
+    def __init__(self, volume: TsdfVolume):
+        self._vol = volume
+        self._ver = None
+        self._cache = {}
+        self._order = None
+
+    def _fresh(self):
+        ver = getattr(self._vol, "_version", 0)
+        if ver != self._ver:
+            self._ver = ver
+            self._cache.clear()
+            self._order = None
+
+    def __getitem__(self, coord):
+        key = self._vol._key(coord)
+        self._fresh()
+        b = self._cache.get(key)
+        if b is None:
+            b = self._vol._fetch(key)
+            if b is None:
+                raise KeyError(key)
+            self._cache[key] = b
+        return b
+
+    def __setitem__(self, coord, block):
+        """Write one block through to the device (new keys append, as a dict)."""
+        self._vol._import([self._vol._key(coord)], [block.weight], [block.wdist], [block.wcolor])
+
+    def __delitem__(self, coord):
+        raise TypeError("device TsdfVolume blocks are removed by deintegrate() only")
+
+    def __iter__(self):
+        self._fresh()
+        if self._order is None:
+            self._order = self._vol._coords()
+        return iter(list(self._order))
+
+    def __len__(self):
+        return len(self._vol)
+
+    def __contains__(self, coord):
+        try:
+            self[coord]
+        except KeyError:
+            return False
+        return True
+
+    def _all(self) -> dict:
+        self._fresh()
+        snap = self._vol.snapshot()
+        self._cache.update(snap)
+        self._order = list(snap)
+        return snap
+
+    def items(self):
+        return self._all().items()
+
+    def values(self):
+        return self._all().values()
+
+    def copy(self) -> dict:
+        return dict(self._all())
+
+    def __repr__(self):
+        return f"<TsdfVolume.blocks: {len(self)} blocks>"
+
+
+def _blocks_dict(volume) -> dict:
+    """All blocks of a device volume (one export) or a reference volume's dict."""
+    if isinstance(volume, TsdfVolume):
+        return volume.snapshot()
+    return volume.blocks
+
+
 def volumes_equal(a, b, dist_tol: float = 1e-5) -> bool:
     """Equality over occupied voxels: weights exact, distances within tolerance
     (tsdf.py:223-240).  Works on this module's volumes and on reference ones."""
-    ba_all, bb_all = a.blocks, b.blocks
+    ba_all, bb_all = _blocks_dict(a), _blocks_dict(b)
     for coord in set(ba_all) | set(bb_all):
         ba, bb = ba_all.get(coord), bb_all.get(coord)
         wa = ba.weight if ba is not None else np.zeros(BLOCK_VOXELS, np.float32)
@@ -239,7 +347,7 @@ def volumes_equal(a, b, dist_tol: float = 1e-5) -> bool:
 
 def save_volume(path, volume: TsdfVolume):
     """Dump the sparse volume to a .npz archive, sorted block order (tsdf.py:243-257)."""
-    blocks = volume.blocks
+    blocks = _blocks_dict(volume)
     coords = sorted(blocks)
     np.savez_compressed(
         path, voxel_size=volume.voxel_size, truncation=volume.truncation,
@@ -256,6 +364,6 @@ def load_volume(path) -> TsdfVolume:
     """tsdf.py:260-267 (blocks inserted in the archive's order)."""
     data = np.load(path)
     volume = TsdfVolume(float(data["voxel_size"]), float(data["truncation"]))
-    if data["coords"].shape[0]:
+    if data["coords"].shape[0]:  # one batched write (the reference assigns block by block)
         volume._import(data["coords"], data["weight"], data["wdist"], data["wcolor"])
     return volume

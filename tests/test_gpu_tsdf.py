@@ -98,3 +98,32 @@ def test_tsdf_read_api_save_load_and_oracle(tmp_path):
     e = v2.allocate((10 ** 5, 3, -7))
     assert len(v2) == n + 1 and not e.weight.any()
     assert list(v2.blocks)[-1] == (10 ** 5, 3, -7)
+
+
+def test_tsdf_blocks_view_writes_through_and_is_read_only():
+    """`blocks` is a live view (single-block fetches, write-through
+    assignment, cache invalidated by integrate) and handed-out arrays raise on
+    writes instead of silently losing them."""
+    from paper_1604_01093_b200 import tsdf as T
+    v, _ = _run("vs20")
+    view = v.blocks
+    coords = list(view)
+    snap = v.snapshot()
+    assert coords == list(snap)
+    c = coords[len(coords) // 2]
+    b = view[c]
+    assert np.array_equal(b.weight, snap[c].weight) and np.array_equal(b.wcolor, snap[c].wcolor)
+    assert view[c] is b  # cached until the volume changes
+    with pytest.raises(ValueError):
+        b.weight[0] = 1.0
+    new = T.VoxelBlock(np.full(T.BLOCK_VOXELS, 2.0, np.float32), np.full(T.BLOCK_VOXELS, 0.5, np.float32),
+                       np.ones((T.BLOCK_VOXELS, 3), np.float32))
+    view[c] = new
+    got = v.blocks[c]
+    assert got is not b and np.array_equal(got.weight, new.weight) and np.array_equal(got.wdist, new.wdist)
+    assert list(v.blocks) == coords  # overwrite keeps the insertion order
+    view[(7, 7, 7777)] = new
+    assert list(v.blocks)[-1] == (7, 7, 7777) and (7, 7, 7777) in v.blocks
+    assert v.block((1, 2, 10 ** 6)) is None and (1, 2, 10 ** 6) not in v.blocks
+    with pytest.raises(TypeError):
+        del view[c]
