@@ -736,8 +736,8 @@ int sfb_frames_upload(sfb_ctx* c, int32_t n, const sfb_frame_desc* d, int32_t* s
     devs[k] = f;
   }
   const auto t_scan = std::chrono::steady_clock::now();
-  // pageable planes by DMA, one call each (cudaMemcpyBatchAsync crashed on
-  // pageable sources on the 580 driver)
+  // pageable planes by DMA, one cudaMemcpyAsync per plane (the batched copy
+  // API is not used)
   for (size_t q = 0; q < cdst.size(); ++q)
     CK(c, cudaMemcpyAsync(cdst[q], csrc[q], csz[q], cudaMemcpyHostToDevice, c->stream));
   if (!jobs.empty()) {
