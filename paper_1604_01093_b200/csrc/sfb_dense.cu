@@ -165,19 +165,6 @@ __device__ __forceinline__ void geo_lin_pixel(const EdgeCtx& e, double d0, doubl
   J[5] = m[2];
 }
 
-__device__ __forceinline__ void accum_row(double (&acc)[29], const double J[6], double res,
-                                          double s) {
-  double sJ[6];
-#pragma unroll
-  for (int k = 0; k < 6; ++k) sJ[k] = s * J[k];
-#pragma unroll
-  for (int r = 0; r < 6; ++r)
-#pragma unroll
-    for (int c = r; c < 6; ++c) acc[sym6(r, c)] = fma(sJ[r], J[c], acc[sym6(r, c)]);
-#pragma unroll
-  for (int k = 0; k < 6; ++k) acc[21 + k] = fma(sJ[k], res, acc[21 + k]);
-}
-
 __device__ __forceinline__ bool stride_ok(int p, int w, int stride) {
   if (stride <= 1) return true;
   const int y = p / w, x = p - y * w;
@@ -237,47 +224,20 @@ void launch_stride_counts(const FrameDev* frames, int n, int stride, int2* out, 
 //         identical poses, so both share the warp, the bilinear sample and
 //         the loads.
 // Association decisions need NumPy's exact rounding; the division in the
-// projection is replaced by a correctly-rounded reciprocal and the exact
-// IEEE quotient is recomputed only when the approximate pixel lies within
-// 1e-6 px of a decision boundary (bounds, or a .5 for np.round), where the
-// two could disagree (|u_approx - u| is ~1e-13 px).
-
-struct FusedCtx {
-  Xf rel;              // pose_j^-1 o pose_i, NumPy rounding
-  double Ri[9], ti[3]; // pose_i
-  double Rj[9], tj[3]; // pose_j
-  double back[12];     // pose_i^-1 o pose_j (R row-major, t)
-};
-
-__device__ __forceinline__ void load_fused_ctx(FusedCtx* e, const PoseDev& Pi, const PoseDev& Pj,
-                                               const Rounding& rd) {
-  e->rel = xf_relative_exact(Pi, Pj, rd);
-  for (int k = 0; k < 9; ++k) { e->Ri[k] = Pi.R[k]; e->Rj[k] = Pj.R[k]; }
-  for (int k = 0; k < 3; ++k) { e->ti[k] = Pi.t[k]; e->tj[k] = Pj.t[k]; }
-  double iR[9], it[3];
-  xf_inverse_plain(Pi.R, Pi.t, iR, it);
-  for (int r = 0; r < 3; ++r) {
-    for (int c = 0; c < 3; ++c)
-      e->back[r * 3 + c] = iR[r * 3 + 0] * Pj.R[0 * 3 + c] + iR[r * 3 + 1] * Pj.R[1 * 3 + c] +
-                           iR[r * 3 + 2] * Pj.R[2 * 3 + c];
-    e->back[9 + r] = iR[r * 3 + 0] * Pj.t[0] + iR[r * 3 + 1] * Pj.t[1] + iR[r * 3 + 2] * Pj.t[2] + it[r];
-  }
-}
-
-template <bool STD>
-__device__ __forceinline__ double dot3x(double a0, double a1, double a2, double b0, double b1,
-                                        double b2, int o) {
-  if (STD) return __fma_rn(a2, b2, __fma_rn(a1, b1, __dmul_rn(a0, b0)));
-  return dot3o(a0, a1, a2, b0, b1, b2, o);
-}
-
-// round-half-even for |x| < 2^51 on the FP64 pipe
-__device__ __forceinline__ double rint_magic(double x) {
-  const double M = 6755399441055744.0;  // 1.5 * 2^52
-  return __dsub_rn(__dadd_rn(x, M), M);
-}
-
-
+// projection is replaced by a Newton-refined reciprocal and the exact IEEE
+// quotient is recomputed only when the approximate pixel lies within 1e-6 px
+// of a decision boundary (bounds, or a .5 for np.round), where the two could
+// disagree (|u_approx - u| is ~1e-13 px).
+//
+// Everything after the decisions is evaluated in the target camera j, where
+// both dense Jacobians take the form J_i = M_j v (M_j = [[R_j, -[t_j]x R_j],
+// [0, -R_j]] per edge, applied once in k_edge_reduce):
+//   photo  v = [dq x q ; dq],  dq = d value / d q at q = rel d;
+//   geo    v = [t x n' ; -n'], n' = R_rel n, t = the frozen target point,
+//          residual n . (d - T_i^-1 T_j t) = n' . (q - t)  (R_rel orthonormal),
+// so the rotated normal and q - t of the association gate are reused.  The
+// photo rows are accumulated unscaled and the geo row pre-multiplied by
+// kappa = sqrt(s_geo / s_photo); k_edge_reduce applies the base scale.
 
 #define DENSE_MAX_TILES 1024
 
@@ -293,6 +253,28 @@ extern "C" int sfb_debug_dense_count(unsigned long long* out, int reset) {
   return (int)e;
 }
 #endif
+
+template <bool STD>
+__device__ __forceinline__ double dot3x(double a0, double a1, double a2, double b0, double b1,
+                                        double b2, int o) {
+  if (STD) return __fma_rn(a2, b2, __fma_rn(a1, b1, __dmul_rn(a0, b0)));
+  return dot3o(a0, a1, a2, b0, b1, b2, o);
+}
+
+// round-half-even for |x| < 2^51 on the FP64 pipe
+__device__ __forceinline__ double rint_magic(double x) {
+  const double M = 6755399441055744.0;  // 1.5 * 2^52
+  return __dsub_rn(__dadd_rn(x, M), M);
+}
+
+// 1/z for z > 0 (depths): MUFU seed (~2^-22) + one cubic Newton step, ~1 ulp
+__device__ __forceinline__ double rcp_depth(double z) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(z));
+  double e = fma(-z, r, 1.0);
+  e = fma(e, e, e);
+  return fma(r, e, r);
+}
 
 // Can any point of this tile's bounding sphere (moved by rel) project into
 // the target frustum widened to [-0.5, w-0.5] x [-0.5, h-0.5], z > 0?  The
@@ -315,18 +297,11 @@ __device__ __forceinline__ unsigned char tile_maybe_visible(const Xf& rel, const
   return 1;
 }
 
-#ifndef DENSE_TMEM
-#define DENSE_TMEM 1
-#endif
-#if DENSE_TMEM
 // Tensor-memory accumulators: the 27 H/g sums of each thread live in TMEM (54
 // 32-bit columns of its lane; warp w uses lanes 32(w%4).. and columns
 // 64(w/4)..), read-modify-written once per tile by the warp (tcgen05.ld/st,
-// warp-converged), so registers hold only the tile's Jacobian rows: 80
-// registers, 3 CTAs (24 warps) per SM instead of 128 registers and 2 CTAs
-// (6.61 -> 6.32 ms per launch at cfg4).  The per-entry FMA order (photo row
-// 0, photo row 1, geo row) is the register path's.  -DDENSE_TMEM=0 builds
-// the register-accumulator kernel.
+// warp-converged), so registers hold only the tile's Jacobian rows.  The
+// per-entry FMA order is photo row 0, photo row 1, geo row.
 #define TM_LD16(addr, u)                                                                        \
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" \
                : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]),      \
@@ -348,8 +323,6 @@ __device__ __forceinline__ void tm_set(uint32_t* u, int k, double v) {
   u[2 * k] = (uint32_t)__double2loint(v);
   u[2 * k + 1] = (uint32_t)__double2hiint(v);
 }
-// entry E of the 27 (21 packed H, then 6 g): photo rows 0, 1 then the geo row,
-// the order of the register path's accum_row calls (compile-time indices)
 __host__ __device__ constexpr int sym6_row(int e) {
   int r = 0;
   while (e >= 6 - r) { e -= 6 - r; ++r; }
@@ -360,61 +333,66 @@ __host__ __device__ constexpr int sym6_col(int e) {
   while (e >= 6 - r) { e -= 6 - r; ++r; }
   return e + r;
 }
+// entry E of the 27 (21 packed H, then 6 g)
 template <int E>
 __device__ __forceinline__ double tm_update(double acc, const double (&jp)[2][6],
                                             const double (&rp)[2], const double (&jg)[6],
-                                            double rg, double sp, double sg) {
+                                            double rg) {
   if constexpr (E < 21) {
     constexpr int r = sym6_row(E), c = sym6_col(E);
-    acc = fma(sp * jp[0][r], jp[0][c], acc);
-    acc = fma(sp * jp[1][r], jp[1][c], acc);
-    return fma(sg * jg[r], jg[c], acc);
+    acc = fma(jp[0][r], jp[0][c], acc);
+    acc = fma(jp[1][r], jp[1][c], acc);
+    return fma(jg[r], jg[c], acc);
   } else {
     constexpr int r = E - 21;
-    acc = fma(sp * jp[0][r], rp[0], acc);
-    acc = fma(sp * jp[1][r], rp[1], acc);
-    return fma(sg * jg[r], rg, acc);
+    acc = fma(jp[0][r], rp[0], acc);
+    acc = fma(jp[1][r], rp[1], acc);
+    return fma(jg[r], rg, acc);
   }
 }
 template <int Q>
 __device__ __forceinline__ void tm_chunk(uint32_t tm, const double (&jp)[2][6], const double (&rp)[2],
-                                         const double (&jg)[6], double rg, double sp, double sg) {
+                                         const double (&jg)[6], double rg) {
   uint32_t u[16];
   TM_LD16(tm + 16 * Q, u);
   tm_wait_ld();
-  tm_set(u, 0, tm_update<8 * Q + 0>(tm_d(u, 0), jp, rp, jg, rg, sp, sg));
-  tm_set(u, 1, tm_update<8 * Q + 1>(tm_d(u, 1), jp, rp, jg, rg, sp, sg));
-  tm_set(u, 2, tm_update<8 * Q + 2>(tm_d(u, 2), jp, rp, jg, rg, sp, sg));
+  tm_set(u, 0, tm_update<8 * Q + 0>(tm_d(u, 0), jp, rp, jg, rg));
+  tm_set(u, 1, tm_update<8 * Q + 1>(tm_d(u, 1), jp, rp, jg, rg));
+  tm_set(u, 2, tm_update<8 * Q + 2>(tm_d(u, 2), jp, rp, jg, rg));
   if constexpr (8 * Q + 3 < 27) {
-    tm_set(u, 3, tm_update<8 * Q + 3>(tm_d(u, 3), jp, rp, jg, rg, sp, sg));
-    tm_set(u, 4, tm_update<8 * Q + 4>(tm_d(u, 4), jp, rp, jg, rg, sp, sg));
-    tm_set(u, 5, tm_update<8 * Q + 5>(tm_d(u, 5), jp, rp, jg, rg, sp, sg));
-    tm_set(u, 6, tm_update<8 * Q + 6>(tm_d(u, 6), jp, rp, jg, rg, sp, sg));
-    tm_set(u, 7, tm_update<8 * Q + 7>(tm_d(u, 7), jp, rp, jg, rg, sp, sg));
+    tm_set(u, 3, tm_update<8 * Q + 3>(tm_d(u, 3), jp, rp, jg, rg));
+    tm_set(u, 4, tm_update<8 * Q + 4>(tm_d(u, 4), jp, rp, jg, rg));
+    tm_set(u, 5, tm_update<8 * Q + 5>(tm_d(u, 5), jp, rp, jg, rg));
+    tm_set(u, 6, tm_update<8 * Q + 6>(tm_d(u, 6), jp, rp, jg, rg));
+    tm_set(u, 7, tm_update<8 * Q + 7>(tm_d(u, 7), jp, rp, jg, rg));
   }
   TM_ST16(tm + 16 * Q, u);
 }
 #ifndef DENSE_TMEM_BLOCKS
 #define DENSE_TMEM_BLOCKS 3
 #endif
-#define DENSE_BLOCKS_EFF DENSE_TMEM_BLOCKS
-#else
-#define DENSE_BLOCKS_EFF DENSE_MIN_BLOCKS
-#endif
+
+// H / g base scale and the geo row factor of a linearisation
+__host__ __device__ inline void dense_scales(double s_photo, double s_geo, double* base,
+                                             double* kappa) {
+  if (s_photo > 0.0) {
+    *base = s_photo;
+    *kappa = sqrt(s_geo / s_photo);
+  } else {
+    *base = s_geo;
+    *kappa = 1.0;
+  }
+}
 
 template <bool STD, bool PREV>
-#ifndef DENSE_MIN_BLOCKS
-#define DENSE_MIN_BLOCKS 2
-#endif
-__global__ void __launch_bounds__(DENSE_THREADS, DENSE_BLOCKS_EFF) k_dense_fused(DenseArgs a) {
-  __shared__ FusedCtx ec;
+__global__ void __launch_bounds__(DENSE_THREADS, DENSE_TMEM_BLOCKS) k_dense_fused(DenseArgs a) {
+  __shared__ Xf rel;  // pose_j^-1 o pose_i, NumPy rounding
+  __shared__ uint32_t tm_base;
   const int4 it = a.items[blockIdx.x];
   const int2 de = a.dir_edges[it.x];
-  if (threadIdx.x == 0) load_fused_ctx(&ec, a.poses[de.x], a.poses[de.y], a.rd);
+  if (threadIdx.x == 0) rel = xf_relative_exact(a.poses[de.x], a.poses[de.y], a.rd);
   const FrameDev Fi = a.frames[de.x];
   const FrameDev Fj = a.frames[de.y];
-#if DENSE_TMEM
-  __shared__ uint32_t tm_base;
   if ((threadIdx.x >> 5) == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(
                      (uint32_t)__cvta_generic_to_shared(&tm_base)));
@@ -423,7 +401,7 @@ __global__ void __launch_bounds__(DENSE_THREADS, DENSE_BLOCKS_EFF) k_dense_fused
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
-  // warp w: lanes 32*(w%4).., columns 64*(w/4) .. +56
+  // warp w: lanes 32*(w%4).., columns 64*(w/4) .. +54
   const uint32_t tm = tm_base + ((uint32_t)(((threadIdx.x >> 5) & 3) * 32) << 16) +
                       (uint32_t)((threadIdx.x >> 7) * 64);
   {
@@ -434,9 +412,6 @@ __global__ void __launch_bounds__(DENSE_THREADS, DENSE_BLOCKS_EFF) k_dense_fused
     for (int q = 0; q < 4; ++q) TM_ST16(tm + 16 * q, z);
     tm_wait_st();
   }
-#else
-  __syncthreads();
-#endif
   const int2 nsrc = src_counts(a, Fi, de.x);
   const int ord_ph = (nsrc.x == 1) ? a.rd.apply_1 : a.rd.apply_n;
   const int ord_ge = (nsrc.y == 1) ? a.rd.apply_1 : a.rd.apply_n;
@@ -447,6 +422,8 @@ __global__ void __launch_bounds__(DENSE_THREADS, DENSE_BLOCKS_EFF) k_dense_fused
   const uint16_t* gtgt_prev = PREV ? a.geo_tgt_prev + a.geo_off[it.x] : nullptr;
   const double wm1 = (double)(Fj.w - 1), hm1 = (double)(Fj.h - 1);
   const double dwj = (double)Fj.w, dhj = (double)Fj.h;
+  double base_scale, kappa;
+  dense_scales(a.s_photo, a.s_geo, &base_scale, &kappa);
 
   // Tile culling: a 16x16 source tile whose bounding sphere lies outside
   // the target frustum widened to the geo rounding bounds [-0.5, w-0.5]
@@ -458,19 +435,13 @@ __global__ void __launch_bounds__(DENSE_THREADS, DENSE_BLOCKS_EFF) k_dense_fused
   __shared__ unsigned char tile_state[DENSE_MAX_TILES];
   const int toff = (int)(a.geo_off[it.x] >> 8);  // this edge's first tile flag
   for (int t = it.y + threadIdx.x; t < it.z; t += blockDim.x) {
-    unsigned char s = tile_maybe_visible(ec.rel, Fi.tiles[t], Fj);
+    unsigned char s = tile_maybe_visible(rel, Fi.tiles[t], Fj);
     if (PREV && a.tile_any_prev[toff + t]) s |= 2;
     tile_state[t - it.y] = s;
   }
   __syncthreads();
 
-#if DENSE_TMEM
-  double acc27 = 0.0, acc28 = 0.0;
-#else
-  double acc[29];
-#pragma unroll
-  for (int k = 0; k < 29; ++k) acc[k] = 0.0;
-#endif
+  double acc27 = 0.0, acc28 = 0.0;    // photo / geo energy at association
   double eprev_p = 0.0, eprev_g = 0.0;
 
   // pixels in tile-major order: slot m = tile * 256 + threadIdx.x (the frozen
@@ -487,11 +458,8 @@ __global__ void __launch_bounds__(DENSE_THREADS, DENSE_BLOCKS_EFF) k_dense_fused
     const int p = y * Fi.w + x;           // pixel
     const int m = t * 256 + threadIdx.x;  // slot
     float4 P = make_float4(0.f, 0.f, 0.f, 0.f);
-    unsigned fl = 0;
-    if (live) {
-      P = __ldg(&Fi.P[p]);
-      fl = __float_as_uint(P.w);
-    }
+    if (live) P = __ldg(&Fi.P[p]);
+    const unsigned fl = __float_as_uint(P.w);
     const bool sok = vis && live && stride_ok(p, Fi.w, a.stride);
     const bool ph = a.do_photo && sok && (fl & SFB_FLAG_VD);
     const bool ge = a.do_geo && sok && (fl & SFB_FLAG_VD) && (fl & SFB_FLAG_VN);
@@ -501,27 +469,30 @@ __global__ void __launch_bounds__(DENSE_THREADS, DENSE_BLOCKS_EFF) k_dense_fused
       if (a.prev_photo) pph = (pmask_prev[m >> 5] >> (m & 31)) & 1u;
       if (a.prev_geo) ptg = gtgt_prev[m];
     }
+    const bool pge = PREV && ptg != 0xFFFF;
     bool ph_in = false;
     int tgt = -1;
+    // camera-j point, reciprocal depth, approximate pixel
     double q0 = 0.0, q1 = 0.0, q2 = 1.0, rz = 1.0, ua = 0.0, va = 0.0;
+    // accumulation inputs; zero on lanes without an association
+    double dq0[2] = {0.0, 0.0}, dq1[2] = {0.0, 0.0}, rp[2] = {0.0, 0.0};
+    double nj0 = 0.0, nj1 = 0.0, nj2 = 0.0, t0 = 0.0, t1 = 0.0, t2 = 0.0, rg = 0.0;
     const double d0 = P.x, d1 = P.y, d2 = P.z;
-    float4 N = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (ph || ge || pph) {
+    if (ph || ge || pph || pge) {
       const int ord = ph ? ord_ph : ord_ge;
-      const bool generic = !STD || (ord != 0);
       // warped = relative.apply(points): NumPy rounding
-      if (!generic) {
-        q0 = __dadd_rn(dot3x<true>(d0, d1, d2, ec.rel.R[0], ec.rel.R[1], ec.rel.R[2], 0), ec.rel.t[0]);
-        q1 = __dadd_rn(dot3x<true>(d0, d1, d2, ec.rel.R[3], ec.rel.R[4], ec.rel.R[5], 0), ec.rel.t[1]);
-        q2 = __dadd_rn(dot3x<true>(d0, d1, d2, ec.rel.R[6], ec.rel.R[7], ec.rel.R[8], 0), ec.rel.t[2]);
+      if (STD && ord == 0) {
+        q0 = __dadd_rn(dot3x<true>(d0, d1, d2, rel.R[0], rel.R[1], rel.R[2], 0), rel.t[0]);
+        q1 = __dadd_rn(dot3x<true>(d0, d1, d2, rel.R[3], rel.R[4], rel.R[5], 0), rel.t[1]);
+        q2 = __dadd_rn(dot3x<true>(d0, d1, d2, rel.R[6], rel.R[7], rel.R[8], 0), rel.t[2]);
       } else {
-        q0 = __dadd_rn(dot3o(d0, d1, d2, ec.rel.R[0], ec.rel.R[1], ec.rel.R[2], ord), ec.rel.t[0]);
-        q1 = __dadd_rn(dot3o(d0, d1, d2, ec.rel.R[3], ec.rel.R[4], ec.rel.R[5], ord), ec.rel.t[1]);
-        q2 = __dadd_rn(dot3o(d0, d1, d2, ec.rel.R[6], ec.rel.R[7], ec.rel.R[8], ord), ec.rel.t[2]);
+        q0 = __dadd_rn(dot3o(d0, d1, d2, rel.R[0], rel.R[1], rel.R[2], ord), rel.t[0]);
+        q1 = __dadd_rn(dot3o(d0, d1, d2, rel.R[3], rel.R[4], rel.R[5], ord), rel.t[1]);
+        q2 = __dadd_rn(dot3o(d0, d1, d2, rel.R[6], rel.R[7], rel.R[8], ord), rel.t[2]);
       }
       const bool front = q2 > 0.0;
       const double z = front ? q2 : 1.0;
-      rz = __drcp_rn(z);
+      rz = rcp_depth(z);
       const double tu = __dmul_rn(Fj.fx, q0), tv = __dmul_rn(Fj.fy, q1);
       ua = fma(tu, rz, Fj.cx);
       va = fma(tv, rz, Fj.cy);
@@ -538,33 +509,46 @@ __global__ void __launch_bounds__(DENSE_THREADS, DENSE_BLOCKS_EFF) k_dense_fused
           ph_in = front && u >= 0.0 && u <= wm1 && v >= 0.0 && v <= hm1;
         }
       }
-      if (ge) {
-        double u = ua, v = va;
+      if (ge || pge) {
         if (ph && ord_ge != ord_ph) {  // m == 1 special case: re-derive the warp
-          q0 = __dadd_rn(dot3o(d0, d1, d2, ec.rel.R[0], ec.rel.R[1], ec.rel.R[2], ord_ge), ec.rel.t[0]);
-          q1 = __dadd_rn(dot3o(d0, d1, d2, ec.rel.R[3], ec.rel.R[4], ec.rel.R[5], ord_ge), ec.rel.t[1]);
-          q2 = __dadd_rn(dot3o(d0, d1, d2, ec.rel.R[6], ec.rel.R[7], ec.rel.R[8], ord_ge), ec.rel.t[2]);
+          q0 = __dadd_rn(dot3o(d0, d1, d2, rel.R[0], rel.R[1], rel.R[2], ord_ge), rel.t[0]);
+          q1 = __dadd_rn(dot3o(d0, d1, d2, rel.R[3], rel.R[4], rel.R[5], ord_ge), rel.t[1]);
+          q2 = __dadd_rn(dot3o(d0, d1, d2, rel.R[6], rel.R[7], rel.R[8], ord_ge), rel.t[2]);
         }
-        const bool fr = q2 > 0.0;
-        const double zz = fr ? q2 : 1.0;
-        const bool finite_uv = fabs(u) < 1e9 && fabs(v) < 1e9;
-        double xr = finite_uv ? rint_magic(u) : 0.0, yr = finite_uv ? rint_magic(v) : 0.0;
-        // np.round ties: recompute the exact quotient when within 1e-6 px of a .5
-        if (finite_uv && (fabs(u - xr) > 0.5 - 1e-6 || fabs(v - yr) > 0.5 - 1e-6 ||
-                          (ph && ord_ge != ord_ph))) {
-          u = __dadd_rn(__ddiv_rn(__dmul_rn(Fj.fx, q0), zz), Fj.cx);
-          v = __dadd_rn(__ddiv_rn(__dmul_rn(Fj.fy, q1), zz), Fj.cy);
-          xr = rint_magic(u);
-          yr = rint_magic(v);
+        // normal_dot operand: relative.rotate(normals), NumPy rounding
+        const float4 N = __ldg(&Fi.N[p]);
+        const double n0 = N.x, n1 = N.y, n2 = N.z;
+        double nr0, nr1, nr2;
+        if (STD && ord_ge == 0) {
+          nr0 = dot3x<true>(n0, n1, n2, rel.R[0], rel.R[1], rel.R[2], 0);
+          nr1 = dot3x<true>(n0, n1, n2, rel.R[3], rel.R[4], rel.R[5], 0);
+          nr2 = dot3x<true>(n0, n1, n2, rel.R[6], rel.R[7], rel.R[8], 0);
+        } else {
+          nr0 = dot3o(n0, n1, n2, rel.R[0], rel.R[1], rel.R[2], ord_ge);
+          nr1 = dot3o(n0, n1, n2, rel.R[3], rel.R[4], rel.R[5], ord_ge);
+          nr2 = dot3o(n0, n1, n2, rel.R[6], rel.R[7], rel.R[8], ord_ge);
         }
-        if (fr && finite_uv) {
-          if (xr >= 0.0 && xr < dwj && yr >= 0.0 && yr < dhj) {
+        double r_new = 0.0;
+        if (ge) {
+          double u = ua, v = va;
+          const bool fr = q2 > 0.0;
+          const double zz = fr ? q2 : 1.0;
+          const bool finite_uv = fabs(u) < 1e9 && fabs(v) < 1e9;
+          double xr = finite_uv ? rint_magic(u) : 0.0, yr = finite_uv ? rint_magic(v) : 0.0;
+          // np.round ties: recompute the exact quotient when within 1e-6 px of a .5
+          if (finite_uv && (fabs(u - xr) > 0.5 - 1e-6 || fabs(v - yr) > 0.5 - 1e-6 ||
+                            (ph && ord_ge != ord_ph))) {
+            u = __dadd_rn(__ddiv_rn(__dmul_rn(Fj.fx, q0), zz), Fj.cx);
+            v = __dadd_rn(__ddiv_rn(__dmul_rn(Fj.fy, q1), zz), Fj.cy);
+            xr = rint_magic(u);
+            yr = rint_magic(v);
+          }
+          if (fr && finite_uv && xr >= 0.0 && xr < dwj && yr >= 0.0 && yr < dhj) {
             const int ti = __double2loint(__dadd_rn(yr, 6755399441055744.0)) * Fj.w +
                            __double2loint(__dadd_rn(xr, 6755399441055744.0));
             const float4 PT = __ldg(&Fj.P[ti]);
             const unsigned tf = __float_as_uint(PT.w);
             if ((tf & (SFB_FLAG_VD | SFB_FLAG_VN)) == (SFB_FLAG_VD | SFB_FLAG_VN)) {
-              N = __ldg(&Fi.N[p]);
               const float4 NT = __ldg(&Fj.N[ti]);
               const double x0 = __dsub_rn(q0, (double)PT.x);
               const double x1 = __dsub_rn(q1, (double)PT.y);
@@ -575,22 +559,33 @@ __global__ void __launch_bounds__(DENSE_THREADS, DENSE_BLOCKS_EFF) k_dense_fused
               const double dm2 = a.geo_dmax * a.geo_dmax;
               const double dist = s2 < dm2 * (1.0 - 1e-12) ? 0.0
                                   : (s2 > dm2 * (1.0 + 1e-12) ? a.geo_dmax : __dsqrt_rn(s2));
-              const double n0 = N.x, n1 = N.y, n2 = N.z;
-              double nr0, nr1, nr2;
-              if (STD && ord_ge == 0) {
-                nr0 = dot3x<true>(n0, n1, n2, ec.rel.R[0], ec.rel.R[1], ec.rel.R[2], 0);
-                nr1 = dot3x<true>(n0, n1, n2, ec.rel.R[3], ec.rel.R[4], ec.rel.R[5], 0);
-                nr2 = dot3x<true>(n0, n1, n2, ec.rel.R[6], ec.rel.R[7], ec.rel.R[8], 0);
-              } else {
-                nr0 = dot3o(n0, n1, n2, ec.rel.R[0], ec.rel.R[1], ec.rel.R[2], ord_ge);
-                nr1 = dot3o(n0, n1, n2, ec.rel.R[3], ec.rel.R[4], ec.rel.R[5], ord_ge);
-                nr2 = dot3o(n0, n1, n2, ec.rel.R[6], ec.rel.R[7], ec.rel.R[8], ord_ge);
-              }
+              // normal_dot = np.sum(rotated * target_normals, axis=1)
               const double nd = __dadd_rn(__dadd_rn(__dmul_rn(nr0, (double)NT.x),
                                                     __dmul_rn(nr1, (double)NT.y)),
                                           __dmul_rn(nr2, (double)NT.z));
-              if (dist < a.geo_dmax && nd > a.geo_nmin) tgt = ti;
+              if (dist < a.geo_dmax && nd > a.geo_nmin) {
+                tgt = ti;
+                r_new = nr0 * x0 + nr1 * x1 + nr2 * x2;  // geo_linearize residual
+                acc28 += r_new * r_new;
+                rg = kappa * r_new;
+                nj0 = kappa * nr0;
+                nj1 = kappa * nr1;
+                nj2 = kappa * nr2;
+                t0 = PT.x;
+                t1 = PT.y;
+                t2 = PT.z;
+              }
             }
+          }
+        }
+        if (PREV && pge) {
+          if (ptg == tgt) {
+            eprev_g += r_new * r_new;  // same frozen target at the same poses
+          } else {
+            const float4 PT = __ldg(&Fj.P[ptg]);
+            const double r = nr0 * (q0 - (double)PT.x) + nr1 * (q1 - (double)PT.y) +
+                             nr2 * (q2 - (double)PT.z);
+            eprev_g += r * r;
           }
         }
       }
@@ -624,120 +619,51 @@ __global__ void __launch_bounds__(DENSE_THREADS, DENSE_BLOCKS_EFF) k_dense_fused
     if (__ballot_sync(0xffffffffu, ph_in || tgt >= 0) && lane == 0)
       tile_state[t - it.y] = (unsigned char)(st | 4u);
 
-#if DENSE_TMEM
-    double jp[2][6], rp[2] = {0.0, 0.0}, jg[6], rg = 0.0;
-#pragma unroll
-    for (int k = 0; k < 6; ++k) jp[0][k] = jp[1][k] = jg[k] = 0.0;
-#endif
     // ---- photometric: one bilinear sample serves the frozen energy and J
     if (ph_in || pph) {
       double val[2], ddx[2], ddy[2];
-      // (the F2I-floor form issues the tap loads sooner than bilinear_fast's
-      // FP64 rint chain: 6.71 vs 6.83 ms per launch at cfg4)
       bilinear_grad2(Fj, ua, va, val, ddx, ddy);
       const float2 ref = __ldg(&Fi.G[p]);
       const double r0 = (double)ref.x - val[0], r1 = (double)ref.y - val[1];
       const double e2 = r0 * r0 + r1 * r1;
       if (PREV && pph) eprev_p += e2;
       if (ph_in) {
-        // J_i = M_j v with M_j = [[R_j, -[t_j]x R_j], [0, -R_j]] (per edge) and
-        // v = [dq x q ; dq] in camera-j coordinates (dq = d value / d q):
-        // accumulate v v^T here, apply M_j once per edge (k_edge_reduce).
-#if DENSE_TMEM
         acc27 += e2;
         const double a_ = Fj.fx * rz, b_ = Fj.fy * rz;
+        dq0[0] = ddx[0] * a_;
+        dq0[1] = ddx[1] * a_;
+        dq1[0] = ddy[0] * b_;
+        dq1[1] = ddy[1] * b_;
         rp[0] = r0;
         rp[1] = r1;
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const double dq0 = ddx[c] * a_, dq1 = ddy[c] * b_;
-          const double dq2 = -(dq0 * q0 + dq1 * q1) * rz;
-          jp[c][0] = dq1 * q2 - dq2 * q1;
-          jp[c][1] = dq2 * q0 - dq0 * q2;
-          jp[c][2] = dq0 * q1 - dq1 * q0;
-          jp[c][3] = dq0;
-          jp[c][4] = dq1;
-          jp[c][5] = dq2;
-        }
-      }
-#else
-        acc[27] += e2;
-        const double a_ = Fj.fx * rz, b_ = Fj.fy * rz;
-        const double res[2] = {r0, r1};
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const double dq0 = ddx[c] * a_, dq1 = ddy[c] * b_;
-          const double dq2 = -(dq0 * q0 + dq1 * q1) * rz;
-          const double v[6] = {dq1 * q2 - dq2 * q1, dq2 * q0 - dq0 * q2, dq0 * q1 - dq1 * q0,
-                               dq0, dq1, dq2};
-          accum_row(acc, v, res[c], a.s_photo);
-        }
-      }
-#endif
-    }
-    // ---- point-to-plane: new association and/or frozen target
-    if (tgt >= 0 || (PREV && ptg != 0xFFFF)) {
-      if (tgt < 0) N = __ldg(&Fi.N[p]);
-      const double n0 = N.x, n1 = N.y, n2 = N.z;
-      double r_new = 0.0;
-      if (tgt >= 0) {
-        const float4 PT = __ldg(&Fj.P[tgt]);  // (L1 hit; keeping the association's copy
-                                               // live costs more in registers)
-        const double t0 = PT.x, t1 = PT.y, t2 = PT.z;
-        const double m0 = ec.back[0] * t0 + ec.back[1] * t1 + ec.back[2] * t2 + ec.back[9];
-        const double m1 = ec.back[3] * t0 + ec.back[4] * t1 + ec.back[5] * t2 + ec.back[10];
-        const double m2 = ec.back[6] * t0 + ec.back[7] * t1 + ec.back[8] * t2 + ec.back[11];
-        const double r = n0 * (d0 - m0) + n1 * (d1 - m1) + n2 * (d2 - m2);
-        r_new = r;
-        // J_i = M_j v, v = [p_t x n_j ; -n_j], n_j = R_j^T R_i n = rel.R n
-        const double nj0 = ec.rel.R[0] * n0 + ec.rel.R[1] * n1 + ec.rel.R[2] * n2;
-        const double nj1 = ec.rel.R[3] * n0 + ec.rel.R[4] * n1 + ec.rel.R[5] * n2;
-        const double nj2 = ec.rel.R[6] * n0 + ec.rel.R[7] * n1 + ec.rel.R[8] * n2;
-#if DENSE_TMEM
-        jg[0] = t1 * nj2 - t2 * nj1;
-        jg[1] = t2 * nj0 - t0 * nj2;
-        jg[2] = t0 * nj1 - t1 * nj0;
-        jg[3] = -nj0;
-        jg[4] = -nj1;
-        jg[5] = -nj2;
-        rg = r;
-        acc28 += r * r;
-#else
-        const double v[6] = {t1 * nj2 - t2 * nj1, t2 * nj0 - t0 * nj2, t0 * nj1 - t1 * nj0,
-                             -nj0, -nj1, -nj2};
-        accum_row(acc, v, r, a.s_geo);
-        acc[28] += r * r;
-#endif
-      }
-      if (PREV && ptg != 0xFFFF) {
-        if (ptg == tgt) {
-          // the previous pass froze the same target: same residual at these poses
-          eprev_g += r_new * r_new;
-        } else {
-          const float4 PT = __ldg(&Fj.P[ptg]);
-          const double t0 = PT.x, t1 = PT.y, t2 = PT.z;
-          const double m0 = ec.back[0] * t0 + ec.back[1] * t1 + ec.back[2] * t2 + ec.back[9];
-          const double m1 = ec.back[3] * t0 + ec.back[4] * t1 + ec.back[5] * t2 + ec.back[10];
-          const double m2 = ec.back[6] * t0 + ec.back[7] * t1 + ec.back[8] * t2 + ec.back[11];
-          const double r = n0 * (d0 - m0) + n1 * (d1 - m1) + n2 * (d2 - m2);
-          eprev_g += r * r;
-        }
       }
     }
-#if DENSE_TMEM
-    __syncwarp();
     if (__any_sync(0xffffffffu, ph_in || tgt >= 0)) {
-      const double sp = a.s_photo, sg = a.s_geo;
-      tm_chunk<0>(tm, jp, rp, jg, rg, sp, sg);
-      tm_chunk<1>(tm, jp, rp, jg, rg, sp, sg);
-      tm_chunk<2>(tm, jp, rp, jg, rg, sp, sg);
-      tm_chunk<3>(tm, jp, rp, jg, rg, sp, sg);
+      double jp[2][6], jg[6];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const double dq2 = -(dq0[c] * q0 + dq1[c] * q1) * rz;
+        jp[c][0] = dq1[c] * q2 - dq2 * q1;
+        jp[c][1] = dq2 * q0 - dq0[c] * q2;
+        jp[c][2] = dq0[c] * q1 - dq1[c] * q0;
+        jp[c][3] = dq0[c];
+        jp[c][4] = dq1[c];
+        jp[c][5] = dq2;
+      }
+      jg[0] = t1 * nj2 - t2 * nj1;
+      jg[1] = t2 * nj0 - t0 * nj2;
+      jg[2] = t0 * nj1 - t1 * nj0;
+      jg[3] = -nj0;
+      jg[4] = -nj1;
+      jg[5] = -nj2;
+      tm_chunk<0>(tm, jp, rp, jg, rg);
+      tm_chunk<1>(tm, jp, rp, jg, rg);
+      tm_chunk<2>(tm, jp, rp, jg, rg);
+      tm_chunk<3>(tm, jp, rp, jg, rg);
       tm_wait_st();
     }
-#endif
   }
-#if DENSE_TMEM
-  double acc[29];
+  double acc[31];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     uint32_t u[16];
@@ -745,33 +671,22 @@ __global__ void __launch_bounds__(DENSE_THREADS, DENSE_BLOCKS_EFF) k_dense_fused
     tm_wait_ld();
 #pragma unroll
     for (int k = 0; k < 8; ++k)
-      if (8 * q + k < 27) acc[8 * q + k] = tm_d(u, k);
+      if (8 * q + k < 27) acc[8 * q + k] = base_scale * tm_d(u, k);
   }
   acc[27] = acc27;
   acc[28] = acc28;
-#endif
   double* out = a.item_out + (int64_t)blockIdx.x * SFB_ITEM_STRIDE;
-  if (PREV) {
-    double tail[31];
-#pragma unroll
-    for (int k = 0; k < 29; ++k) tail[k] = acc[k];
-    tail[29] = eprev_p;
-    tail[30] = eprev_g;
-    block_reduce_store<31>(tail, out);
-  } else {
-    block_reduce_store<29>(acc, out);
-    if (threadIdx.x == 0) { out[29] = 0.0; out[30] = 0.0; }
-  }
+  acc[29] = eprev_p;  // zero without PREV
+  acc[30] = eprev_g;
+  block_reduce_store<31>(acc, out);
   // (block_reduce_store synchronised the CTA: tile_state bit2 is final)
   for (int t = it.y + threadIdx.x; t < it.z; t += blockDim.x)
     a.tile_any[toff + t] = (tile_state[t - it.y] & 4u) ? 1 : 0;
-#if DENSE_TMEM
   // every warp's last TMEM read completed (wait::ld) before block_reduce_store's barrier
   if ((threadIdx.x >> 5) == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tm_base));
   }
-#endif
 }
 
 void launch_dense_linearize(const DenseArgs& a, cudaStream_t s) {
