@@ -254,13 +254,6 @@ extern "C" int sfb_debug_dense_count(unsigned long long* out, int reset) {
 }
 #endif
 
-template <bool STD>
-__device__ __forceinline__ double dot3x(double a0, double a1, double a2, double b0, double b1,
-                                        double b2, int o) {
-  if (STD) return __fma_rn(a2, b2, __fma_rn(a1, b1, __dmul_rn(a0, b0)));
-  return dot3o(a0, a1, a2, b0, b1, b2, o);
-}
-
 // round-half-even for |x| < 2^51 on the FP64 pipe
 __device__ __forceinline__ double rint_magic(double x) {
   const double M = 6755399441055744.0;  // 1.5 * 2^52
@@ -384,7 +377,248 @@ __host__ __device__ inline void dense_scales(double s_photo, double s_geo, doubl
   }
 }
 
-template <bool STD, bool PREV>
+// Loop-invariant state of one (directed edge, tile range) item.
+struct TileCtx {
+  const float4* Pi;
+  const float4* Ni;
+  const float2* Gi;
+  int wi, hi, tiles_x;
+  int ord_ph, ord_ge;   // NumPy apply rounding orders (generic path)
+  double wm1, hm1, dwj, dhj;
+  double kappa;
+  uint32_t* pmask;
+  uint16_t* gtgt;
+  const uint32_t* pmask_prev;
+  const uint16_t* gtgt_prev;
+  uint32_t tm;
+};
+
+// exact 3-term dot in NumPy's order: FAST = the forward FMA chain
+template <bool FAST>
+__device__ __forceinline__ double dotx(double a0, double a1, double a2, double b0, double b1,
+                                       double b2, int o) {
+  if (FAST) return __fma_rn(a2, b2, __fma_rn(a1, b1, __dmul_rn(a0, b0)));
+  return dot3o(a0, a1, a2, b0, b1, b2, o);
+}
+
+// One 16x16 source tile of an item: the warp's 32 pixels are evaluated
+// branch-free (every lane computes with clamped indices, results are
+// selected by the lane's predicates), so all gathers of a pixel issue as
+// soon as their addresses are known; sections no lane of the warp needs are
+// skipped warp-uniformly.  Rare exact-rounding fallbacks stay divergent.
+template <bool PREV, bool FAST>
+__device__ __forceinline__ void dense_tile(const DenseArgs& a, const TileCtx& c, const Xf& rel,
+                                           const FrameDev& Fj, int t, int tx, int ty, unsigned st,
+                                           unsigned char* tstate, double& acc27, double& acc28,
+                                           double& eprev_p, double& eprev_g) {
+  const int lane = threadIdx.x & 31;
+  const bool vis = st & 1u;
+  const bool prev_here = PREV && (st & 2u);
+  const int x = tx * SFB_TILE + (threadIdx.x & (SFB_TILE - 1));
+  const int y = ty * SFB_TILE + (threadIdx.x / SFB_TILE);
+  const bool live = x < c.wi && y < c.hi;
+  const int p = live ? y * c.wi + x : 0;  // pixel (0: safe index)
+  const int m = t * 256 + threadIdx.x;    // slot
+  const float4 P = __ldg(&c.Pi[p]);
+  const unsigned fl = live ? __float_as_uint(P.w) : 0u;
+  const bool sok = vis && stride_ok(p, c.wi, a.stride);
+  const bool ph = a.do_photo && sok && (fl & SFB_FLAG_VD);
+  const bool ge = a.do_geo && sok && (fl & SFB_FLAG_VD) && (fl & SFB_FLAG_VN);
+  bool pph = false;
+  int ptg = 0xFFFF;
+  if (prev_here) {
+    const uint32_t w = c.pmask_prev[m >> 5];
+    const int g = c.gtgt_prev[m];
+    if (live) {
+      pph = a.prev_photo && ((w >> (m & 31)) & 1u);
+      ptg = a.prev_geo ? g : 0xFFFF;
+    }
+  }
+  const bool pge = PREV && ptg != 0xFFFF;
+  const bool any_ph = __any_sync(0xffffffffu, ph || pph);
+  const bool any_ge = __any_sync(0xffffffffu, ge || pge);
+  if (!(any_ph || any_ge)) {
+    if (a.do_photo && lane == 0) c.pmask[m >> 5] = 0u;
+    if (a.do_geo) c.gtgt[m] = 0xFFFF;
+    return;
+  }
+  const double d0 = P.x, d1 = P.y, d2 = P.z;
+  const int ord = FAST ? 0 : (ph ? c.ord_ph : c.ord_ge);
+  // warped = relative.apply(points): NumPy rounding
+  double q0 = __dadd_rn(dotx<FAST>(d0, d1, d2, rel.R[0], rel.R[1], rel.R[2], ord), rel.t[0]);
+  double q1 = __dadd_rn(dotx<FAST>(d0, d1, d2, rel.R[3], rel.R[4], rel.R[5], ord), rel.t[1]);
+  double q2 = __dadd_rn(dotx<FAST>(d0, d1, d2, rel.R[6], rel.R[7], rel.R[8], ord), rel.t[2]);
+  bool front = q2 > 0.0;
+  double z = front ? q2 : 1.0;
+  const double rz = rcp_depth(z);
+  const double tu = __dmul_rn(Fj.fx, q0), tv = __dmul_rn(Fj.fy, q1);
+  const double ua = fma(tu, rz, Fj.cx);
+  const double va = fma(tv, rz, Fj.cy);
+  // associate_photo: decide with a 1e-6 px guard band, exact quotient inside it
+  bool ph_in = false;
+  {
+    const double E = 1e-6;
+    const bool in_c = ua > E && ua < c.wm1 - E && va > E && va < c.hm1 - E;
+    const bool out_c = ua < -E || ua > c.wm1 + E || va < -E || va > c.hm1 + E;
+    ph_in = ph && front && in_c;
+    if (ph && !(in_c | out_c)) {
+      const double u = __dadd_rn(__ddiv_rn(tu, z), Fj.cx);
+      const double v = __dadd_rn(__ddiv_rn(tv, z), Fj.cy);
+      ph_in = front && u >= 0.0 && u <= c.wm1 && v >= 0.0 && v <= c.hm1;
+    }
+  }
+  // ---- associate_geo (+ the frozen geo energy of the previous pass)
+  int tgt = -1;
+  double nj0 = 0.0, nj1 = 0.0, nj2 = 0.0, t0 = 0.0, t1 = 0.0, t2 = 0.0, rg = 0.0;
+  if (any_ge) {
+    if (!FAST && ph && c.ord_ge != c.ord_ph) {  // m == 1 special case: re-derive the warp
+      q0 = __dadd_rn(dot3o(d0, d1, d2, rel.R[0], rel.R[1], rel.R[2], c.ord_ge), rel.t[0]);
+      q1 = __dadd_rn(dot3o(d0, d1, d2, rel.R[3], rel.R[4], rel.R[5], c.ord_ge), rel.t[1]);
+      q2 = __dadd_rn(dot3o(d0, d1, d2, rel.R[6], rel.R[7], rel.R[8], c.ord_ge), rel.t[2]);
+      front = q2 > 0.0;
+      z = front ? q2 : 1.0;
+    }
+    double u = ua, v = va;
+    const bool finite_uv = fabs(u) < 1e9 && fabs(v) < 1e9;
+    double xr = finite_uv ? rint_magic(u) : 0.0, yr = finite_uv ? rint_magic(v) : 0.0;
+    // np.round ties: recompute the exact quotient when within 1e-6 px of a .5
+    if (ge && finite_uv &&
+        (fabs(u - xr) > 0.5 - 1e-6 || fabs(v - yr) > 0.5 - 1e-6 || (!FAST && ph && c.ord_ge != c.ord_ph))) {
+      u = __dadd_rn(__ddiv_rn(__dmul_rn(Fj.fx, q0), z), Fj.cx);
+      v = __dadd_rn(__ddiv_rn(__dmul_rn(Fj.fy, q1), z), Fj.cy);
+      xr = rint_magic(u);
+      yr = rint_magic(v);
+    }
+    const bool inside = ge && front && finite_uv && xr >= 0.0 && xr < c.dwj && yr >= 0.0 && yr < c.dhj;
+    const int ti = inside ? __double2loint(__dadd_rn(yr, 6755399441055744.0)) * Fj.w +
+                                __double2loint(__dadd_rn(xr, 6755399441055744.0))
+                          : 0;
+    const float4 PT = __ldg(&Fj.P[ti]);
+    const float4 NT = __ldg(&Fj.N[ti]);
+    const float4 N = __ldg(&c.Ni[p]);
+    const float4 PP = __ldg(&Fj.P[pge ? ptg : ti]);
+    // normal_dot operand: relative.rotate(normals), NumPy rounding
+    const int og = FAST ? 0 : c.ord_ge;
+    const double n0 = N.x, n1 = N.y, n2 = N.z;
+    const double nr0 = dotx<FAST>(n0, n1, n2, rel.R[0], rel.R[1], rel.R[2], og);
+    const double nr1 = dotx<FAST>(n0, n1, n2, rel.R[3], rel.R[4], rel.R[5], og);
+    const double nr2 = dotx<FAST>(n0, n1, n2, rel.R[6], rel.R[7], rel.R[8], og);
+    const unsigned tf = __float_as_uint(PT.w);
+    const bool tvalid = inside && (tf & (SFB_FLAG_VD | SFB_FLAG_VN)) == (SFB_FLAG_VD | SFB_FLAG_VN);
+    const double x0 = __dsub_rn(q0, (double)PT.x);
+    const double x1 = __dsub_rn(q1, (double)PT.y);
+    const double x2 = __dsub_rn(q2, (double)PT.z);
+    // norm < dmax: compare squares; correctly rounded sqrt only near the gate
+    const double s2 = __dadd_rn(__dadd_rn(__dmul_rn(x0, x0), __dmul_rn(x1, x1)), __dmul_rn(x2, x2));
+    const double dm2 = a.geo_dmax * a.geo_dmax;
+    bool near = s2 < dm2 * (1.0 - 1e-12);
+    if (tvalid && !near && !(s2 > dm2 * (1.0 + 1e-12))) near = __dsqrt_rn(s2) < a.geo_dmax;
+    // normal_dot = np.sum(rotated * target_normals, axis=1)
+    const double nd = __dadd_rn(__dadd_rn(__dmul_rn(nr0, (double)NT.x), __dmul_rn(nr1, (double)NT.y)),
+                                __dmul_rn(nr2, (double)NT.z));
+    const bool gok = tvalid && near && nd > a.geo_nmin;
+    tgt = gok ? ti : -1;
+    const double r_new = nr0 * x0 + nr1 * x1 + nr2 * x2;  // geo_linearize residual
+    const double e_new = r_new * r_new;
+    acc28 += gok ? e_new : 0.0;
+    if (PREV) {
+      const double rpv = nr0 * (q0 - (double)PP.x) + nr1 * (q1 - (double)PP.y) + nr2 * (q2 - (double)PP.z);
+      eprev_g += pge ? (ptg == tgt ? e_new : rpv * rpv) : 0.0;
+    }
+    const double kg = gok ? c.kappa : 0.0;
+    rg = kg * r_new;
+    nj0 = kg * nr0;
+    nj1 = kg * nr1;
+    nj2 = kg * nr2;
+    t0 = PT.x;
+    t1 = PT.y;
+    t2 = PT.z;
+  }
+  // frozen sets (tile-major slots)
+  const unsigned pword = __ballot_sync(0xffffffffu, ph_in);
+  if (a.do_photo && lane == 0) c.pmask[m >> 5] = pword;
+  if (a.do_geo) c.gtgt[m] = tgt >= 0 ? (uint16_t)tgt : (uint16_t)0xFFFF;
+  const bool any_new = __any_sync(0xffffffffu, ph_in || tgt >= 0);
+  // every warp that freezes an association in this tile stores the same
+  // byte (bits 0-1 are constant after the barrier): no read-modify-write
+  if (any_new && lane == 0) tstate[0] = (unsigned char)(st | 4u);
+#ifdef DENSE_COUNT
+  {
+    const unsigned b0 = __ballot_sync(0xffffffffu, live && vis);
+    const unsigned b1 = __ballot_sync(0xffffffffu, ph);
+    const unsigned b3 = __ballot_sync(0xffffffffu, ge);
+    const unsigned b4 = __ballot_sync(0xffffffffu, tgt >= 0);
+    const unsigned b5 = __ballot_sync(0xffffffffu, live);
+    if (lane == 0) {
+      atomicAdd(&g_dense_count[0], (unsigned long long)__popc(b0));
+      atomicAdd(&g_dense_count[1], (unsigned long long)__popc(b1));
+      atomicAdd(&g_dense_count[2], (unsigned long long)__popc(pword));
+      atomicAdd(&g_dense_count[3], (unsigned long long)__popc(b3));
+      atomicAdd(&g_dense_count[4], (unsigned long long)__popc(b4));
+      atomicAdd(&g_dense_count[5], (unsigned long long)__popc(b5));
+      atomicAdd(&g_dense_count[6], 32ull);
+    }
+  }
+#endif
+  // ---- photometric: one bilinear sample serves the frozen energy and J
+  double dq0[2] = {0.0, 0.0}, dq1[2] = {0.0, 0.0}, rp[2] = {0.0, 0.0};
+  if (any_ph) {
+    double val[2], ddx[2], ddy[2];
+    bilinear_grad2(Fj, ua, va, val, ddx, ddy);
+    const float2 ref = __ldg(&c.Gi[p]);
+    const double r0 = (double)ref.x - val[0], r1 = (double)ref.y - val[1];
+    const double e2 = r0 * r0 + r1 * r1;
+    if (PREV) eprev_p += pph ? e2 : 0.0;
+    acc27 += ph_in ? e2 : 0.0;
+    const double a_ = ph_in ? Fj.fx * rz : 0.0, b_ = ph_in ? Fj.fy * rz : 0.0;
+    dq0[0] = ddx[0] * a_;
+    dq0[1] = ddx[1] * a_;
+    dq1[0] = ddy[0] * b_;
+    dq1[1] = ddy[1] * b_;
+    rp[0] = ph_in ? r0 : 0.0;
+    rp[1] = ph_in ? r1 : 0.0;
+  }
+  if (any_new) {
+    double jp[2][6], jg[6];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const double dq2 = -(dq0[k] * q0 + dq1[k] * q1) * rz;
+      jp[k][0] = dq1[k] * q2 - dq2 * q1;
+      jp[k][1] = dq2 * q0 - dq0[k] * q2;
+      jp[k][2] = dq0[k] * q1 - dq1[k] * q0;
+      jp[k][3] = dq0[k];
+      jp[k][4] = dq1[k];
+      jp[k][5] = dq2;
+    }
+    jg[0] = t1 * nj2 - t2 * nj1;
+    jg[1] = t2 * nj0 - t0 * nj2;
+    jg[2] = t0 * nj1 - t1 * nj0;
+    jg[3] = -nj0;
+    jg[4] = -nj1;
+    jg[5] = -nj2;
+    tm_chunk<0>(c.tm, jp, rp, jg, rg);
+    tm_chunk<1>(c.tm, jp, rp, jg, rg);
+    tm_chunk<2>(c.tm, jp, rp, jg, rg);
+    tm_chunk<3>(c.tm, jp, rp, jg, rg);
+    tm_wait_st();
+  }
+}
+
+template <bool PREV, bool FAST>
+__device__ __forceinline__ void dense_tiles(const DenseArgs& a, const TileCtx& c, const Xf& rel,
+                                            const FrameDev& Fj, int4 it, unsigned char* tile_state,
+                                            double& acc27, double& acc28, double& eprev_p,
+                                            double& eprev_g) {
+  int tx = it.y % c.tiles_x, ty = it.y / c.tiles_x;
+  for (int t = it.y; t < it.z; ++t, (++tx == c.tiles_x ? (tx = 0, ++ty) : 0)) {
+    const unsigned st = tile_state[t - it.y];
+    if (!(st & 3u)) continue;  // nothing to associate, nothing frozen
+    dense_tile<PREV, FAST>(a, c, rel, Fj, t, tx, ty, st, &tile_state[t - it.y], acc27, acc28,
+                           eprev_p, eprev_g);
+  }
+}
+
+template <bool PREV>
 __global__ void __launch_bounds__(DENSE_THREADS, DENSE_TMEM_BLOCKS) k_dense_fused(DenseArgs a) {
   __shared__ Xf rel;  // pose_j^-1 o pose_i, NumPy rounding
   __shared__ uint32_t tm_base;
@@ -401,29 +635,37 @@ __global__ void __launch_bounds__(DENSE_THREADS, DENSE_TMEM_BLOCKS) k_dense_fuse
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
+  TileCtx c;
   // warp w: lanes 32*(w%4).., columns 64*(w/4) .. +54
-  const uint32_t tm = tm_base + ((uint32_t)(((threadIdx.x >> 5) & 3) * 32) << 16) +
-                      (uint32_t)((threadIdx.x >> 7) * 64);
+  c.tm = tm_base + ((uint32_t)(((threadIdx.x >> 5) & 3) * 32) << 16) +
+         (uint32_t)((threadIdx.x >> 7) * 64);
   {
     uint32_t z[16];
 #pragma unroll
     for (int k = 0; k < 16; ++k) z[k] = 0u;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) TM_ST16(tm + 16 * q, z);
+    for (int q = 0; q < 4; ++q) TM_ST16(c.tm + 16 * q, z);
     tm_wait_st();
   }
   const int2 nsrc = src_counts(a, Fi, de.x);
-  const int ord_ph = (nsrc.x == 1) ? a.rd.apply_1 : a.rd.apply_n;
-  const int ord_ge = (nsrc.y == 1) ? a.rd.apply_1 : a.rd.apply_n;
-  const int lane = threadIdx.x & 31;
-  uint32_t* pmask = a.photo_mask + a.photo_off[it.x];
-  uint16_t* gtgt = a.geo_tgt + a.geo_off[it.x];
-  const uint32_t* pmask_prev = PREV ? a.photo_mask_prev + a.photo_off[it.x] : nullptr;
-  const uint16_t* gtgt_prev = PREV ? a.geo_tgt_prev + a.geo_off[it.x] : nullptr;
-  const double wm1 = (double)(Fj.w - 1), hm1 = (double)(Fj.h - 1);
-  const double dwj = (double)Fj.w, dhj = (double)Fj.h;
-  double base_scale, kappa;
-  dense_scales(a.s_photo, a.s_geo, &base_scale, &kappa);
+  c.ord_ph = (nsrc.x == 1) ? a.rd.apply_1 : a.rd.apply_n;
+  c.ord_ge = (nsrc.y == 1) ? a.rd.apply_1 : a.rd.apply_n;
+  c.Pi = Fi.P;
+  c.Ni = Fi.N;
+  c.Gi = Fi.G;
+  c.wi = Fi.w;
+  c.hi = Fi.h;
+  c.tiles_x = Fi.tiles_x;
+  c.pmask = a.photo_mask + a.photo_off[it.x];
+  c.gtgt = a.geo_tgt + a.geo_off[it.x];
+  c.pmask_prev = PREV ? a.photo_mask_prev + a.photo_off[it.x] : nullptr;
+  c.gtgt_prev = PREV ? a.geo_tgt_prev + a.geo_off[it.x] : nullptr;
+  c.wm1 = (double)(Fj.w - 1);
+  c.hm1 = (double)(Fj.h - 1);
+  c.dwj = (double)Fj.w;
+  c.dhj = (double)Fj.h;
+  double base_scale;
+  dense_scales(a.s_photo, a.s_geo, &base_scale, &c.kappa);
 
   // Tile culling: a 16x16 source tile whose bounding sphere lies outside
   // the target frustum widened to the geo rounding bounds [-0.5, w-0.5]
@@ -441,233 +683,20 @@ __global__ void __launch_bounds__(DENSE_THREADS, DENSE_TMEM_BLOCKS) k_dense_fuse
   }
   __syncthreads();
 
-  double acc27 = 0.0, acc28 = 0.0;    // photo / geo energy at association
+  double acc27 = 0.0, acc28 = 0.0;  // photo / geo energy at association
   double eprev_p = 0.0, eprev_g = 0.0;
-
   // pixels in tile-major order: slot m = tile * 256 + threadIdx.x (the frozen
   // association buffers use the same slots; a warp covers 16x2 pixels)
-  int tx = it.y % Fi.tiles_x, ty = it.y / Fi.tiles_x;
-  for (int t = it.y; t < it.z; ++t, (++tx == Fi.tiles_x ? (tx = 0, ++ty) : 0)) {
-    const unsigned st = tile_state[t - it.y];
-    if (!(st & 3u)) continue;  // nothing to associate, nothing frozen
-    const bool vis = st & 1u;
-    const bool prev_here = PREV && (st & 2u);
-    const int x = tx * SFB_TILE + (threadIdx.x & (SFB_TILE - 1));
-    const int y = ty * SFB_TILE + (threadIdx.x / SFB_TILE);
-    const bool live = x < Fi.w && y < Fi.h;
-    const int p = y * Fi.w + x;           // pixel
-    const int m = t * 256 + threadIdx.x;  // slot
-    float4 P = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (live) P = __ldg(&Fi.P[p]);
-    const unsigned fl = __float_as_uint(P.w);
-    const bool sok = vis && live && stride_ok(p, Fi.w, a.stride);
-    const bool ph = a.do_photo && sok && (fl & SFB_FLAG_VD);
-    const bool ge = a.do_geo && sok && (fl & SFB_FLAG_VD) && (fl & SFB_FLAG_VN);
-    bool pph = false;
-    int ptg = 0xFFFF;
-    if (prev_here && live) {
-      if (a.prev_photo) pph = (pmask_prev[m >> 5] >> (m & 31)) & 1u;
-      if (a.prev_geo) ptg = gtgt_prev[m];
-    }
-    const bool pge = PREV && ptg != 0xFFFF;
-    bool ph_in = false;
-    int tgt = -1;
-    // camera-j point, reciprocal depth, approximate pixel
-    double q0 = 0.0, q1 = 0.0, q2 = 1.0, rz = 1.0, ua = 0.0, va = 0.0;
-    // accumulation inputs; zero on lanes without an association
-    double dq0[2] = {0.0, 0.0}, dq1[2] = {0.0, 0.0}, rp[2] = {0.0, 0.0};
-    double nj0 = 0.0, nj1 = 0.0, nj2 = 0.0, t0 = 0.0, t1 = 0.0, t2 = 0.0, rg = 0.0;
-    const double d0 = P.x, d1 = P.y, d2 = P.z;
-    if (ph || ge || pph || pge) {
-      const int ord = ph ? ord_ph : ord_ge;
-      // warped = relative.apply(points): NumPy rounding
-      if (STD && ord == 0) {
-        q0 = __dadd_rn(dot3x<true>(d0, d1, d2, rel.R[0], rel.R[1], rel.R[2], 0), rel.t[0]);
-        q1 = __dadd_rn(dot3x<true>(d0, d1, d2, rel.R[3], rel.R[4], rel.R[5], 0), rel.t[1]);
-        q2 = __dadd_rn(dot3x<true>(d0, d1, d2, rel.R[6], rel.R[7], rel.R[8], 0), rel.t[2]);
-      } else {
-        q0 = __dadd_rn(dot3o(d0, d1, d2, rel.R[0], rel.R[1], rel.R[2], ord), rel.t[0]);
-        q1 = __dadd_rn(dot3o(d0, d1, d2, rel.R[3], rel.R[4], rel.R[5], ord), rel.t[1]);
-        q2 = __dadd_rn(dot3o(d0, d1, d2, rel.R[6], rel.R[7], rel.R[8], ord), rel.t[2]);
-      }
-      const bool front = q2 > 0.0;
-      const double z = front ? q2 : 1.0;
-      rz = rcp_depth(z);
-      const double tu = __dmul_rn(Fj.fx, q0), tv = __dmul_rn(Fj.fy, q1);
-      ua = fma(tu, rz, Fj.cx);
-      va = fma(tv, rz, Fj.cy);
-      if (ph) {
-        // decide with a 1e-6 px guard band; exact IEEE quotient only inside it
-        const double E = 1e-6;
-        const bool in_c = ua > E && ua < wm1 - E && va > E && va < hm1 - E;
-        const bool out_c = ua < -E || ua > wm1 + E || va < -E || va > hm1 + E;
-        if (in_c | out_c) {
-          ph_in = front && in_c;
-        } else {
-          const double u = __dadd_rn(__ddiv_rn(tu, z), Fj.cx);
-          const double v = __dadd_rn(__ddiv_rn(tv, z), Fj.cy);
-          ph_in = front && u >= 0.0 && u <= wm1 && v >= 0.0 && v <= hm1;
-        }
-      }
-      if (ge || pge) {
-        if (ph && ord_ge != ord_ph) {  // m == 1 special case: re-derive the warp
-          q0 = __dadd_rn(dot3o(d0, d1, d2, rel.R[0], rel.R[1], rel.R[2], ord_ge), rel.t[0]);
-          q1 = __dadd_rn(dot3o(d0, d1, d2, rel.R[3], rel.R[4], rel.R[5], ord_ge), rel.t[1]);
-          q2 = __dadd_rn(dot3o(d0, d1, d2, rel.R[6], rel.R[7], rel.R[8], ord_ge), rel.t[2]);
-        }
-        // normal_dot operand: relative.rotate(normals), NumPy rounding
-        const float4 N = __ldg(&Fi.N[p]);
-        const double n0 = N.x, n1 = N.y, n2 = N.z;
-        double nr0, nr1, nr2;
-        if (STD && ord_ge == 0) {
-          nr0 = dot3x<true>(n0, n1, n2, rel.R[0], rel.R[1], rel.R[2], 0);
-          nr1 = dot3x<true>(n0, n1, n2, rel.R[3], rel.R[4], rel.R[5], 0);
-          nr2 = dot3x<true>(n0, n1, n2, rel.R[6], rel.R[7], rel.R[8], 0);
-        } else {
-          nr0 = dot3o(n0, n1, n2, rel.R[0], rel.R[1], rel.R[2], ord_ge);
-          nr1 = dot3o(n0, n1, n2, rel.R[3], rel.R[4], rel.R[5], ord_ge);
-          nr2 = dot3o(n0, n1, n2, rel.R[6], rel.R[7], rel.R[8], ord_ge);
-        }
-        double r_new = 0.0;
-        if (ge) {
-          double u = ua, v = va;
-          const bool fr = q2 > 0.0;
-          const double zz = fr ? q2 : 1.0;
-          const bool finite_uv = fabs(u) < 1e9 && fabs(v) < 1e9;
-          double xr = finite_uv ? rint_magic(u) : 0.0, yr = finite_uv ? rint_magic(v) : 0.0;
-          // np.round ties: recompute the exact quotient when within 1e-6 px of a .5
-          if (finite_uv && (fabs(u - xr) > 0.5 - 1e-6 || fabs(v - yr) > 0.5 - 1e-6 ||
-                            (ph && ord_ge != ord_ph))) {
-            u = __dadd_rn(__ddiv_rn(__dmul_rn(Fj.fx, q0), zz), Fj.cx);
-            v = __dadd_rn(__ddiv_rn(__dmul_rn(Fj.fy, q1), zz), Fj.cy);
-            xr = rint_magic(u);
-            yr = rint_magic(v);
-          }
-          if (fr && finite_uv && xr >= 0.0 && xr < dwj && yr >= 0.0 && yr < dhj) {
-            const int ti = __double2loint(__dadd_rn(yr, 6755399441055744.0)) * Fj.w +
-                           __double2loint(__dadd_rn(xr, 6755399441055744.0));
-            const float4 PT = __ldg(&Fj.P[ti]);
-            const unsigned tf = __float_as_uint(PT.w);
-            if ((tf & (SFB_FLAG_VD | SFB_FLAG_VN)) == (SFB_FLAG_VD | SFB_FLAG_VN)) {
-              const float4 NT = __ldg(&Fj.N[ti]);
-              const double x0 = __dsub_rn(q0, (double)PT.x);
-              const double x1 = __dsub_rn(q1, (double)PT.y);
-              const double x2 = __dsub_rn(q2, (double)PT.z);
-              // norm < dmax: compare squares; correctly rounded sqrt only near the gate
-              const double s2 = __dadd_rn(__dadd_rn(__dmul_rn(x0, x0), __dmul_rn(x1, x1)),
-                                          __dmul_rn(x2, x2));
-              const double dm2 = a.geo_dmax * a.geo_dmax;
-              const double dist = s2 < dm2 * (1.0 - 1e-12) ? 0.0
-                                  : (s2 > dm2 * (1.0 + 1e-12) ? a.geo_dmax : __dsqrt_rn(s2));
-              // normal_dot = np.sum(rotated * target_normals, axis=1)
-              const double nd = __dadd_rn(__dadd_rn(__dmul_rn(nr0, (double)NT.x),
-                                                    __dmul_rn(nr1, (double)NT.y)),
-                                          __dmul_rn(nr2, (double)NT.z));
-              if (dist < a.geo_dmax && nd > a.geo_nmin) {
-                tgt = ti;
-                r_new = nr0 * x0 + nr1 * x1 + nr2 * x2;  // geo_linearize residual
-                acc28 += r_new * r_new;
-                rg = kappa * r_new;
-                nj0 = kappa * nr0;
-                nj1 = kappa * nr1;
-                nj2 = kappa * nr2;
-                t0 = PT.x;
-                t1 = PT.y;
-                t2 = PT.z;
-              }
-            }
-          }
-        }
-        if (PREV && pge) {
-          if (ptg == tgt) {
-            eprev_g += r_new * r_new;  // same frozen target at the same poses
-          } else {
-            const float4 PT = __ldg(&Fj.P[ptg]);
-            const double r = nr0 * (q0 - (double)PT.x) + nr1 * (q1 - (double)PT.y) +
-                             nr2 * (q2 - (double)PT.z);
-            eprev_g += r * r;
-          }
-        }
-      }
-    }
-    if (a.do_photo) {
-      const unsigned word = __ballot_sync(0xffffffffu, ph_in);
-      if (lane == 0) pmask[m >> 5] = word;
-    }
-#ifdef DENSE_COUNT
-    {
-      const unsigned b0 = __ballot_sync(0xffffffffu, live && vis);
-      const unsigned b1 = __ballot_sync(0xffffffffu, ph);
-      const unsigned b2 = __ballot_sync(0xffffffffu, ph_in);
-      const unsigned b3 = __ballot_sync(0xffffffffu, ge);
-      const unsigned b4 = __ballot_sync(0xffffffffu, tgt >= 0);
-      const unsigned b5 = __ballot_sync(0xffffffffu, live && (st & 3u));
-      if (lane == 0) {
-        atomicAdd(&g_dense_count[0], (unsigned long long)__popc(b0));
-        atomicAdd(&g_dense_count[1], (unsigned long long)__popc(b1));
-        atomicAdd(&g_dense_count[2], (unsigned long long)__popc(b2));
-        atomicAdd(&g_dense_count[3], (unsigned long long)__popc(b3));
-        atomicAdd(&g_dense_count[4], (unsigned long long)__popc(b4));
-        atomicAdd(&g_dense_count[5], (unsigned long long)__popc(b5));
-        atomicAdd(&g_dense_count[6], 32ull);
-      }
-    }
-#endif
-    if (a.do_geo) gtgt[m] = tgt >= 0 ? (uint16_t)tgt : (uint16_t)0xFFFF;
-    // every warp that freezes an association in this tile stores the same
-    // byte (bits 0-1 are constant after the barrier above): no read-modify-write
-    if (__ballot_sync(0xffffffffu, ph_in || tgt >= 0) && lane == 0)
-      tile_state[t - it.y] = (unsigned char)(st | 4u);
+  if (a.rd.apply_n == 0 && c.ord_ph == 0 && c.ord_ge == 0)
+    dense_tiles<PREV, true>(a, c, rel, Fj, it, tile_state, acc27, acc28, eprev_p, eprev_g);
+  else
+    dense_tiles<PREV, false>(a, c, rel, Fj, it, tile_state, acc27, acc28, eprev_p, eprev_g);
 
-    // ---- photometric: one bilinear sample serves the frozen energy and J
-    if (ph_in || pph) {
-      double val[2], ddx[2], ddy[2];
-      bilinear_grad2(Fj, ua, va, val, ddx, ddy);
-      const float2 ref = __ldg(&Fi.G[p]);
-      const double r0 = (double)ref.x - val[0], r1 = (double)ref.y - val[1];
-      const double e2 = r0 * r0 + r1 * r1;
-      if (PREV && pph) eprev_p += e2;
-      if (ph_in) {
-        acc27 += e2;
-        const double a_ = Fj.fx * rz, b_ = Fj.fy * rz;
-        dq0[0] = ddx[0] * a_;
-        dq0[1] = ddx[1] * a_;
-        dq1[0] = ddy[0] * b_;
-        dq1[1] = ddy[1] * b_;
-        rp[0] = r0;
-        rp[1] = r1;
-      }
-    }
-    if (__any_sync(0xffffffffu, ph_in || tgt >= 0)) {
-      double jp[2][6], jg[6];
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const double dq2 = -(dq0[c] * q0 + dq1[c] * q1) * rz;
-        jp[c][0] = dq1[c] * q2 - dq2 * q1;
-        jp[c][1] = dq2 * q0 - dq0[c] * q2;
-        jp[c][2] = dq0[c] * q1 - dq1[c] * q0;
-        jp[c][3] = dq0[c];
-        jp[c][4] = dq1[c];
-        jp[c][5] = dq2;
-      }
-      jg[0] = t1 * nj2 - t2 * nj1;
-      jg[1] = t2 * nj0 - t0 * nj2;
-      jg[2] = t0 * nj1 - t1 * nj0;
-      jg[3] = -nj0;
-      jg[4] = -nj1;
-      jg[5] = -nj2;
-      tm_chunk<0>(tm, jp, rp, jg, rg);
-      tm_chunk<1>(tm, jp, rp, jg, rg);
-      tm_chunk<2>(tm, jp, rp, jg, rg);
-      tm_chunk<3>(tm, jp, rp, jg, rg);
-      tm_wait_st();
-    }
-  }
   double acc[31];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     uint32_t u[16];
-    TM_LD16(tm + 16 * q, u);
+    TM_LD16(c.tm + 16 * q, u);
     tm_wait_ld();
 #pragma unroll
     for (int k = 0; k < 8; ++k)
@@ -675,9 +704,9 @@ __global__ void __launch_bounds__(DENSE_THREADS, DENSE_TMEM_BLOCKS) k_dense_fuse
   }
   acc[27] = acc27;
   acc[28] = acc28;
-  double* out = a.item_out + (int64_t)blockIdx.x * SFB_ITEM_STRIDE;
   acc[29] = eprev_p;  // zero without PREV
   acc[30] = eprev_g;
+  double* out = a.item_out + (int64_t)blockIdx.x * SFB_ITEM_STRIDE;
   block_reduce_store<31>(acc, out);
   // (block_reduce_store synchronised the CTA: tile_state bit2 is final)
   for (int t = it.y + threadIdx.x; t < it.z; t += blockDim.x)
@@ -691,13 +720,10 @@ __global__ void __launch_bounds__(DENSE_THREADS, DENSE_TMEM_BLOCKS) k_dense_fuse
 
 void launch_dense_linearize(const DenseArgs& a, cudaStream_t s) {
   if (a.n_items <= 0) return;
-  const bool std_order = a.rd.apply_n == 0;
   const bool prev = a.photo_mask_prev != nullptr;
   sfb_count_launch();
-  if (std_order && prev) k_dense_fused<true, true><<<a.n_items, DENSE_THREADS, 0, s>>>(a);
-  else if (std_order) k_dense_fused<true, false><<<a.n_items, DENSE_THREADS, 0, s>>>(a);
-  else if (prev) k_dense_fused<false, true><<<a.n_items, DENSE_THREADS, 0, s>>>(a);
-  else k_dense_fused<false, false><<<a.n_items, DENSE_THREADS, 0, s>>>(a);
+  if (prev) k_dense_fused<true><<<a.n_items, DENSE_THREADS, 0, s>>>(a);
+  else k_dense_fused<false><<<a.n_items, DENSE_THREADS, 0, s>>>(a);
 }
 
 // Frozen-association energy at the current poses.
