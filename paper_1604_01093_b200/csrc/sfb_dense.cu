@@ -362,7 +362,7 @@ __device__ __forceinline__ void tm_chunk(uint32_t tm, const double (&jp)[2][6], 
   TM_ST16(tm + 16 * Q, u);
 }
 #ifndef DENSE_TMEM_BLOCKS
-#define DENSE_TMEM_BLOCKS 3
+#define DENSE_TMEM_BLOCKS 4
 #endif
 
 // H / g base scale and the geo row factor of a linearisation
@@ -390,7 +390,6 @@ struct TileCtx {
   uint16_t* gtgt;
   const uint32_t* pmask_prev;
   const uint16_t* gtgt_prev;
-  uint32_t tm;
 };
 
 // exact 3-term dot in NumPy's order: FAST = the forward FMA chain
@@ -408,9 +407,9 @@ __device__ __forceinline__ double dotx(double a0, double a1, double a2, double b
 // skipped warp-uniformly.  Rare exact-rounding fallbacks stay divergent.
 template <bool PREV, bool FAST>
 __device__ __forceinline__ void dense_tile(const DenseArgs& a, const TileCtx& c, const Xf& rel,
-                                           const FrameDev& Fj, int t, int tx, int ty, unsigned st,
-                                           unsigned char* tstate, double& acc27, double& acc28,
-                                           double& eprev_p, double& eprev_g) {
+                                           const FrameDev& Fj, uint32_t tm, int t, int tx, int ty,
+                                           unsigned st, unsigned char* tstate, double& acc27,
+                                           double& acc28, double& eprev_p, double& eprev_g) {
   const int lane = threadIdx.x & 31;
   const bool vis = st & 1u;
   const bool prev_here = PREV && (st & 2u);
@@ -564,7 +563,7 @@ __device__ __forceinline__ void dense_tile(const DenseArgs& a, const TileCtx& c,
   double dq0[2] = {0.0, 0.0}, dq1[2] = {0.0, 0.0}, rp[2] = {0.0, 0.0};
   if (any_ph) {
     double val[2], ddx[2], ddy[2];
-    bilinear_grad2(Fj, ua, va, val, ddx, ddy);
+    bilinear_grad2_fast(Fj, ua, va, val, ddx, ddy);
     const float2 ref = __ldg(&c.Gi[p]);
     const double r0 = (double)ref.x - val[0], r1 = (double)ref.y - val[1];
     const double e2 = r0 * r0 + r1 * r1;
@@ -596,37 +595,62 @@ __device__ __forceinline__ void dense_tile(const DenseArgs& a, const TileCtx& c,
     jg[3] = -nj0;
     jg[4] = -nj1;
     jg[5] = -nj2;
-    tm_chunk<0>(c.tm, jp, rp, jg, rg);
-    tm_chunk<1>(c.tm, jp, rp, jg, rg);
-    tm_chunk<2>(c.tm, jp, rp, jg, rg);
-    tm_chunk<3>(c.tm, jp, rp, jg, rg);
+    tm_chunk<0>(tm, jp, rp, jg, rg);
+    tm_chunk<1>(tm, jp, rp, jg, rg);
+    tm_chunk<2>(tm, jp, rp, jg, rg);
+    tm_chunk<3>(tm, jp, rp, jg, rg);
     tm_wait_st();
   }
 }
 
 template <bool PREV, bool FAST>
 __device__ __forceinline__ void dense_tiles(const DenseArgs& a, const TileCtx& c, const Xf& rel,
-                                            const FrameDev& Fj, int4 it, unsigned char* tile_state,
-                                            double& acc27, double& acc28, double& eprev_p,
-                                            double& eprev_g) {
+                                            const FrameDev& Fj, uint32_t tm, int4 it,
+                                            unsigned char* tile_state, double& acc27, double& acc28,
+                                            double& eprev_p, double& eprev_g) {
   int tx = it.y % c.tiles_x, ty = it.y / c.tiles_x;
   for (int t = it.y; t < it.z; ++t, (++tx == c.tiles_x ? (tx = 0, ++ty) : 0)) {
     const unsigned st = tile_state[t - it.y];
     if (!(st & 3u)) continue;  // nothing to associate, nothing frozen
-    dense_tile<PREV, FAST>(a, c, rel, Fj, t, tx, ty, st, &tile_state[t - it.y], acc27, acc28,
+    dense_tile<PREV, FAST>(a, c, rel, Fj, tm, t, tx, ty, st, &tile_state[t - it.y], acc27, acc28,
                            eprev_p, eprev_g);
   }
 }
 
 template <bool PREV>
 __global__ void __launch_bounds__(DENSE_THREADS, DENSE_TMEM_BLOCKS) k_dense_fused(DenseArgs a) {
+  // per-item context in shared memory (re-read per tile instead of held in
+  // registers across the tile loop)
   __shared__ Xf rel;  // pose_j^-1 o pose_i, NumPy rounding
+  __shared__ TileCtx c;
+  __shared__ FrameDev Fj;
   __shared__ uint32_t tm_base;
   const int4 it = a.items[blockIdx.x];
   const int2 de = a.dir_edges[it.x];
-  if (threadIdx.x == 0) rel = xf_relative_exact(a.poses[de.x], a.poses[de.y], a.rd);
-  const FrameDev Fi = a.frames[de.x];
-  const FrameDev Fj = a.frames[de.y];
+  if (threadIdx.x == 0) {
+    rel = xf_relative_exact(a.poses[de.x], a.poses[de.y], a.rd);
+    const FrameDev Fi = a.frames[de.x];
+    Fj = a.frames[de.y];
+    const int2 nsrc = src_counts(a, Fi, de.x);
+    c.ord_ph = (nsrc.x == 1) ? a.rd.apply_1 : a.rd.apply_n;
+    c.ord_ge = (nsrc.y == 1) ? a.rd.apply_1 : a.rd.apply_n;
+    c.Pi = Fi.P;
+    c.Ni = Fi.N;
+    c.Gi = Fi.G;
+    c.wi = Fi.w;
+    c.hi = Fi.h;
+    c.tiles_x = Fi.tiles_x;
+    c.pmask = a.photo_mask + a.photo_off[it.x];
+    c.gtgt = a.geo_tgt + a.geo_off[it.x];
+    c.pmask_prev = PREV ? a.photo_mask_prev + a.photo_off[it.x] : nullptr;
+    c.gtgt_prev = PREV ? a.geo_tgt_prev + a.geo_off[it.x] : nullptr;
+    c.wm1 = (double)(Fj.w - 1);
+    c.hm1 = (double)(Fj.h - 1);
+    c.dwj = (double)Fj.w;
+    c.dhj = (double)Fj.h;
+    double base;
+    dense_scales(a.s_photo, a.s_geo, &base, &c.kappa);
+  }
   if ((threadIdx.x >> 5) == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(
                      (uint32_t)__cvta_generic_to_shared(&tm_base)));
@@ -635,37 +659,17 @@ __global__ void __launch_bounds__(DENSE_THREADS, DENSE_TMEM_BLOCKS) k_dense_fuse
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
-  TileCtx c;
   // warp w: lanes 32*(w%4).., columns 64*(w/4) .. +54
-  c.tm = tm_base + ((uint32_t)(((threadIdx.x >> 5) & 3) * 32) << 16) +
-         (uint32_t)((threadIdx.x >> 7) * 64);
+  const uint32_t tm = tm_base + ((uint32_t)(((threadIdx.x >> 5) & 3) * 32) << 16) +
+                      (uint32_t)((threadIdx.x >> 7) * 64);
   {
     uint32_t z[16];
 #pragma unroll
     for (int k = 0; k < 16; ++k) z[k] = 0u;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) TM_ST16(c.tm + 16 * q, z);
+    for (int q = 0; q < 4; ++q) TM_ST16(tm + 16 * q, z);
     tm_wait_st();
   }
-  const int2 nsrc = src_counts(a, Fi, de.x);
-  c.ord_ph = (nsrc.x == 1) ? a.rd.apply_1 : a.rd.apply_n;
-  c.ord_ge = (nsrc.y == 1) ? a.rd.apply_1 : a.rd.apply_n;
-  c.Pi = Fi.P;
-  c.Ni = Fi.N;
-  c.Gi = Fi.G;
-  c.wi = Fi.w;
-  c.hi = Fi.h;
-  c.tiles_x = Fi.tiles_x;
-  c.pmask = a.photo_mask + a.photo_off[it.x];
-  c.gtgt = a.geo_tgt + a.geo_off[it.x];
-  c.pmask_prev = PREV ? a.photo_mask_prev + a.photo_off[it.x] : nullptr;
-  c.gtgt_prev = PREV ? a.geo_tgt_prev + a.geo_off[it.x] : nullptr;
-  c.wm1 = (double)(Fj.w - 1);
-  c.hm1 = (double)(Fj.h - 1);
-  c.dwj = (double)Fj.w;
-  c.dhj = (double)Fj.h;
-  double base_scale;
-  dense_scales(a.s_photo, a.s_geo, &base_scale, &c.kappa);
 
   // Tile culling: a 16x16 source tile whose bounding sphere lies outside
   // the target frustum widened to the geo rounding bounds [-0.5, w-0.5]
@@ -676,10 +680,13 @@ __global__ void __launch_bounds__(DENSE_THREADS, DENSE_TMEM_BLOCKS) k_dense_fuse
   // tile whose bit2 ends up clear are never read (the flag says so).
   __shared__ unsigned char tile_state[DENSE_MAX_TILES];
   const int toff = (int)(a.geo_off[it.x] >> 8);  // this edge's first tile flag
-  for (int t = it.y + threadIdx.x; t < it.z; t += blockDim.x) {
-    unsigned char s = tile_maybe_visible(rel, Fi.tiles[t], Fj);
-    if (PREV && a.tile_any_prev[toff + t]) s |= 2;
-    tile_state[t - it.y] = s;
+  {
+    const double4* tiles = a.frames[de.x].tiles;
+    for (int t = it.y + threadIdx.x; t < it.z; t += blockDim.x) {
+      unsigned char s = tile_maybe_visible(rel, tiles[t], Fj);
+      if (PREV && a.tile_any_prev[toff + t]) s |= 2;
+      tile_state[t - it.y] = s;
+    }
   }
   __syncthreads();
 
@@ -688,15 +695,17 @@ __global__ void __launch_bounds__(DENSE_THREADS, DENSE_TMEM_BLOCKS) k_dense_fuse
   // pixels in tile-major order: slot m = tile * 256 + threadIdx.x (the frozen
   // association buffers use the same slots; a warp covers 16x2 pixels)
   if (a.rd.apply_n == 0 && c.ord_ph == 0 && c.ord_ge == 0)
-    dense_tiles<PREV, true>(a, c, rel, Fj, it, tile_state, acc27, acc28, eprev_p, eprev_g);
+    dense_tiles<PREV, true>(a, c, rel, Fj, tm, it, tile_state, acc27, acc28, eprev_p, eprev_g);
   else
-    dense_tiles<PREV, false>(a, c, rel, Fj, it, tile_state, acc27, acc28, eprev_p, eprev_g);
+    dense_tiles<PREV, false>(a, c, rel, Fj, tm, it, tile_state, acc27, acc28, eprev_p, eprev_g);
 
+  double base_scale, kappa;
+  dense_scales(a.s_photo, a.s_geo, &base_scale, &kappa);
   double acc[31];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     uint32_t u[16];
-    TM_LD16(c.tm + 16 * q, u);
+    TM_LD16(tm + 16 * q, u);
     tm_wait_ld();
 #pragma unroll
     for (int k = 0; k < 8; ++k)

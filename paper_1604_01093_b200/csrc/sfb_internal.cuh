@@ -174,6 +174,31 @@ __device__ __forceinline__ void bilinear_grad2(const FrameDev& f, double x, doub
 }
 
 
+// The same sample, evaluated with integer clamping and the difference form
+// val = v00 + ax d01 + ay (d10 + ax dxy), ddx = d01 + ay dxy, ddy = d10 + ax dxy
+// (rounding differs from interp.py's weight form at the ulp level only).
+__device__ __forceinline__ void bilinear_grad2_fast(const FrameDev& f, double x, double y,
+                                                    double val[2], double ddx[2], double ddy[2]) {
+  const int xf = __double2int_rd(x), yf = __double2int_rd(y);  // saturating floor
+  const int x0 = min(max(xf, 0), f.w - 2), y0 = min(max(yf, 0), f.h - 2);
+  double ax = x - (double)x0, ay = y - (double)y0;
+  // clip(x, 0, w-1): below -> weight 0, beyond w-1 -> weight 1 exactly
+  ax = xf < 0 ? 0.0 : (xf > f.w - 2 ? 1.0 : ax);
+  ay = yf < 0 ? 0.0 : (yf > f.h - 2 ? 1.0 : ay);
+  const float4 t0 = __ldg(&f.T[2 * (y0 * f.w + x0)]);
+  const float4 t1 = __ldg(&f.T[2 * (y0 * f.w + x0) + 1]);
+  const double v00[2] = {t0.x, t0.y}, v01[2] = {t0.z, t0.w};
+  const double v10[2] = {t1.x, t1.y}, v11[2] = {t1.z, t1.w};
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const double d01 = v01[c] - v00[c], d10 = v10[c] - v00[c];
+    const double dxy = (v11[c] - v10[c]) - d01;
+    val[c] = fma(ay, fma(ax, dxy, d10), fma(ax, d01, v00[c]));
+    ddx[c] = fma(ay, dxy, d01);
+    ddy[c] = fma(ax, dxy, d10);
+  }
+}
+
 // Warp-level deterministic butterfly sum (every lane ends with the same bits).
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
