@@ -295,17 +295,15 @@ __device__ __forceinline__ unsigned char tile_maybe_visible(const Xf& rel, const
 // 64(w/4)..), read-modify-written once per tile by the warp (tcgen05.ld/st,
 // warp-converged), so registers hold only the tile's Jacobian rows.  The
 // per-entry FMA order is photo row 0, photo row 1, geo row.
-#define TM_LD16(addr, u)                                                                        \
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" \
+#define TM_LD8(addr, u)                                                                         \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"         \
                : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]),      \
-                 "=r"(u[6]), "=r"(u[7]), "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]),    \
-                 "=r"(u[12]), "=r"(u[13]), "=r"(u[14]), "=r"(u[15])                            \
+                 "=r"(u[6]), "=r"(u[7])                                                        \
                : "r"(addr))
-#define TM_ST16(addr, u)                                                                        \
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" \
+#define TM_ST8(addr, u)                                                                         \
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"         \
                ::"r"(addr), "r"(u[0]), "r"(u[1]), "r"(u[2]), "r"(u[3]), "r"(u[4]), "r"(u[5]), \
-                 "r"(u[6]), "r"(u[7]), "r"(u[8]), "r"(u[9]), "r"(u[10]), "r"(u[11]),           \
-                 "r"(u[12]), "r"(u[13]), "r"(u[14]), "r"(u[15])                                \
+                 "r"(u[6]), "r"(u[7])                                                          \
                : "memory")
 __device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
@@ -343,23 +341,19 @@ __device__ __forceinline__ double tm_update(double acc, const double (&jp)[2][6]
     return fma(jg[r], rg, acc);
   }
 }
+// entries 4Q..4Q+3 (x8 = 4 doubles per tcgen05.ld/st: at 64 registers the
+// narrower chunk spills less than x16 - 4.34 vs 4.65 ms per launch at cfg4)
 template <int Q>
 __device__ __forceinline__ void tm_chunk(uint32_t tm, const double (&jp)[2][6], const double (&rp)[2],
                                          const double (&jg)[6], double rg) {
-  uint32_t u[16];
-  TM_LD16(tm + 16 * Q, u);
+  uint32_t u[8];
+  TM_LD8(tm + 8 * Q, u);
   tm_wait_ld();
-  tm_set(u, 0, tm_update<8 * Q + 0>(tm_d(u, 0), jp, rp, jg, rg));
-  tm_set(u, 1, tm_update<8 * Q + 1>(tm_d(u, 1), jp, rp, jg, rg));
-  tm_set(u, 2, tm_update<8 * Q + 2>(tm_d(u, 2), jp, rp, jg, rg));
-  if constexpr (8 * Q + 3 < 27) {
-    tm_set(u, 3, tm_update<8 * Q + 3>(tm_d(u, 3), jp, rp, jg, rg));
-    tm_set(u, 4, tm_update<8 * Q + 4>(tm_d(u, 4), jp, rp, jg, rg));
-    tm_set(u, 5, tm_update<8 * Q + 5>(tm_d(u, 5), jp, rp, jg, rg));
-    tm_set(u, 6, tm_update<8 * Q + 6>(tm_d(u, 6), jp, rp, jg, rg));
-    tm_set(u, 7, tm_update<8 * Q + 7>(tm_d(u, 7), jp, rp, jg, rg));
-  }
-  TM_ST16(tm + 16 * Q, u);
+  tm_set(u, 0, tm_update<4 * Q + 0>(tm_d(u, 0), jp, rp, jg, rg));
+  tm_set(u, 1, tm_update<4 * Q + 1>(tm_d(u, 1), jp, rp, jg, rg));
+  tm_set(u, 2, tm_update<4 * Q + 2>(tm_d(u, 2), jp, rp, jg, rg));
+  if constexpr (4 * Q + 3 < 27) tm_set(u, 3, tm_update<4 * Q + 3>(tm_d(u, 3), jp, rp, jg, rg));
+  TM_ST8(tm + 8 * Q, u);
 }
 #ifndef DENSE_TMEM_BLOCKS
 #define DENSE_TMEM_BLOCKS 4
@@ -599,6 +593,9 @@ __device__ __forceinline__ void dense_tile(const DenseArgs& a, const TileCtx& c,
     tm_chunk<1>(tm, jp, rp, jg, rg);
     tm_chunk<2>(tm, jp, rp, jg, rg);
     tm_chunk<3>(tm, jp, rp, jg, rg);
+    tm_chunk<4>(tm, jp, rp, jg, rg);
+    tm_chunk<5>(tm, jp, rp, jg, rg);
+    tm_chunk<6>(tm, jp, rp, jg, rg);
     tm_wait_st();
   }
 }
@@ -663,11 +660,11 @@ __global__ void __launch_bounds__(DENSE_THREADS, DENSE_TMEM_BLOCKS) k_dense_fuse
   const uint32_t tm = tm_base + ((uint32_t)(((threadIdx.x >> 5) & 3) * 32) << 16) +
                       (uint32_t)((threadIdx.x >> 7) * 64);
   {
-    uint32_t z[16];
+    uint32_t z[8];
 #pragma unroll
-    for (int k = 0; k < 16; ++k) z[k] = 0u;
+    for (int k = 0; k < 8; ++k) z[k] = 0u;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) TM_ST16(tm + 16 * q, z);
+    for (int q = 0; q < 7; ++q) TM_ST8(tm + 8 * q, z);
     tm_wait_st();
   }
 
@@ -703,13 +700,13 @@ __global__ void __launch_bounds__(DENSE_THREADS, DENSE_TMEM_BLOCKS) k_dense_fuse
   dense_scales(a.s_photo, a.s_geo, &base_scale, &kappa);
   double acc[31];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    uint32_t u[16];
-    TM_LD16(tm + 16 * q, u);
+  for (int q = 0; q < 7; ++q) {
+    uint32_t u[8];
+    TM_LD8(tm + 8 * q, u);
     tm_wait_ld();
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
-      if (8 * q + k < 27) acc[8 * q + k] = base_scale * tm_d(u, k);
+    for (int k = 0; k < 4; ++k)
+      if (4 * q + k < 27) acc[4 * q + k] = base_scale * tm_d(u, k);
   }
   acc[27] = acc27;
   acc[28] = acc28;
