@@ -314,6 +314,13 @@ int sfb_point_eval(sfb_problem* p, int32_t frame_i, int32_t frame_j,
                    const double* aux, const double* targets, double* res,
                    double* jac);
 
+/* PCG preconditioner of this problem (every later sfb_pcg / GN step):
+ * 0 = scalar Jacobi, the reference's pcg_solve (solver.py:477, default);
+ * 1 = block Jacobi, the inverse of each variable's 6x6 diagonal block of A
+ *     (opt-in performance mode: NOT the reference's recurrence, so results
+ *     differ from the reference beyond rounding). */
+int sfb_set_preconditioner(sfb_problem* p, int32_t kind);
+
 /* ---- data-parallel sharding over frame pairs -----
  * A problem replicated on world ranks (one process per GPU) owns every
  * world-th directed dense edge and every world-th filter candidate.  The

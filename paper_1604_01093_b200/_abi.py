@@ -116,6 +116,7 @@ SIGNATURES = {
     "sfb_point_eval": [_P, _I32, _I32, _I32, _I64, _P, _P, _P, _P, _P],
     "sfb_energy_and_linearize": [_P, C.POINTER(Weights), _I32, _D, C.POINTER(Config), _P],
     "sfb_set_shard": [_P, _I32, _I32],
+    "sfb_set_preconditioner": [_P, _I32],
     "sfb_exchange_buffer": [_P, _I32, C.POINTER(_P), C.POINTER(_I64)],
     "sfb_build_dense_edges_begin": [_P, _D],
     "sfb_build_dense_edges_end": [_P, C.POINTER(_I64)],

@@ -86,6 +86,8 @@ struct sfb_problem : Handle {
   DBuf<double> pv2;            // second search-direction buffer (PCG ping-pong)
   DBuf<double> x, r, z, pv, Ap, inv_diag, bvec, part, tmp, jdiag;
   DBuf<int> flags;
+  int precond = 0;             // 0: scalar Jacobi (reference), 1: block Jacobi (opt-in)
+  DBuf<double> bj_inv;         // block-Jacobi inverses, n_blk x 36
   bool have_system = false;
   bool have_solution = false;
   // scalars
@@ -142,6 +144,7 @@ PcgArgs pcg_args(sfb_problem* p) {
   a.jdiag = p->jdiag.p;
   a.part = p->part.p;
   a.flags = p->flags.p;
+  a.bj_inv = p->precond ? p->bj_inv.p : nullptr;
   return a;
 }
 
@@ -495,6 +498,11 @@ int enqueue_linearize_end(sfb_problem* p) {
     k_jacobi_diag<<<(6 * p->n_blk + 255) / 256, 256, 0, s>>>(p->D.p, p->d_ptr.p, p->d_ent.p,
                                                              p->set_out.p, p->n_blk, p->jdiag.p);
     CKL(p);
+    if (p->precond) {
+      CK(p, p->bj_inv.ensure((size_t)p->n_blk * 36, s));
+      launch_block_jacobi_inv(p->D.p, p->jdiag.p, p->n_blk, p->bj_inv.p, s);
+      CKL(p);
+    }
   }
   launch_sum_energies(p->set_out.p, p->n_sets, p->edge_out.p, dense_on ? p->n_dir : 0, nullptr, 0,
                       p->dscal.p, 0, s);
@@ -935,7 +943,7 @@ int sfb_problem_destroy(sfb_problem* p) {
   DBuf<double>* db[] = {&p->pts_i, &p->pts_j, &p->world_i, &p->world_j, &p->set_out,
                         &p->item_out, &p->edge_out, &p->item_e2, &p->D, &p->B, &p->g, &p->x,
                         &p->r, &p->z, &p->pv, &p->Ap, &p->inv_diag, &p->bvec, &p->part, &p->tmp, &p->jdiag,
-                        &p->pv2, &p->Brow,
+                        &p->pv2, &p->Brow, &p->bj_inv,
                         &p->dscal};
   for (auto* b : db) b->release();
   p->frames.release();
@@ -1777,6 +1785,22 @@ int sfb_set_shard(sfb_problem* p, int32_t rank, int32_t world) {
   p->shard_rank = rank;
   p->shard_world = world;
   return rebuild_structure(p, p->struct_bidir < 0 ? 0 : p->struct_bidir);
+}
+
+int sfb_set_preconditioner(sfb_problem* p, int32_t kind) {
+  if (!p || kind < 0 || kind > 1) return fail(p, SFB_E_ARG, "preconditioner must be 0 or 1");
+  CK(p, cudaSetDevice(p->ctx->device));
+  if (kind == p->precond) return SFB_OK;
+  CK(p, cudaStreamSynchronize(p->stream));  // a speculative PCG used the previous one
+  p->precond = kind;
+  p->spec_pcg = false;
+  p->have_solution = false;
+  if (kind && p->have_system && p->n_blk > 0) {
+    CK(p, p->bj_inv.ensure((size_t)p->n_blk * 36, p->stream));
+    launch_block_jacobi_inv(p->D.p, p->jdiag.p, p->n_blk, p->bj_inv.p, p->stream);
+    CKL(p);
+  }
+  return SFB_OK;
 }
 
 int sfb_exchange_buffer(sfb_problem* p, int32_t which, void** dev_ptr, int64_t* bytes) {

@@ -100,6 +100,7 @@ struct PcgArgs {
   int restart;
   double* out_scalars; // [0] iterations, [1] relative, [2] status
   const double* skip;  // optional: skip when *skip != 0
+  const double* bj_inv;  // block-Jacobi inverses (n_blk x 36) or null: scalar Jacobi
 };
 
 // dense_verify (filters.py:216-277): one item = one direction of one pair
@@ -181,6 +182,8 @@ void launch_sparse(const SparseArgs& a, cudaStream_t s);
 void launch_dense_linearize(const DenseArgs& a, cudaStream_t s);
 void launch_stride_counts(const FrameDev* frames, int n, int stride, int2* out, cudaStream_t s);
 void launch_dense_energy(const DenseArgs& a, double* item_e2, cudaStream_t s);
+void launch_block_jacobi_inv(const double* D, const double* jdiag, int n_blk, double* out,
+                             cudaStream_t s);
 void launch_edge_reduce2(const int* edge_item_ptr, const double* item_e2, double* edge_e2, int n_dir,
                          cudaStream_t s);
 void launch_edge_reduce(const int* edge_item_ptr, const double* item_out, double* edge_out,

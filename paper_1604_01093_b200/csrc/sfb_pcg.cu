@@ -182,6 +182,19 @@ __device__ __forceinline__ void grid_allsum(const double* part, double (&out)[NV
   }
 }
 
+// z = M^-1 r for one block row: scalar Jacobi (the reference's pcg_solve,
+// solver.py:477) or, opt-in, block Jacobi with the row's inverted 6x6
+// diagonal block (k_block_jacobi_inv).  Called by the whole warp (r in lanes
+// 0..5, grid-uniform branch); lanes 0..5 get their z.
+__device__ __forceinline__ double precond(const PcgArgs& a, int row, double ri, double inv, int lane) {
+  if (a.bj_inv == nullptr) return inv * ri;
+  const double* M = a.bj_inv + (int64_t)row * 36 + 6 * (lane % 6);
+  double z = 0.0;
+#pragma unroll
+  for (int c = 0; c < 6; ++c) z = fma(__ldg(M + c), __shfl_sync(0xffffffffu, ri, c), z);
+  return z;
+}
+
 // fixed-order sum of lanes 0..5 (one row value each), result in all lanes
 __device__ __forceinline__ double sum6(double v) {
   double t = 0.0;
@@ -285,11 +298,11 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg(PcgArgs a, Mv mv, int ro
     double v[2] = {0.0, 0.0};
     for (int row = rc.r0 + wid; row < rc.r1; row += PCG_WARPS) {
       double bb = 0.0, bz = 0.0;
+      const int i = 6 * row + (own ? lane : 0);
+      const double bi = own ? -a.g[i] : 0.0;
+      const double inv = own ? 1.0 / fmax(a.jdiag[i], 1e-12) : 0.0;
+      const double zi = precond(a, row, bi, inv, lane);
       if (own) {
-        const int i = 6 * row + lane;
-        const double bi = -a.g[i];
-        const double inv = 1.0 / fmax(a.jdiag[i], 1e-12);
-        const double zi = inv * bi;
         a.b[i] = bi;
         a.x[i] = 0.0;
         a.inv_diag[i] = inv;
@@ -360,9 +373,12 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg(PcgArgs a, Mv mv, int ro
             const double xi = fma(alpha, pb[i], a.x[i]);
             a.x[i] = xi;
             bad = isfinite(xi) ? 0.0 : 1.0;
-            if (!restart) {
-              const double ri = fma(-alpha, a.Ap[i], a.r[i]);
-              const double zi = a.inv_diag[i] * ri;
+          }
+          if (!restart) {
+            const int i = 6 * row + (own ? lane : 0);
+            const double ri = own ? fma(-alpha, a.Ap[i], a.r[i]) : 0.0;
+            const double zi = precond(a, row, ri, own ? a.inv_diag[i] : 0.0, lane);
+            if (own) {
               a.r[i] = ri;
               a.z[i] = zi;
               rr = ri * ri;
@@ -378,10 +394,10 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg(PcgArgs a, Mv mv, int ro
           for (int row = rc.r0 + wid; row < rc.r1; row += PCG_WARPS) {
             const double y = mv.template row<false>(a, rc, row, nullptr, a.x, 0.0, lane);
             double rr = 0.0, rzv = 0.0;
+            const int i = 6 * row + (own ? lane : 0);
+            const double ri = own ? a.b[i] - y : 0.0;
+            const double zi = precond(a, row, ri, own ? a.inv_diag[i] : 0.0, lane);
             if (own) {
-              const int i = 6 * row + lane;
-              const double ri = a.b[i] - y;
-              const double zi = a.inv_diag[i] * ri;
               a.r[i] = ri;
               a.z[i] = zi;
               rr = ri * ri;
@@ -490,11 +506,11 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg_reg(PcgArgs a, Mv mv, in
     for (int j = 0; j < nrow; ++j) {
       const int row = rc.r0 + wid + PCG_WARPS * j;
       double bb = 0.0, bz = 0.0;
+      const int i = 6 * row + (own ? lane : 0);
+      const double bi = own ? -a.g[i] : 0.0;
+      const double inv = own ? 1.0 / fmax(a.jdiag[i], 1e-12) : 0.0;
+      const double zi = precond(a, row, bi, inv, lane);
       if (own) {
-        const int i = 6 * row + lane;
-        const double bi = -a.g[i];
-        const double inv = 1.0 / fmax(a.jdiag[i], 1e-12);
-        const double zi = inv * bi;
         rset(br, j, bi);
         rset(idr, j, inv);
         rset(rr_, j, bi);
@@ -567,14 +583,15 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg_reg(PcgArgs a, Mv mv, in
             const double xi = fma(alpha, rsel(pr, j), rsel(xr, j));
             rset(xr, j, xi);
             bad = isfinite(xi) ? 0.0 : 1.0;
-            if (restart) {
-              a.x[i] = xi;  // read by the neighbours' r = b - A x
-            } else {
-              const double ri = fma(-alpha, rsel(apr, j), rsel(rr_, j));
-              const double zi = rsel(idr, j) * ri;
+            if (restart) a.x[i] = xi;  // read by the neighbours' r = b - A x
+          }
+          if (!restart) {
+            const double ri = own ? fma(-alpha, rsel(apr, j), rsel(rr_, j)) : 0.0;
+            const double zi = precond(a, row, ri, rsel(idr, j), lane);
+            if (own) {
               rset(rr_, j, ri);
               rset(zr, j, zi);
-              a.z[i] = zi;
+              a.z[6 * row + lane] = zi;
               rrv = ri * ri;
               rzv = ri * zi;
             }
@@ -589,9 +606,9 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg_reg(PcgArgs a, Mv mv, in
             const int row = rc.r0 + wid + PCG_WARPS * j;
             const double y = mv.template row<false>(a, rc, row, nullptr, a.x, 0.0, lane);
             double rrv = 0.0, rzv = 0.0;
+            const double ri = own ? rsel(br, j) - y : 0.0;
+            const double zi = precond(a, row, ri, rsel(idr, j), lane);
             if (own) {
-              const double ri = rsel(br, j) - y;
-              const double zi = rsel(idr, j) * ri;
               rset(rr_, j, ri);
               rset(zr, j, zi);
               a.z[6 * row + lane] = zi;
@@ -632,6 +649,80 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg_reg(PcgArgs a, Mv mv, in
     a.out_scalars[1] = relative;
     a.out_scalars[2] = (double)status;
   }
+}
+
+// Block-Jacobi preconditioner (opt-in, not the reference's scalar Jacobi):
+// the inverse of each variable's 6x6 diagonal block of A (D, sparse + dense),
+// by Cholesky; a block that is not numerically positive definite falls back
+// to the scalar Jacobi inverse of the reference (1 / max(diag, 1e-12)).
+__global__ void k_block_jacobi_inv(const double* D, const double* jdiag, int n_blk, double* out) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= n_blk) return;
+  double A[36];
+#pragma unroll
+  for (int k = 0; k < 36; ++k) A[k] = D[(int64_t)v * 36 + k];
+  double L[36];
+#pragma unroll
+  for (int k = 0; k < 36; ++k) L[k] = 0.0;
+  double dmax = 0.0;
+#pragma unroll
+  for (int r = 0; r < 6; ++r) dmax = fmax(dmax, fabs(A[r * 7]));
+  bool ok = dmax > 0.0 && isfinite(dmax);
+#pragma unroll
+  for (int c = 0; c < 6; ++c) {
+    double d = A[c * 7];
+#pragma unroll
+    for (int k = 0; k < c; ++k) d -= L[c * 6 + k] * L[c * 6 + k];
+    ok = ok && d > 1e-12 * dmax;
+    const double lc = sqrt(fmax(d, 1e-300));
+    L[c * 7] = lc;
+#pragma unroll
+    for (int r = c + 1; r < 6; ++r) {
+      double x = A[r * 6 + c];
+#pragma unroll
+      for (int k = 0; k < c; ++k) x -= L[r * 6 + k] * L[c * 6 + k];
+      L[r * 6 + c] = x / lc;
+    }
+  }
+  double* o = out + (int64_t)v * 36;
+  if (!ok) {
+#pragma unroll
+    for (int k = 0; k < 36; ++k) o[k] = 0.0;
+#pragma unroll
+    for (int r = 0; r < 6; ++r) o[r * 7] = 1.0 / fmax(jdiag[6 * v + r], 1e-12);
+    return;
+  }
+  // W = L^-1 (lower triangular), A^-1 = W^T W
+  double W[36];
+#pragma unroll
+  for (int k = 0; k < 36; ++k) W[k] = 0.0;
+#pragma unroll
+  for (int c = 0; c < 6; ++c) {
+    W[c * 7] = 1.0 / L[c * 7];
+#pragma unroll
+    for (int r = c + 1; r < 6; ++r) {
+      double x = 0.0;
+#pragma unroll
+      for (int k = c; k < r; ++k) x -= L[r * 6 + k] * W[k * 6 + c];
+      W[r * 6 + c] = x / L[r * 7];
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 6; ++r)
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+      double x = 0.0;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) x += W[k * 6 + r] * W[k * 6 + c];
+      o[r * 6 + c] = x;
+    }
+}
+
+void launch_block_jacobi_inv(const double* D, const double* jdiag, int n_blk, double* out,
+                             cudaStream_t s) {
+  if (n_blk <= 0) return;
+  sfb_count_launch();
+  k_block_jacobi_inv<<<(n_blk + 127) / 128, 128, 0, s>>>(D, jdiag, n_blk, out);
 }
 
 template <class Mv>

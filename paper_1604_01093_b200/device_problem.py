@@ -161,6 +161,10 @@ class DeviceProblem:
         self._ck(self.lib.sfb_problem_stream(self.handle, C.byref(s)))
         return s.value or 0
 
+    def set_preconditioner(self, kind: int) -> None:
+        """0: scalar Jacobi (the reference's), 1: block Jacobi (opt-in)."""
+        self._ck(self.lib.sfb_set_preconditioner(self.handle, int(kind)))
+
     # -- sharding (DESIGN.md section 6) ---------------------------------------
     def set_shard(self, rank: int, world: int) -> None:
         self._ck(self.lib.sfb_set_shard(self.handle, int(rank), int(world)))

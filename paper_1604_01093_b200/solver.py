@@ -68,6 +68,21 @@ class SolverConfig:
     dense_pixel_stride: int = 1
     dense_bidirectional: bool = False
     prune_residual_max: float = 0.05
+    # PCG preconditioner (not a reference field): "jacobi" is the reference's
+    # scalar Jacobi (solver.py:477); "block_jacobi" (opt-in performance mode)
+    # inverts each frame's 6x6 diagonal block and does NOT reproduce the
+    # reference's iterates.
+    preconditioner: str = "jacobi"
+
+
+_PRECONDITIONERS = {"jacobi": 0, "block_jacobi": 1}
+
+
+def _precond_kind(config) -> int:
+    name = getattr(config, "preconditioner", "jacobi")
+    if name not in _PRECONDITIONERS:
+        raise ValueError(f"unknown preconditioner {name!r} (expected one of {sorted(_PRECONDITIONERS)})")
+    return _PRECONDITIONERS[name]
 
 
 # ---------------------------------------------------------------------------
@@ -760,6 +775,7 @@ class AlignmentProblem:
     def normal_equations(self, weights: EnergyWeights, w_dense: float, config: SolverConfig):
         """(equations, energy, photo_assocs, geo_assocs) at the current poses (solver.py:630-660)."""
         dp = self._problem()
+        dp.set_preconditioner(_precond_kind(config))
         self._push_poses()
         self._sync_edges()
         e = dp.linearize(weights, w_dense, config, exchange=self._xch)
@@ -794,6 +810,7 @@ class AlignmentProblem:
             return stats
         tr = _Tracer()
         dp = self._problem()
+        dp.set_preconditioner(_precond_kind(config))
         self._push_poses()
         tr.mark("setup")
         if self.caches is not None:
