@@ -76,3 +76,66 @@ def test_sharded_solve_bit_identical(name):
         assert edges == edges1
         assert recs == recs1
         assert np.array_equal(R, R1) and np.array_equal(t, t1)
+
+
+def _nccl_worker(port, name, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), SFB_DEVICE="0")
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        from paper_1604_01093_b200 import solver as S
+        from paper_1604_01093_b200.shard import ShardComm
+        comm = ShardComm()
+        sc = GoldenScene(name)
+        p = S.AlignmentProblem(sc.ids, sc.init, sc.corr_sets, sc.caches)
+        # force the two-phase sharded protocol on a one-rank NCCL group: every
+        # exchange buffer goes through ShardComm's device path (the solver's
+        # stream as an ExternalStream, the libsfb buffer as a CUDA array view)
+        p._xch = comm
+        p._problem()
+        p._dp.set_shard(0, 1)
+        calls = []
+        orig = comm.__call__
+
+        def counted(dp, which):
+            calls.append(which)
+            return orig(dp, which)
+        p._xch = counted
+        counted.rank, counted.world = 0, 1
+        st = p.solve(sc.weights_obj(S), sc.config_obj(S), sc.max_iterations)
+        R = np.stack([np.asarray(p.poses[f].rotation) for f in sc.ids])
+        t = np.stack([np.asarray(p.poses[f].translation) for f in sc.ids])
+        recs = [(r.energy_before, r.energy_after, r.pcg_iterations, r.accepted) for r in st.iterations]
+        q.put((R, t, recs, list(p.dense_edges), sorted(set(calls)), dist.get_backend()))
+    except Exception as e:
+        import traceback
+        q.put(traceback.format_exc())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(600)
+def test_nccl_exchange_path_world1():
+    """The NCCL branch of ShardComm (device buffers on the solver's stream)
+    on a one-rank NCCL group: the sharded protocol must reproduce the plain
+    solve bit-for-bit (all_reduce over one rank is the identity)."""
+    import torch.multiprocessing as mp
+    R1, t1, recs1, edges1 = _solve("cfg2")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    proc = ctx.Process(target=_nccl_worker, args=(_free_port(), "cfg2", q))
+    proc.start()
+    try:
+        res = q.get(timeout=300)
+    finally:
+        proc.join(timeout=30)
+        if proc.is_alive():
+            proc.kill()
+    assert not isinstance(res, str), res
+    R, t, recs, edges, calls, backend = res
+    assert backend == "nccl"
+    assert set(calls) >= {0, 2}, calls  # per-edge sums and the filter flags were exchanged
+    assert edges == edges1 and recs == recs1
+    assert np.array_equal(R, R1) and np.array_equal(t, t1)
