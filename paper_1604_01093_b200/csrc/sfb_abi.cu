@@ -17,6 +17,9 @@
 #include <unordered_map>
 #include <vector>
 
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_run_length_encode.cuh>
+#include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 
 #include "../../include/sfb.h"
@@ -80,8 +83,16 @@ struct sfb_problem : Handle {
   int last_do_photo = 0, last_do_geo = 0;
   // system
   int n_pairs = 0;
-  std::vector<int2> pair_vars;
   DBuf<int> d_ptr, d_ent, b_ptr, b_ent, row_ptr, row_ent, row_col;
+  DBuf<unsigned> pair_key;     // pair q = (a, b): a * n_blk + b, increasing
+  DBuf<int2> edges_d;          // the undirected edges on the device
+  struct {                     // rebuild_structure scratch
+    DBuf<int> icount, per, dcount, bcount, doff, boff, dval, bval, runs, hval, hval2;
+    DBuf<int64_t> pcount, gcount;
+    DBuf<unsigned> dkey, dkey2, bkey, bkey2, hkey, hkey2;
+    DBuf<double> scal;
+    DBuf<uint8_t> temp;
+  } sc;
   DBuf<double> D, B, g, Brow;  // Brow: row-major pre-oriented blocks for the matvec
   DBuf<double> pv2;            // second search-direction buffer (PCG ping-pong)
   DBuf<double> x, r, z, pv, Ap, inv_diag, bvec, part, tmp, jdiag;
@@ -155,184 +166,171 @@ cudaError_t upload_vec(DBuf<T>& d, const std::vector<T>& h, cudaStream_t s) {
   return cudaMemcpyAsync(d.p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, s);
 }
 
-// Which frame pairs couple, the contribution lists, the dense work items.
+// CUB device-wide primitives with the problem's shared temp storage.
+template <class F>
+cudaError_t cub_call(DBuf<uint8_t>& temp, cudaStream_t s, F f) {
+  size_t bytes = 0;
+  cudaError_t e = f(nullptr, bytes);
+  if (e != cudaSuccess) return e;
+  if ((e = temp.ensure(bytes, s)) != cudaSuccess) return e;
+  return f(temp.p, bytes);
+}
+
+// Which frame pairs couple, the contribution lists, the dense work items
+// (built on the device, sfb_struct.cu).  One host sync at the end reads the
+// sizes the later allocations need.
 int rebuild_structure(sfb_problem* p, int bidir) {
   const auto t_start = std::chrono::steady_clock::now();
   const int nb = p->n_blk;
-  // directed dense edges (solver.py:151-155)
-  std::vector<int2> dir(p->edges.begin(), p->edges.end());
-  if (bidir)
-    for (const int2& e : p->edges) dir.push_back(make_int2(e.y, e.x));
-  p->n_dir = (int)dir.size();
-
-  // dense work items: (dir edge, range of 16x16 source tiles); enough items
-  // to fill the GPU, at most 1024 tiles each.  Frozen associations live in
-  // tile-major slots: 256 per tile (8 photo-mask words, 256 geo targets).
-  std::vector<int4> items;
-  std::vector<int> eptr(1, 0);
-  std::vector<int64_t> poff, goff;
-  int64_t pw = 0, gw = 0;
-  const int target = 148 * 8;
-  for (int d = 0; d < p->n_dir; ++d) {
-    const FrameDev& F = p->frames_h[dir[d].x];
-    const int nt = F.tiles_x * F.tiles_y;
-    int parts = std::max(1, (target + p->n_dir - 1) / std::max(1, p->n_dir));
-    parts = std::max(parts, (nt + 1023) / 1024);
-    parts = std::min(parts, nt);
-    const int per = (nt + parts - 1) / parts;
-    // sharded: this rank only owns every world-th directed edge
-    if (p->shard_world <= 1 || d % p->shard_world == p->shard_rank)
-      for (int b = 0; b < nt; b += per) items.push_back(make_int4(d, b, std::min(nt, b + per), 0));
-    eptr.push_back((int)items.size());
-    poff.push_back(pw);
-    goff.push_back(gw);
-    pw += (int64_t)nt * 8;
-    gw += (int64_t)nt * 256;
-  }
-  p->n_items = (int)items.size();
-  const auto t_items = std::chrono::steady_clock::now();
-
-  // Contribution lists as CSR, built in two counting passes (entries keep
-  // set order then edge order, so every sum is assembled in a fixed order).
-  // D/g entries per var: (id << 3) | kind; B entries per coupled pair.
-  struct Contrib {
-    int var, ent;
-  };
-  std::vector<Contrib> dc;
-  dc.reserve(2 * (size_t)(p->n_sets + p->n_dir) + 8);
-  std::vector<Contrib> bc;  // var = pair id
-  bc.reserve((size_t)(p->n_sets + p->n_dir) + 8);
-  // pair id lookup: a flat nb x nb table while it stays small (<= 64 MB),
-  // a hash map beyond that
-  std::vector<int2> pv;
-  const bool flat = (int64_t)nb * nb <= ((int64_t)16 << 20);
-  // persistent per host thread (a 16 MB table costs ~3 ms of page faults to
-  // create), all -1 between rebuilds
-  static thread_local std::vector<int> pair_table;
-  std::vector<int>& pid_flat = pair_table;
-  std::unordered_map<int64_t, int> pid;
-  if (flat) {
-    if (pid_flat.size() < (size_t)nb * nb) pid_flat.resize((size_t)nb * nb, -1);
-  } else {
-    pid.reserve(2 * (size_t)(p->n_sets + p->n_dir) + 8);
-  }
-  auto pair_of = [&](int a, int b) {
-    const int64_t key = (int64_t)a * nb + b;
-    if (flat) {
-      int& slot = pid_flat[key];
-      if (slot < 0) {
-        slot = (int)pv.size();
-        pv.push_back(make_int2(a, b));
-      }
-      return slot;
-    }
-    auto ins = pid.emplace(key, (int)pv.size());
-    if (ins.second) pv.push_back(make_int2(a, b));
-    return ins.first->second;
-  };
-  for (int s = 0; s < p->n_sets; ++s) {
-    const int vi = p->set_fi_h[s] - 1, vj = p->set_fj_h[s] - 1;
-    if (vi == vj) {
-      if (vi >= 0) {
-        dc.push_back({vi, s << 3 | 0});
-        dc.push_back({vi, s << 3 | 1});
-        dc.push_back({vi, s << 3 | 2});
-      }
-      continue;
-    }
-    if (vi >= 0) dc.push_back({vi, s << 3 | 0});
-    if (vj >= 0) dc.push_back({vj, s << 3 | 1});
-    if (vi >= 0 && vj >= 0) {
-      const int a = std::min(vi, vj), b = std::max(vi, vj);
-      bc.push_back({pair_of(a, b), s << 3 | (vi == a ? 0 : 1)});
-    }
-  }
-  for (int d = 0; d < p->n_dir; ++d) {
-    const int vs = dir[d].x - 1, vd = dir[d].y - 1;
-    if (vs >= 0) dc.push_back({vs, d << 3 | 4});
-    if (vd >= 0) dc.push_back({vd, d << 3 | 5});
-    if (vs >= 0 && vd >= 0) {
-      const int a = std::min(vs, vd), b = std::max(vs, vd);
-      bc.push_back({pair_of(a, b), d << 3 | 4});
-    }
-  }
-  const auto t_pairs = std::chrono::steady_clock::now();
-  p->n_pairs = (int)pv.size();
-  p->pair_vars = pv;
-  if (flat)  // reset only the entries this rebuild touched
-    for (const int2& q : pv) pid_flat[(size_t)q.x * nb + q.y] = -1;
-  auto to_csr = [](const std::vector<Contrib>& c, int rows, std::vector<int>& ptr,
-                   std::vector<int>& ent) {
-    ptr.assign(rows + 1, 0);
-    for (const Contrib& e : c) ++ptr[e.var + 1];
-    for (int r = 0; r < rows; ++r) ptr[r + 1] += ptr[r];
-    ent.resize(c.size());
-    std::vector<int> fill(ptr.begin(), ptr.end() - 1);
-    for (const Contrib& e : c) ent[fill[e.var]++] = e.ent;  // stable: input order kept
-  };
-  std::vector<int> dptr, dent, bptr, bent;
-  to_csr(dc, nb, dptr, dent);
-  to_csr(bc, p->n_pairs, bptr, bent);
-  // matvec rows: slot 0 of row v is its diagonal block, then one pre-oriented
-  // copy of every off-diagonal block touching v (pair_slot[2q] in row a as
-  // is, pair_slot[2q+1] in row b transposed).
-  std::vector<int> rcount(nb, 1);
-  for (int q = 0; q < p->n_pairs; ++q) {
-    ++rcount[pv[q].x];
-    ++rcount[pv[q].y];
-  }
-  std::vector<int> rptr(nb + 1, 0);
-  for (int v = 0; v < nb; ++v) rptr[v + 1] = rptr[v] + rcount[v];
-  std::vector<int> rcol(rptr[nb]), fill(nb), pslot(2 * (size_t)std::max(1, p->n_pairs));
-  for (int v = 0; v < nb; ++v) {
-    rcol[rptr[v]] = v;
-    fill[v] = rptr[v] + 1;
-  }
-  for (int q = 0; q < p->n_pairs; ++q) {
-    const int a = pv[q].x, b = pv[q].y;
-    pslot[2 * q] = fill[a];
-    rcol[fill[a]++] = b;
-    pslot[2 * q + 1] = fill[b];
-    rcol[fill[b]++] = a;
-  }
-  std::vector<int>& rent = pslot;
-
   cudaStream_t s = p->stream;
-  const auto t_host = std::chrono::steady_clock::now();
-  CK(p, upload_vec(p->dir_edges, dir, s));
-  CK(p, upload_vec(p->items, items, s));
-  CK(p, upload_vec(p->edge_item_ptr, eptr, s));
-  CK(p, upload_vec(p->photo_off, poff, s));
-  CK(p, upload_vec(p->geo_off, goff, s));
+  const int n_e = (int)p->edges.size();
+  const int n_dir = n_e * (bidir ? 2 : 1);
+  const int n_units = p->n_sets + n_dir;
+  p->n_dir = n_dir;
+  if ((int64_t)nb * (nb + 1) >= ((int64_t)1 << 32) - 1)
+    return fail(p, SFB_E_ARG, "too many frames for 32-bit structure keys");
+  // directed dense edges (solver.py:151-155) and the work decomposition:
+  // enough (edge, tile range) items to fill the GPU, at most 1024 tiles each;
+  // frozen associations in tile-major slots (8 photo-mask words and 256 geo
+  // targets per 16x16 tile)
+  const int target = 148 * 8;
+  int max_nt = 1;
+  for (const FrameDev& F : p->frames_h) max_nt = std::max(max_nt, F.tiles_x * F.tiles_y);
+  const int64_t items_bound =
+      (int64_t)n_dir * std::max((target + std::max(1, n_dir) - 1) / std::max(1, n_dir), (max_nt + 1023) / 1024) + 1;
+  const int64_t nd_bound = 3 * (int64_t)p->n_sets + 2 * (int64_t)n_dir;  // D entries
+  const int64_t np_bound = (int64_t)p->n_sets + n_dir;                     // B entries >= pairs
+  const int64_t nh_bound = nb + 2 * np_bound;                               // row slots
+  auto& sc = p->sc;
+  CK(p, upload_vec(p->edges_d, p->edges, s));
+  CK(p, p->dir_edges.ensure((size_t)std::max(1, n_dir), s));
+  CK(p, sc.icount.ensure((size_t)n_dir + 1, s));
+  CK(p, sc.per.ensure((size_t)std::max(1, n_dir), s));
+  CK(p, sc.pcount.ensure((size_t)n_dir + 1, s));
+  CK(p, sc.gcount.ensure((size_t)n_dir + 1, s));
+  CK(p, p->edge_item_ptr.ensure((size_t)n_dir + 1, s));
+  CK(p, p->photo_off.ensure((size_t)n_dir + 1, s));
+  CK(p, p->geo_off.ensure((size_t)n_dir + 1, s));
+  CK(p, p->items.ensure((size_t)items_bound, s));
+  CK(p, sc.dcount.ensure((size_t)n_units + 1, s));
+  CK(p, sc.bcount.ensure((size_t)n_units + 1, s));
+  CK(p, sc.doff.ensure((size_t)n_units + 1, s));
+  CK(p, sc.boff.ensure((size_t)n_units + 1, s));
+  CK(p, sc.dkey.ensure((size_t)std::max<int64_t>(1, nd_bound), s));
+  CK(p, sc.dkey2.ensure((size_t)std::max<int64_t>(1, nd_bound), s));
+  CK(p, sc.dval.ensure((size_t)std::max<int64_t>(1, nd_bound), s));
+  CK(p, p->d_ent.ensure((size_t)std::max<int64_t>(1, nd_bound), s));
+  CK(p, p->d_ptr.ensure((size_t)nb + 1, s));
+  CK(p, sc.bkey.ensure((size_t)std::max<int64_t>(1, np_bound), s));
+  CK(p, sc.bkey2.ensure((size_t)std::max<int64_t>(1, np_bound), s));
+  CK(p, sc.bval.ensure((size_t)std::max<int64_t>(1, np_bound), s));
+  CK(p, p->b_ent.ensure((size_t)std::max<int64_t>(1, np_bound), s));
+  CK(p, p->pair_key.ensure((size_t)std::max<int64_t>(1, np_bound), s));
+  CK(p, sc.runs.ensure((size_t)np_bound + 1, s));
+  CK(p, p->b_ptr.ensure((size_t)np_bound + 1, s));
+  CK(p, sc.hkey.ensure((size_t)nh_bound, s));
+  CK(p, sc.hkey2.ensure((size_t)nh_bound, s));
+  CK(p, sc.hval.ensure((size_t)nh_bound, s));
+  CK(p, sc.hval2.ensure((size_t)nh_bound, s));
+  CK(p, p->row_ptr.ensure((size_t)nb + 1, s));
+  CK(p, p->row_col.ensure((size_t)nh_bound, s));
+  CK(p, p->row_ent.ensure((size_t)std::max<int64_t>(2, 2 * np_bound), s));
+  CK(p, sc.scal.ensure(8, s));
+  const auto t_alloc = std::chrono::steady_clock::now();
+
+  // work items
+  launch_struct_edges(p->edges_d.p, n_e, bidir, p->frames.p, p->shard_rank, p->shard_world, target,
+                      p->dir_edges.p, sc.icount.p, sc.pcount.p, sc.gcount.p, sc.per.p, s);
+  CKL(p);
+  CK(p, cub_call(sc.temp, s, [&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, sc.icount.p, p->edge_item_ptr.p, n_dir + 1, s);
+  }));
+  CK(p, cub_call(sc.temp, s, [&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, sc.pcount.p, p->photo_off.p, n_dir + 1, s);
+  }));
+  CK(p, cub_call(sc.temp, s, [&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, sc.gcount.p, p->geo_off.p, n_dir + 1, s);
+  }));
+  launch_struct_items(p->dir_edges.p, n_dir, p->frames.p, p->edge_item_ptr.p, sc.per.p, p->items.p, s);
+  CKL(p);
+
+  // contribution lists: sets in set order, then directed edges; stable
+  // sorts keep that order within a variable / pair.  Unused tail keys are
+  // 0xFFFFFFFF (after every real key).
+  launch_struct_count(p->set_fi.p, p->set_fj.p, p->n_sets, p->dir_edges.p, n_dir, sc.dcount.p,
+                      sc.bcount.p, s);
+  CKL(p);
+  CK(p, cub_call(sc.temp, s, [&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, sc.dcount.p, sc.doff.p, n_units + 1, s);
+  }));
+  CK(p, cub_call(sc.temp, s, [&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, sc.bcount.p, sc.boff.p, n_units + 1, s);
+  }));
+  CK(p, cudaMemsetAsync(sc.dkey.p, 0xFF, sizeof(unsigned) * std::max<int64_t>(1, nd_bound), s));
+  CK(p, cudaMemsetAsync(sc.bkey.p, 0xFF, sizeof(unsigned) * std::max<int64_t>(1, np_bound), s));
+  launch_struct_fill(p->set_fi.p, p->set_fj.p, p->n_sets, p->dir_edges.p, n_dir, nb, sc.doff.p,
+                     sc.boff.p, sc.dkey.p, sc.dval.p, sc.bkey.p, sc.bval.p, s);
+  CKL(p);
+  const int nd = (int)std::max<int64_t>(1, nd_bound), npb = (int)std::max<int64_t>(1, np_bound);
+  CK(p, cub_call(sc.temp, s, [&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortPairs(t, b, sc.dkey.p, sc.dkey2.p, sc.dval.p, p->d_ent.p, nd, 0, 32, s);
+  }));
+  launch_struct_ptr(sc.dkey2.p, nd, nb, p->d_ptr.p, s);
+  CKL(p);
+  CK(p, cub_call(sc.temp, s, [&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortPairs(t, b, sc.bkey.p, sc.bkey2.p, sc.bval.p, p->b_ent.p, npb, 0, 32, s);
+  }));
+  int* n_runs = reinterpret_cast<int*>(sc.scal.p);
+  CK(p, cub_call(sc.temp, s, [&](void* t, size_t& b) {
+    return cub::DeviceRunLengthEncode::Encode(t, b, sc.bkey2.p, p->pair_key.p, sc.runs.p, n_runs, npb, s);
+  }));
+  // drop the sentinel run: pairs = runs whose key is real
+  launch_struct_pairs_count(p->pair_key.p, n_runs, n_runs + 1, s);
+  CKL(p);
+  CK(p, cub_call(sc.temp, s, [&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, sc.runs.p, p->b_ptr.p, npb + 1, s);
+  }));
+  // matvec rows
+  const int nh = (int)nh_bound;
+  CK(p, cudaMemsetAsync(sc.hkey.p, 0xFF, sizeof(unsigned) * nh, s));
+  launch_rows_keys(p->pair_key.p, n_runs + 1, nb, nh, sc.hkey.p, sc.hval.p, s);
+  CKL(p);
+  CK(p, cub_call(sc.temp, s, [&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortPairs(t, b, sc.hkey.p, sc.hkey2.p, sc.hval.p, sc.hval2.p, nh, 0, 32, s);
+  }));
+  launch_rows_out(sc.hkey2.p, sc.hval2.p, n_runs + 1, nb, nh, p->row_ptr.p, p->row_col.p, p->row_ent.p, s);
+  CKL(p);
+  // sizes for the allocations below
+  int64_t hsz[4] = {0, 0, 0, 0};
+  CK(p, cudaMemcpyAsync(&hsz[0], p->edge_item_ptr.p + n_dir, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(p, cudaMemcpyAsync(&hsz[1], p->photo_off.p + n_dir, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CK(p, cudaMemcpyAsync(&hsz[2], p->geo_off.p + n_dir, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CK(p, cudaMemcpyAsync(&hsz[3], n_runs + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(p, cudaStreamSynchronize(s));
+  const auto t_dev = std::chrono::steady_clock::now();
+  p->n_items = (int)(hsz[0] & 0xFFFFFFFF);
+  const int64_t pw = hsz[1], gw = hsz[2];
+  p->n_pairs = (int)(hsz[3] & 0xFFFFFFFF);
   for (int b = 0; b < 2; ++b) {
     CK(p, p->photo_mask[b].ensure((size_t)std::max<int64_t>(pw, 1), s));
     CK(p, p->geo_tgt[b].ensure((size_t)std::max<int64_t>(gw, 1), s));
     CK(p, p->tile_any[b].ensure((size_t)std::max<int64_t>(gw / 256, 1), s));
   }
-  CK(p, p->item_out.ensure((size_t)p->n_items * SFB_ITEM_STRIDE, s));
-  CK(p, p->edge_out.ensure((size_t)p->n_dir * SFB_ITEM_STRIDE, s));
+  CK(p, p->item_out.ensure((size_t)std::max(1, p->n_items) * SFB_ITEM_STRIDE, s));
+  CK(p, p->edge_out.ensure((size_t)std::max(1, p->n_dir) * SFB_ITEM_STRIDE, s));
   CK(p, p->item_e2.ensure((size_t)std::max(1, p->n_items) * 2, s));
   CK(p, p->edge_e2.ensure((size_t)std::max(1, p->n_dir) * 2, s));
-  CK(p, upload_vec(p->d_ptr, dptr, s));
-  CK(p, upload_vec(p->d_ent, dent, s));
-  CK(p, upload_vec(p->b_ptr, bptr, s));
-  CK(p, upload_vec(p->b_ent, bent, s));
-  CK(p, upload_vec(p->row_ptr, rptr, s));
-  CK(p, upload_vec(p->row_ent, rent, s));
-  CK(p, upload_vec(p->row_col, rcol, s));
-  CK(p, p->D.ensure((size_t)nb * 36, s));
+  CK(p, p->D.ensure((size_t)std::max(1, nb) * 36, s));
   CK(p, p->B.ensure((size_t)std::max(1, p->n_pairs) * 36, s));
-  CK(p, p->Brow.ensure((size_t)std::max(1, rptr[nb]) * 36, s));
-  CK(p, cudaStreamSynchronize(s));  // host vectors die here
+  CK(p, p->Brow.ensure((size_t)std::max(1, nb + 2 * p->n_pairs) * 36, s));
   if (trace_on()) {
     const auto t_end = std::chrono::steady_clock::now();
-    fprintf(stderr, "sfb rebuild_structure: items %.2f ms, pairs %.2f ms, csr+rows %.2f ms; ",
-            std::chrono::duration<double, std::milli>(t_items - t_start).count(),
-            std::chrono::duration<double, std::milli>(t_pairs - t_items).count(),
-            std::chrono::duration<double, std::milli>(t_host - t_pairs).count());
-    fprintf(stderr, "sfb rebuild_structure: host %.2f ms, alloc+upload %.2f ms (%d dir edges, %d pairs)\n",
-            std::chrono::duration<double, std::milli>(t_host - t_start).count(),
-            std::chrono::duration<double, std::milli>(t_end - t_host).count(), p->n_dir, p->n_pairs);
+    fprintf(stderr, "sfb rebuild_structure (device): buffers %.2f ms, build+sync %.2f ms, alloc %.2f ms "
+            "(%d dir edges, %d pairs, %d items)\n",
+            std::chrono::duration<double, std::milli>(t_alloc - t_start).count(),
+            std::chrono::duration<double, std::milli>(t_dev - t_alloc).count(),
+            std::chrono::duration<double, std::milli>(t_end - t_dev).count(), p->n_dir, p->n_pairs,
+            p->n_items);
   }
   p->struct_bidir = bidir;
   p->have_system = false;
@@ -946,6 +944,20 @@ int sfb_problem_destroy(sfb_problem* p) {
                         &p->pv2, &p->Brow, &p->bj_inv,
                         &p->dscal};
   for (auto* b : db) b->release();
+  p->pair_key.release();
+  p->edges_d.release();
+  {
+    auto& sc = p->sc;
+    DBuf<int>* si[] = {&sc.icount, &sc.per, &sc.dcount, &sc.bcount, &sc.doff, &sc.boff, &sc.dval,
+                       &sc.bval, &sc.runs, &sc.hval, &sc.hval2};
+    for (auto* b : si) b->release();
+    sc.pcount.release();
+    sc.gcount.release();
+    DBuf<unsigned>* su[] = {&sc.dkey, &sc.dkey2, &sc.bkey, &sc.bkey2, &sc.hkey, &sc.hkey2};
+    for (auto* b : su) b->release();
+    sc.scal.release();
+    sc.temp.release();
+  }
   p->frames.release();
   p->stride_counts.release();
   p->poses.release();
@@ -1433,11 +1445,16 @@ int sfb_get_blocks(sfb_problem* p, double* diag_blocks, double* pair_blocks, int
     int rc = copy_out(p, pair_blocks, p->B.p, 36 * (size_t)p->n_pairs);
     if (rc) return rc;
   }
-  if (pair_vars)
+  if (pair_vars && p->n_pairs > 0) {
+    std::vector<unsigned> keys(p->n_pairs);
+    CK(p, cudaMemcpyAsync(keys.data(), p->pair_key.p, sizeof(unsigned) * p->n_pairs,
+                          cudaMemcpyDeviceToHost, p->stream));
+    CK(p, cudaStreamSynchronize(p->stream));
     for (int q = 0; q < p->n_pairs; ++q) {
-      pair_vars[2 * q] = p->pair_vars[q].x;
-      pair_vars[2 * q + 1] = p->pair_vars[q].y;
+      pair_vars[2 * q] = (int32_t)(keys[q] / (unsigned)p->n_blk);
+      pair_vars[2 * q + 1] = (int32_t)(keys[q] % (unsigned)p->n_blk);
     }
+  }
   return SFB_OK;
 }
 

@@ -184,6 +184,24 @@ void launch_stride_counts(const FrameDev* frames, int n, int stride, int2* out, 
 void launch_dense_energy(const DenseArgs& a, double* item_e2, cudaStream_t s);
 void launch_block_jacobi_inv(const double* D, const double* jdiag, int n_blk, double* out,
                              cudaStream_t s);
+// block-system structure (sfb_struct.cu)
+void launch_struct_edges(const int2* edges, int n_e, int bidir, const FrameDev* frames,
+                         int shard_rank, int shard_world, int target, int2* dir, int* icount,
+                         int64_t* pcount, int64_t* gcount, int* per, cudaStream_t s);
+void launch_struct_items(const int2* dir, int n_dir, const FrameDev* frames, const int* eptr,
+                         const int* per, int4* items, cudaStream_t s);
+void launch_struct_count(const int* set_fi, const int* set_fj, int n_sets, const int2* dir,
+                         int n_dir, int* dcount, int* bcount, cudaStream_t s);
+void launch_struct_fill(const int* set_fi, const int* set_fj, int n_sets, const int2* dir,
+                        int n_dir, int nb, const int* doff, const int* boff, unsigned* dkey,
+                        int* dval, unsigned* bkey, int* bval, cudaStream_t s);
+void launch_struct_ptr(const unsigned* keys, int n, int rows, int* ptr, cudaStream_t s);
+void launch_struct_pairs_count(const unsigned* unique_keys, const int* n_runs, int* n_pairs,
+                               cudaStream_t s);
+void launch_rows_keys(const unsigned* pair_key, const int* n_pairs_d, int nb, int n_max,
+                      unsigned* hkey, int* hval, cudaStream_t s);
+void launch_rows_out(const unsigned* hkey, const int* hval, const int* n_pairs_d, int nb, int n_max,
+                     int* row_ptr, int* row_col, int* pair_slot, cudaStream_t s);
 void launch_edge_reduce2(const int* edge_item_ptr, const double* item_e2, double* edge_e2, int n_dir,
                          cudaStream_t s);
 void launch_edge_reduce(const int* edge_item_ptr, const double* item_out, double* edge_out,
