@@ -314,6 +314,14 @@ int sfb_point_eval(sfb_problem* p, int32_t frame_i, int32_t frame_j,
                    const double* aux, const double* targets, double* res,
                    double* jac);
 
+/* Drop correspondence sets from a live problem (solve_with_pruning,
+ * solver.py:779-816, removes the worst set each round).  The surviving sets
+ * keep their order and are renumbered 0..n-1 (set ids of later calls refer
+ * to the compacted list); their correspondences stay resident and the block
+ * structure is rebuilt on the device.  The problem is then exactly one
+ * created from the surviving sets. */
+int sfb_problem_drop_sets(sfb_problem* p, int64_t n, const int32_t* set_ids);
+
 /* PCG preconditioner of this problem (every later sfb_pcg / GN step):
  * 0 = scalar Jacobi, the reference's pcg_solve (solver.py:477, default);
  * 1 = block Jacobi, the inverse of each variable's 6x6 diagonal block of A

@@ -117,6 +117,7 @@ SIGNATURES = {
     "sfb_energy_and_linearize": [_P, C.POINTER(Weights), _I32, _D, C.POINTER(Config), _P],
     "sfb_set_shard": [_P, _I32, _I32],
     "sfb_set_preconditioner": [_P, _I32],
+    "sfb_problem_drop_sets": [_P, _I64, _P],
     "sfb_exchange_buffer": [_P, _I32, C.POINTER(_P), C.POINTER(_I64)],
     "sfb_build_dense_edges_begin": [_P, _D],
     "sfb_build_dense_edges_end": [_P, C.POINTER(_I64)],

@@ -45,8 +45,10 @@ struct sfb_problem : Handle {
   int n_sets = 0;
   int64_t n_corr = 0;
   std::vector<int> set_fi_h, set_fj_h;
+  std::vector<int64_t> set_beg_h, set_end_h;  // per set [begin, end) into the correspondences
   DBuf<int> set_fi, set_fj;
-  DBuf<int64_t> set_off;
+  DBuf<int64_t> set_off;   // per set: first correspondence
+  DBuf<int64_t> set_end;   // per set: one past its last correspondence
   DBuf<double> pts_i, pts_j, world_i, world_j, set_out;
   // dense
   std::vector<int2> edges;  // undirected (a < b in frame order)
@@ -257,8 +259,8 @@ int rebuild_structure(sfb_problem* p, int bidir) {
   // contribution lists: sets in set order, then directed edges; stable
   // sorts keep that order within a variable / pair.  Unused tail keys are
   // 0xFFFFFFFF (after every real key).
-  launch_struct_count(p->set_fi.p, p->set_fj.p, p->n_sets, p->dir_edges.p, n_dir, sc.dcount.p,
-                      sc.bcount.p, s);
+  launch_struct_count(p->set_fi.p, p->set_fj.p, p->set_off.p, p->set_end.p, p->n_sets,
+                      p->dir_edges.p, n_dir, sc.dcount.p, sc.bcount.p, s);
   CKL(p);
   CK(p, cub_call(sc.temp, s, [&](void* t, size_t& b) {
     return cub::DeviceScan::ExclusiveSum(t, b, sc.dcount.p, sc.doff.p, n_units + 1, s);
@@ -268,8 +270,9 @@ int rebuild_structure(sfb_problem* p, int bidir) {
   }));
   CK(p, cudaMemsetAsync(sc.dkey.p, 0xFF, sizeof(unsigned) * std::max<int64_t>(1, nd_bound), s));
   CK(p, cudaMemsetAsync(sc.bkey.p, 0xFF, sizeof(unsigned) * std::max<int64_t>(1, np_bound), s));
-  launch_struct_fill(p->set_fi.p, p->set_fj.p, p->n_sets, p->dir_edges.p, n_dir, nb, sc.doff.p,
-                     sc.boff.p, sc.dkey.p, sc.dval.p, sc.bkey.p, sc.bval.p, s);
+  launch_struct_fill(p->set_fi.p, p->set_fj.p, p->set_off.p, p->set_end.p, p->n_sets,
+                     p->dir_edges.p, n_dir, nb, sc.doff.p, sc.boff.p, sc.dkey.p, sc.dval.p, sc.bkey.p,
+                     sc.bval.p, s);
   CKL(p);
   const int nd = (int)std::max<int64_t>(1, nd_bound), npb = (int)std::max<int64_t>(1, np_bound);
   CK(p, cub_call(sc.temp, s, [&](void* t, size_t& b) {
@@ -377,6 +380,7 @@ SparseArgs sparse_args(sfb_problem* p) {
   a.set_fi = p->set_fi.p;
   a.set_fj = p->set_fj.p;
   a.set_off = p->set_off.p;
+  a.set_end = p->set_end.p;
   a.pts_i = p->pts_i.p;
   a.pts_j = p->pts_j.p;
   a.set_out = p->set_out.p;
@@ -896,10 +900,10 @@ int sfb_problem_create(sfb_ctx* c, int32_t n_frames, const int32_t* slots, int32
   }
   p->set_fi_h.assign(set_fi, set_fi + n_sets);
   p->set_fj_h.assign(set_fj, set_fj + n_sets);
-  std::vector<int64_t> off(set_off, set_off + (n_sets > 0 ? n_sets + 1 : 0));
-  if (off.empty()) off.push_back(0);
+  p->set_beg_h.assign(set_off, set_off + n_sets);
+  p->set_end_h.assign(n_sets > 0 ? set_off + 1 : set_off, n_sets > 0 ? set_off + 1 + n_sets : set_off);
   if (upload_vec(p->set_fi, p->set_fi_h, s) || upload_vec(p->set_fj, p->set_fj_h, s) ||
-      upload_vec(p->set_off, off, s))
+      upload_vec(p->set_off, p->set_beg_h, s) || upload_vec(p->set_end, p->set_end_h, s))
     return bail(SFB_E_OOM, "sets");
   const size_t nc = (size_t)std::max<int64_t>(p->n_corr, 1) * 3;
   if (p->pts_i.ensure(nc) || p->pts_j.ensure(nc) || p->world_i.ensure(nc) || p->world_j.ensure(nc) ||
@@ -963,6 +967,7 @@ int sfb_problem_destroy(sfb_problem* p) {
   p->poses.release();
   p->best.release();
   p->set_off.release();
+  p->set_end.release();
   p->dir_edges.release();
   p->items.release();
   p->photo_off.release();
@@ -1801,6 +1806,43 @@ int sfb_set_shard(sfb_problem* p, int32_t rank, int32_t world) {
   CK(p, cudaSetDevice(p->ctx->device));
   p->shard_rank = rank;
   p->shard_world = world;
+  return rebuild_structure(p, p->struct_bidir < 0 ? 0 : p->struct_bidir);
+}
+
+int sfb_problem_drop_sets(sfb_problem* p, int64_t n, const int32_t* set_ids) {
+  if (!p || n < 0 || (n > 0 && !set_ids)) return fail(p, SFB_E_ARG, "bad arguments");
+  CK(p, cudaSetDevice(p->ctx->device));
+  std::vector<char> drop(p->n_sets, 0);
+  for (int64_t k = 0; k < n; ++k) {
+    if (set_ids[k] < 0 || set_ids[k] >= p->n_sets) return fail(p, SFB_E_ARG, "set id out of range");
+    drop[set_ids[k]] = 1;
+  }
+  // compact the per-set arrays (the survivors keep their order and their
+  // resident correspondence ranges): the problem is then exactly one built
+  // from the surviving sets
+  std::vector<int> fi, fj;
+  std::vector<int64_t> beg, end;
+  for (int k = 0; k < p->n_sets; ++k) {
+    if (drop[k]) continue;
+    fi.push_back(p->set_fi_h[k]);
+    fj.push_back(p->set_fj_h[k]);
+    beg.push_back(p->set_beg_h[k]);
+    end.push_back(p->set_end_h[k]);
+  }
+  CK(p, cudaStreamSynchronize(p->stream));  // no kernel may still read the old arrays
+  p->set_fi_h.swap(fi);
+  p->set_fj_h.swap(fj);
+  p->set_beg_h.swap(beg);
+  p->set_end_h.swap(end);
+  p->n_sets = (int)p->set_fi_h.size();
+  if (p->n_sets > 0) {
+    CK(p, upload_vec(p->set_fi, p->set_fi_h, p->stream));
+    CK(p, upload_vec(p->set_fj, p->set_fj_h, p->stream));
+    CK(p, upload_vec(p->set_off, p->set_beg_h, p->stream));
+    CK(p, upload_vec(p->set_end, p->set_end_h, p->stream));
+  }
+  p->spec_pcg = false;
+  p->have_solution = false;
   return rebuild_structure(p, p->struct_bidir < 0 ? 0 : p->struct_bidir);
 }
 

@@ -20,7 +20,7 @@ __global__ void __launch_bounds__(256) k_sparse(SparseArgs a) {
   const int lane = threadIdx.x & 31;
   if (warp >= a.n_sets) return;
   const int fi = a.set_fi[warp], fj = a.set_fj[warp];
-  const int64_t c0 = a.set_off[warp], c1 = a.set_off[warp + 1];
+  const int64_t c0 = a.set_off[warp], c1 = a.set_end[warp];
   const PoseDev& Pi = a.poses[fi];
   const PoseDev& Pj = a.poses[fj];
   double Ri[9], ti[3], Rj[9], tj[3];
@@ -152,7 +152,7 @@ __global__ void k_sparse_residuals(SparseArgs a, double* res, double* set_max) {
   const PoseDev& Pi = a.poses[a.set_fi[warp]];
   const PoseDev& Pj = a.poses[a.set_fj[warp]];
   double mx = 0.0;
-  for (int64_t c = a.set_off[warp] + lane; c < a.set_off[warp + 1]; c += 32) {
+  for (int64_t c = a.set_off[warp] + lane; c < a.set_end[warp]; c += 32) {
     double yi[3], yj[3];
     xf_apply(Pi.R, Pi.t, a.pts_i[3 * c], a.pts_i[3 * c + 1], a.pts_i[3 * c + 2], yi);
     xf_apply(Pj.R, Pj.t, a.pts_j[3 * c], a.pts_j[3 * c + 1], a.pts_j[3 * c + 2], yj);

@@ -23,7 +23,8 @@ struct SparseArgs {
   const PoseDev* poses;
   const int* set_fi;
   const int* set_fj;
-  const int64_t* set_off;
+  const int64_t* set_off;   // set s covers [set_off[s], set_end[s])
+  const int64_t* set_end;
   const double* pts_i;
   const double* pts_j;
   double* world_i;     // may be null (energy-only)
@@ -190,11 +191,13 @@ void launch_struct_edges(const int2* edges, int n_e, int bidir, const FrameDev* 
                          int64_t* pcount, int64_t* gcount, int* per, cudaStream_t s);
 void launch_struct_items(const int2* dir, int n_dir, const FrameDev* frames, const int* eptr,
                          const int* per, int4* items, cudaStream_t s);
-void launch_struct_count(const int* set_fi, const int* set_fj, int n_sets, const int2* dir,
-                         int n_dir, int* dcount, int* bcount, cudaStream_t s);
-void launch_struct_fill(const int* set_fi, const int* set_fj, int n_sets, const int2* dir,
-                        int n_dir, int nb, const int* doff, const int* boff, unsigned* dkey,
-                        int* dval, unsigned* bkey, int* bval, cudaStream_t s);
+void launch_struct_count(const int* set_fi, const int* set_fj, const int64_t* set_off,
+                         const int64_t* set_end, int n_sets, const int2* dir, int n_dir,
+                         int* dcount, int* bcount, cudaStream_t s);
+void launch_struct_fill(const int* set_fi, const int* set_fj, const int64_t* set_off,
+                        const int64_t* set_end, int n_sets, const int2* dir, int n_dir, int nb,
+                        const int* doff, const int* boff, unsigned* dkey, int* dval, unsigned* bkey,
+                        int* bval, cudaStream_t s);
 void launch_struct_ptr(const unsigned* keys, int n, int rows, int* ptr, cudaStream_t s);
 void launch_struct_pairs_count(const unsigned* unique_keys, const int* n_runs, int* n_pairs,
                                cudaStream_t s);

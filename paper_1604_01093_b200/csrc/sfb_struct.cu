@@ -57,12 +57,17 @@ __global__ void k_struct_items(const int2* dir, int n_dir, const FrameDev* frame
 }
 
 // Contribution counts of unit u: sets [0, n_sets), then directed edges.
-__device__ __forceinline__ void contrib_vars(const int* set_fi, const int* set_fj, int n_sets,
-                                             const int2* dir, int u, int& vi, int& vj, bool& is_set) {
+// An empty set (no correspondences, or dropped by sfb_problem_drop_sets)
+// contributes nothing and couples nothing.
+__device__ __forceinline__ void contrib_vars(const int* set_fi, const int* set_fj,
+                                             const int64_t* set_off, const int64_t* set_end,
+                                             int n_sets, const int2* dir, int u, int& vi, int& vj,
+                                             bool& is_set) {
   is_set = u < n_sets;
   if (is_set) {
-    vi = set_fi[u] - 1;
-    vj = set_fj[u] - 1;
+    const bool empty = set_end[u] <= set_off[u];
+    vi = empty ? -1 : set_fi[u] - 1;
+    vj = empty ? -1 : set_fj[u] - 1;
   } else {
     const int2 e = dir[u - n_sets];
     vi = e.x - 1;
@@ -70,8 +75,9 @@ __device__ __forceinline__ void contrib_vars(const int* set_fi, const int* set_f
   }
 }
 
-__global__ void k_struct_count(const int* set_fi, const int* set_fj, int n_sets, const int2* dir,
-                               int n_dir, int* dcount, int* bcount) {
+__global__ void k_struct_count(const int* set_fi, const int* set_fj, const int64_t* set_off,
+                               const int64_t* set_end, int n_sets, const int2* dir, int n_dir,
+                               int* dcount, int* bcount) {
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
   const int n = n_sets + n_dir;
   if (u > n) return;
@@ -82,7 +88,7 @@ __global__ void k_struct_count(const int* set_fi, const int* set_fj, int n_sets,
   }
   int vi, vj;
   bool is_set;
-  contrib_vars(set_fi, set_fj, n_sets, dir, u, vi, vj, is_set);
+  contrib_vars(set_fi, set_fj, set_off, set_end, n_sets, dir, u, vi, vj, is_set);
   if (is_set && vi == vj) {
     dcount[u] = vi >= 0 ? 3 : 0;
     bcount[u] = 0;
@@ -95,14 +101,15 @@ __global__ void k_struct_count(const int* set_fi, const int* set_fj, int n_sets,
 // D entries (id << 3 | kind): kind 0/1 set side i/j, 2 self-set, 4/5 edge
 // source/destination; B entries keyed by the pair a * nb + b (a < b), kind
 // 0/1 = which side of the set is the pair's first variable, 4 for edges.
-__global__ void k_struct_fill(const int* set_fi, const int* set_fj, int n_sets, const int2* dir,
-                              int n_dir, int nb, const int* doff, const int* boff,
-                              unsigned* dkey, int* dval, unsigned* bkey, int* bval) {
+__global__ void k_struct_fill(const int* set_fi, const int* set_fj, const int64_t* set_off,
+                              const int64_t* set_end, int n_sets, const int2* dir, int n_dir, int nb,
+                              const int* doff, const int* boff, unsigned* dkey, int* dval,
+                              unsigned* bkey, int* bval) {
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= n_sets + n_dir) return;
   int vi, vj;
   bool is_set;
-  contrib_vars(set_fi, set_fj, n_sets, dir, u, vi, vj, is_set);
+  contrib_vars(set_fi, set_fj, set_off, set_end, n_sets, dir, u, vi, vj, is_set);
   int k = doff[u];
   const int id = is_set ? u : u - n_sets;
   if (is_set) {
@@ -201,21 +208,24 @@ void launch_struct_items(const int2* dir, int n_dir, const FrameDev* frames, con
   k_struct_items<<<(n_dir + 255) / 256, 256, 0, s>>>(dir, n_dir, frames, eptr, per, items);
 }
 
-void launch_struct_count(const int* set_fi, const int* set_fj, int n_sets, const int2* dir,
-                         int n_dir, int* dcount, int* bcount, cudaStream_t s) {
+void launch_struct_count(const int* set_fi, const int* set_fj, const int64_t* set_off,
+                         const int64_t* set_end, int n_sets, const int2* dir, int n_dir,
+                         int* dcount, int* bcount, cudaStream_t s) {
   const int n = n_sets + n_dir + 1;
   sfb_count_launch();
-  k_struct_count<<<(n + 255) / 256, 256, 0, s>>>(set_fi, set_fj, n_sets, dir, n_dir, dcount, bcount);
+  k_struct_count<<<(n + 255) / 256, 256, 0, s>>>(set_fi, set_fj, set_off, set_end, n_sets, dir,
+                                                 n_dir, dcount, bcount);
 }
 
-void launch_struct_fill(const int* set_fi, const int* set_fj, int n_sets, const int2* dir,
-                        int n_dir, int nb, const int* doff, const int* boff, unsigned* dkey,
-                        int* dval, unsigned* bkey, int* bval, cudaStream_t s) {
+void launch_struct_fill(const int* set_fi, const int* set_fj, const int64_t* set_off,
+                        const int64_t* set_end, int n_sets, const int2* dir, int n_dir, int nb,
+                        const int* doff, const int* boff, unsigned* dkey, int* dval, unsigned* bkey,
+                        int* bval, cudaStream_t s) {
   const int n = n_sets + n_dir;
   if (n <= 0) return;
   sfb_count_launch();
-  k_struct_fill<<<(n + 255) / 256, 256, 0, s>>>(set_fi, set_fj, n_sets, dir, n_dir, nb, doff, boff,
-                                                dkey, dval, bkey, bval);
+  k_struct_fill<<<(n + 255) / 256, 256, 0, s>>>(set_fi, set_fj, set_off, set_end, n_sets, dir, n_dir,
+                                                nb, doff, boff, dkey, dval, bkey, bval);
 }
 
 void launch_struct_ptr(const unsigned* keys, int n, int rows, int* ptr, cudaStream_t s) {

@@ -359,6 +359,11 @@ class DeviceProblem:
             self._ck(self.lib.sfb_sparse_residuals(self.handle, _abi.ptr(r)))
         return r
 
+    def drop_sets(self, set_ids) -> None:
+        """Empty the given correspondence sets on the device (sfb_problem_drop_sets)."""
+        ids = np.ascontiguousarray(set_ids, dtype=np.int32)
+        self._ck(self.lib.sfb_problem_drop_sets(self.handle, int(ids.size), _abi.ptr(ids)))
+
     def sparse_set_max(self) -> np.ndarray:
         m = np.zeros(self.n_sets)
         if self.n_sets:

@@ -939,27 +939,52 @@ def max_residual_set(poses, corr_sets):
 
 def solve_with_pruning(frame_ids, poses, corr_sets, weights, config: SolverConfig,
                        caches=None, max_iterations=None):
-    """Alternate solving and pruning of the worst set (solver.py:779-816)."""
+    """Alternate solving and pruning of the worst set (solver.py:779-816).
+
+    The device problem stays resident across rounds while the connected
+    frames are unchanged: the pruned set's range is emptied on the device
+    (sfb_problem_drop_sets; the result equals a problem built without it)
+    and the per-set residual maxima of max_residual_set (:765-776) are read
+    from the live problem at the solved poses, instead of stacking and
+    uploading every set twice per round.  A round that disconnects a frame
+    builds a new problem over the remaining frames, as the reference does."""
     sets = list(corr_sets)
     poses = dict(poses)
     removed_pairs, invalid_frames, stats_list = [], [], []
     rounds = 0
     r_max = 0.0
-    while True:
-        rounds += 1
-        connected = {f for cs in sets for f in (cs.frame_i, cs.frame_j)}
-        active = [f for f in frame_ids if f in connected]
-        invalid_frames.extend(f for f in frame_ids if f not in connected and f not in invalid_frames)
-        if len(active) < 2 or not sets:
-            r_max = 0.0
-            break
-        problem = AlignmentProblem(active, poses, sets, caches)
-        stats_list.append(problem.solve(weights, config, max_iterations))
-        poses.update(problem.poses)
-        problem.close()
-        worst_idx, r_max = max_residual_set(poses, sets)
-        if r_max <= config.prune_residual_max:
-            break
-        offender = sets.pop(worst_idx)
-        removed_pairs.append((offender.frame_i, offender.frame_j))
+    problem, problem_active = None, None
+    try:
+        while True:
+            rounds += 1
+            connected = {f for cs in sets for f in (cs.frame_i, cs.frame_j)}
+            active = [f for f in frame_ids if f in connected]
+            invalid_frames.extend(f for f in frame_ids if f not in connected and f not in invalid_frames)
+            if len(active) < 2 or not sets:
+                r_max = 0.0
+                break
+            if problem is None or active != problem_active:
+                if problem is not None:
+                    problem.close()
+                problem = AlignmentProblem(active, poses, sets, caches)
+                problem_active = active
+            else:
+                problem.poses = {f: poses[f] for f in active}
+            stats_list.append(problem.solve(weights, config, max_iterations))
+            poses.update(problem.poses)
+            peaks = problem._problem().sparse_set_max()
+            worst_idx, r_max = -1, -1.0
+            for idx, cs in enumerate(sets):
+                peak = float(peaks[idx]) if len(cs) else 0.0
+                if peak > r_max:
+                    r_max, worst_idx = peak, idx
+            if r_max <= config.prune_residual_max:
+                break
+            offender = sets.pop(worst_idx)
+            removed_pairs.append((offender.frame_i, offender.frame_j))
+            # the device problem compacts its sets the same way (ids follow `sets`)
+            problem._problem().drop_sets([worst_idx])
+    finally:
+        if problem is not None:
+            problem.close()
     return poses, sets, PruneReport(removed_pairs, invalid_frames, rounds, r_max), stats_list
