@@ -15,12 +15,72 @@
 //   H_ij = [[y_j y_i^T - (y_i.y_j) I, -[y_i]x], [[y_j]x, -I]],
 //   g_i  = [y_i x r ; r],  g_j = -[y_j x r ; r]
 // which is exactly the matrix-free product of solver.py:375-401 regrouped.
+// SPARSE_G lanes per set (a set holds ~20 correspondences at cfg3-5, so a
+// whole warp per set left most lanes idle and spent 5 shuffle levels on each
+// of the 38 moments): each lane strides over the set's correspondences, the
+// moments are summed by a butterfly inside the lane group (every lane holds
+// the totals) and the group's lanes share the 121 output writes.
+#define SPARSE_G 8
+#define SPARSE_NM 38
+
+__device__ __forceinline__ double group_sum(double v) {
+#pragma unroll
+  for (int o = SPARSE_G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// output entry e of a set (layout: Hii[36] Hjj[36] Hij[36] gi[6] gj[6] E)
+// from the summed moments m[]: Ai 0-5, Aj 6-11, M 12-20, Si 21-23, Sj 24-26,
+// gi 27-29, gj 30-32, sr 33-35, E 36, cnt 37
+__device__ __forceinline__ double sparse_entry(int e, const double* m, double w, double wg) {
+  if (e >= SFB_SET_E) return e == SFB_SET_E ? m[36] : 0.0;
+  if (e >= SFB_SET_GJ) {
+    const int k = e - SFB_SET_GJ;
+    return -wg * (k < 3 ? m[30 + k] : m[33 + k - 3]);
+  }
+  if (e >= SFB_SET_GI) {
+    const int k = e - SFB_SET_GI;
+    return wg * (k < 3 ? m[27 + k] : m[33 + k - 3]);
+  }
+  const int blk = e / 36, r = (e % 36) / 6, c = e % 6;
+  const double cnt = m[37];
+  if (r >= 3 && c >= 3) {  // +-cnt I
+    if (r != c) return 0.0;
+    return blk == 2 ? -w * cnt : w * cnt;
+  }
+  if (r < 3 && c < 3) {
+    const int ai[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
+    if (blk == 0) return w * m[ai[r][c]];
+    if (blk == 1) return w * m[6 + ai[r][c]];
+    return w * m[12 + r * 3 + c];
+  }
+  // cross blocks with [s]x = [[0,-s2,s1],[s2,0,-s0],[-s1,s0,0]]
+  auto skew = [&](const double* sv, int rr, int cc) -> double {
+    if (rr == cc) return 0.0;
+    const int k = 3 - rr - cc;  // the remaining index
+    const double sgn = ((rr + 1) % 3 == cc) ? -1.0 : 1.0;
+    return sgn * sv[k];
+  };
+  const double* Si = m + 21;
+  const double* Sj = m + 24;
+  if (r < 3) {  // upper-right
+    if (blk == 0) return w * skew(Si, r, c - 3);
+    if (blk == 1) return w * skew(Sj, r, c - 3);
+    return -w * skew(Si, r, c - 3);
+  }
+  // lower-left
+  if (blk == 0) return -w * skew(Si, r - 3, c);
+  if (blk == 1) return -w * skew(Sj, r - 3, c);
+  return w * skew(Sj, r - 3, c);
+}
+
 __global__ void __launch_bounds__(256) k_sparse(SparseArgs a) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (warp >= a.n_sets) return;
-  const int fi = a.set_fi[warp], fj = a.set_fj[warp];
-  const int64_t c0 = a.set_off[warp], c1 = a.set_end[warp];
+  const int gid = (blockIdx.x * blockDim.x + threadIdx.x) / SPARSE_G;  // set
+  const int gl = threadIdx.x & (SPARSE_G - 1);
+  const bool live = gid < a.n_sets;
+  const int set = live ? gid : a.n_sets - 1;
+  const int fi = a.set_fi[set], fj = a.set_fj[set];
+  const int64_t c0 = a.set_off[set], c1 = live ? a.set_end[set] : c0;
   const PoseDev& Pi = a.poses[fi];
   const PoseDev& Pj = a.poses[fj];
   double Ri[9], ti[3], Rj[9], tj[3];
@@ -30,24 +90,29 @@ __global__ void __launch_bounds__(256) k_sparse(SparseArgs a) {
   for (int k = 0; k < 3; ++k) { ti[k] = Pi.t[k]; tj[k] = Pj.t[k]; }
 
   // moments
-  double Ai[6] = {0, 0, 0, 0, 0, 0};   // |y_i|^2 I - y_i y_i^T, packed (00,01,02,11,12,22)
-  double Aj[6] = {0, 0, 0, 0, 0, 0};
-  double M[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};  // y_j y_i^T - (y_i.y_j) I
-  double Si[3] = {0, 0, 0}, Sj[3] = {0, 0, 0};
-  double gi[3] = {0, 0, 0}, gj[3] = {0, 0, 0}, sr[3] = {0, 0, 0};
-  double E = 0.0, cnt = 0.0;
-  for (int64_t c = c0 + lane; c < c1; c += 32) {
+  double m[SPARSE_NM];
+#pragma unroll
+  for (int k = 0; k < SPARSE_NM; ++k) m[k] = 0.0;
+  double* Ai = m;       // |y_i|^2 I - y_i y_i^T, packed (00,01,02,11,12,22)
+  double* Aj = m + 6;
+  double* M = m + 12;   // y_j y_i^T - (y_i.y_j) I
+  double* Si = m + 21;
+  double* Sj = m + 24;
+  double* gi = m + 27;
+  double* gj = m + 30;
+  double* sr = m + 33;
+  for (int64_t c = c0 + gl; c < c1; c += SPARSE_G) {
     double yi[3], yj[3];
     xf_apply(Ri, ti, a.pts_i[3 * c], a.pts_i[3 * c + 1], a.pts_i[3 * c + 2], yi);
     xf_apply(Rj, tj, a.pts_j[3 * c], a.pts_j[3 * c + 1], a.pts_j[3 * c + 2], yj);
     const double r0 = yi[0] - yj[0], r1 = yi[1] - yj[1], r2 = yi[2] - yj[2];
-    E += r0 * r0 + r1 * r1 + r2 * r2;
+    m[36] += r0 * r0 + r1 * r1 + r2 * r2;
     if (a.world_i) {
       a.world_i[3 * c] = yi[0]; a.world_i[3 * c + 1] = yi[1]; a.world_i[3 * c + 2] = yi[2];
       a.world_j[3 * c] = yj[0]; a.world_j[3 * c + 1] = yj[1]; a.world_j[3 * c + 2] = yj[2];
     }
     if (a.energy_only) continue;
-    cnt += 1.0;
+    m[37] += 1.0;
     Ai[0] += yi[1] * yi[1] + yi[2] * yi[2];
     Ai[1] -= yi[0] * yi[1];
     Ai[2] -= yi[0] * yi[2];
@@ -79,66 +144,31 @@ __global__ void __launch_bounds__(256) k_sparse(SparseArgs a) {
     gj[2] += yj[0] * r1 - yj[1] * r0;
     sr[0] += r0; sr[1] += r1; sr[2] += r2;
   }
-  E = warp_sum(E);
-  double* out = a.set_out + (int64_t)warp * SFB_SET_STRIDE;
+  double* out = a.set_out + (int64_t)set * SFB_SET_STRIDE;
   if (a.energy_only) {
-    if (lane == 0) out[SFB_SET_E] = E;
+    const double E = group_sum(m[36]);
+    if (live && gl == 0) out[SFB_SET_E] = E;
     return;
   }
+  __shared__ double msh[256 / SPARSE_G][SPARSE_NM];
+  double* ms = msh[threadIdx.x / SPARSE_G];
 #pragma unroll
-  for (int k = 0; k < 6; ++k) { Ai[k] = warp_sum(Ai[k]); Aj[k] = warp_sum(Aj[k]); }
-#pragma unroll
-  for (int k = 0; k < 9; ++k) M[k] = warp_sum(M[k]);
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    Si[k] = warp_sum(Si[k]); Sj[k] = warp_sum(Sj[k]);
-    gi[k] = warp_sum(gi[k]); gj[k] = warp_sum(gj[k]); sr[k] = warp_sum(sr[k]);
+  for (int k = 0; k < SPARSE_NM; ++k) {
+    const double t = group_sum(m[k]);
+    if ((k & (SPARSE_G - 1)) == gl) ms[k] = t;
   }
-  cnt = warp_sum(cnt);
-  if (lane != 0) return;
+  __syncwarp();
+  if (!live) return;
   // solver.py:406,414: the J^T J blocks only exist for w_sparse > 0, while the
   // gradient always carries w_sparse (solver.py:644-645).
   const double wg = a.w_sparse;
   const double w = a.w_sparse > 0.0 ? a.w_sparse : 0.0;
-  // blocks, row-major 6x6
-  double* Hii = out;
-  double* Hjj = out + 36;
-  double* Hij = out + 72;
-  const int ai[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
-  for (int r = 0; r < 3; ++r)
-    for (int c = 0; c < 3; ++c) {
-      Hii[r * 6 + c] = w * Ai[ai[r][c]];
-      Hjj[r * 6 + c] = w * Aj[ai[r][c]];
-      Hij[r * 6 + c] = w * M[r * 3 + c];
-      const double eye = (r == c) ? 1.0 : 0.0;
-      Hii[(r + 3) * 6 + (c + 3)] = w * cnt * eye;
-      Hjj[(r + 3) * 6 + (c + 3)] = w * cnt * eye;
-      Hij[(r + 3) * 6 + (c + 3)] = -w * cnt * eye;
-    }
-  // [s]x = [[0,-s2,s1],[s2,0,-s0],[-s1,s0,0]]
-  const double Ki[9] = {0, -Si[2], Si[1], Si[2], 0, -Si[0], -Si[1], Si[0], 0};
-  const double Kj[9] = {0, -Sj[2], Sj[1], Sj[2], 0, -Sj[0], -Sj[1], Sj[0], 0};
-  for (int r = 0; r < 3; ++r)
-    for (int c = 0; c < 3; ++c) {
-      Hii[r * 6 + c + 3] = w * Ki[r * 3 + c];
-      Hii[(r + 3) * 6 + c] = -w * Ki[r * 3 + c];
-      Hjj[r * 6 + c + 3] = w * Kj[r * 3 + c];
-      Hjj[(r + 3) * 6 + c] = -w * Kj[r * 3 + c];
-      Hij[r * 6 + c + 3] = -w * Ki[r * 3 + c];
-      Hij[(r + 3) * 6 + c] = w * Kj[r * 3 + c];
-    }
-  for (int k = 0; k < 3; ++k) {
-    out[SFB_SET_GI + k] = wg * gi[k];
-    out[SFB_SET_GI + 3 + k] = wg * sr[k];
-    out[SFB_SET_GJ + k] = -wg * gj[k];
-    out[SFB_SET_GJ + 3 + k] = -wg * sr[k];
-  }
-  out[SFB_SET_E] = E;
+  for (int e = gl; e <= SFB_SET_E; e += SPARSE_G) out[e] = sparse_entry(e, ms, w, wg);
 }
 
 void launch_sparse(const SparseArgs& a, cudaStream_t s) {
   if (a.n_sets <= 0) return;
-  const int blocks = (a.n_sets * 32 + 255) / 256;
+  const int blocks = (a.n_sets * SPARSE_G + 255) / 256;
   sfb_count_launch();
   k_sparse<<<blocks, 256, 0, s>>>(a);
 }
