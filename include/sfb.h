@@ -341,6 +341,23 @@ int sfb_set_preconditioner(sfb_problem* p, int32_t kind);
  * with bit-identical systems; the PCG then runs replicated.
  * The single-call forms above return SFB_E_STATE on a sharded problem. */
 int sfb_set_shard(sfb_problem* p, int32_t rank, int32_t world);
+
+/* Sharded-PCG mode: mode 1 keeps each rank's system
+ * PARTIAL - its own directed edges, and the correspondence sets on rank 0 -
+ * instead of exchanging the per-edge sums (mode 0, default).  A
+ * linearisation is then sfb_linearize_begin (exchange mask 0) ->
+ * sfb_linearize_end_system -> sum exchange buffer 3 ([g | Jacobi diagonal |
+ * dense energies | diagonal blocks when block-Jacobi]) -> sfb_linearize_finish,
+ * and the PCG is sfb_pcg_sharded: per iteration one all-reduce of the
+ * n_vars partial A.p through the caller's callback, which must sum the
+ * device buffer across ranks in place, ordered on `stream`, and return 0.
+ * Every rank then runs pcg_solve's scalar recurrence on identical bits. */
+typedef int (*sfb_allreduce_fn)(void* user, double* dev_buf, int64_t n, void* stream);
+int sfb_set_shard_mode(sfb_problem* p, int32_t mode);
+int sfb_linearize_end_system(sfb_problem* p);
+int sfb_linearize_finish(sfb_problem* p, double e3[3]);
+int sfb_pcg_sharded(sfb_problem* p, int32_t max_it, double tol, int32_t restart,
+                    sfb_allreduce_fn fn, void* user, int32_t* iters, double* rel, int32_t* status);
 int sfb_exchange_buffer(sfb_problem* p, int32_t which, void** dev_ptr, int64_t* bytes);
 int sfb_build_dense_edges_begin(sfb_problem* p, double view_cos_min);
 int sfb_build_dense_edges_end(sfb_problem* p, int64_t* n_edges);

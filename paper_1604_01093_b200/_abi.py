@@ -75,6 +75,8 @@ _I32 = C.c_int32
 _I64 = C.c_int64
 _D = C.c_double
 _PD = C.POINTER(C.c_double)
+# sfb_allreduce_fn (include/sfb.h): sum a device buffer across ranks in place
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
 
 # name -> argtypes (all return int status except the two noted)
 SIGNATURES = {
@@ -118,6 +120,11 @@ SIGNATURES = {
     "sfb_set_shard": [_P, _I32, _I32],
     "sfb_set_preconditioner": [_P, _I32],
     "sfb_problem_drop_sets": [_P, _I64, _P],
+    "sfb_set_shard_mode": [_P, _I32],
+    "sfb_linearize_end_system": [_P],
+    "sfb_linearize_finish": [_P, _P],
+    "sfb_pcg_sharded": [_P, _I32, _D, _I32, ALLREDUCE_FN, _P, C.POINTER(_I32), C.POINTER(_D),
+                        C.POINTER(_I32)],
     "sfb_exchange_buffer": [_P, _I32, C.POINTER(_P), C.POINTER(_I64)],
     "sfb_build_dense_edges_begin": [_P, _D],
     "sfb_build_dense_edges_end": [_P, C.POINTER(_I64)],

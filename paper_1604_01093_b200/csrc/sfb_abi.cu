@@ -81,6 +81,9 @@ struct sfb_problem : Handle {
   bool pending_energy_dense = false;
   // data-parallel sharding over directed dense edges
   int shard_rank = 0, shard_world = 1;
+  int shard_mode = 0;            // 0: exchange per-edge sums; 1: partial systems + sharded PCG
+  DBuf<double> xsys;             // mode 1: packed [g | jdiag | dense energies | D]
+  DBuf<double> pcgs_state;       // mode 1: PCG scalars (sfb_pcg_sharded)
   int n_cand = 0;                // pair-filter candidates of the last filter pass
   int last_do_photo = 0, last_do_geo = 0;
   // system
@@ -187,7 +190,9 @@ int rebuild_structure(sfb_problem* p, int bidir) {
   cudaStream_t s = p->stream;
   const int n_e = (int)p->edges.size();
   const int n_dir = n_e * (bidir ? 2 : 1);
-  const int n_units = p->n_sets + n_dir;
+  // sharded PCG mode: the correspondence sets belong to rank 0's partial system
+  const int n_sets_s = (p->shard_mode == 1 && p->shard_world > 1 && p->shard_rank != 0) ? 0 : p->n_sets;
+  const int n_units = n_sets_s + n_dir;
   p->n_dir = n_dir;
   if ((int64_t)nb * (nb + 1) >= ((int64_t)1 << 32) - 1)
     return fail(p, SFB_E_ARG, "too many frames for 32-bit structure keys");
@@ -200,8 +205,8 @@ int rebuild_structure(sfb_problem* p, int bidir) {
   for (const FrameDev& F : p->frames_h) max_nt = std::max(max_nt, F.tiles_x * F.tiles_y);
   const int64_t items_bound =
       (int64_t)n_dir * std::max((target + std::max(1, n_dir) - 1) / std::max(1, n_dir), (max_nt + 1023) / 1024) + 1;
-  const int64_t nd_bound = 3 * (int64_t)p->n_sets + 2 * (int64_t)n_dir;  // D entries
-  const int64_t np_bound = (int64_t)p->n_sets + n_dir;                     // B entries >= pairs
+  const int64_t nd_bound = 3 * (int64_t)n_sets_s + 2 * (int64_t)n_dir;  // D entries
+  const int64_t np_bound = (int64_t)n_sets_s + n_dir;                     // B entries >= pairs
   const int64_t nh_bound = nb + 2 * np_bound;                               // row slots
   auto& sc = p->sc;
   CK(p, upload_vec(p->edges_d, p->edges, s));
@@ -259,7 +264,7 @@ int rebuild_structure(sfb_problem* p, int bidir) {
   // contribution lists: sets in set order, then directed edges; stable
   // sorts keep that order within a variable / pair.  Unused tail keys are
   // 0xFFFFFFFF (after every real key).
-  launch_struct_count(p->set_fi.p, p->set_fj.p, p->set_off.p, p->set_end.p, p->n_sets,
+  launch_struct_count(p->set_fi.p, p->set_fj.p, p->set_off.p, p->set_end.p, n_sets_s,
                       p->dir_edges.p, n_dir, sc.dcount.p, sc.bcount.p, s);
   CKL(p);
   CK(p, cub_call(sc.temp, s, [&](void* t, size_t& b) {
@@ -270,7 +275,7 @@ int rebuild_structure(sfb_problem* p, int bidir) {
   }));
   CK(p, cudaMemsetAsync(sc.dkey.p, 0xFF, sizeof(unsigned) * std::max<int64_t>(1, nd_bound), s));
   CK(p, cudaMemsetAsync(sc.bkey.p, 0xFF, sizeof(unsigned) * std::max<int64_t>(1, np_bound), s));
-  launch_struct_fill(p->set_fi.p, p->set_fj.p, p->set_off.p, p->set_end.p, p->n_sets,
+  launch_struct_fill(p->set_fi.p, p->set_fj.p, p->set_off.p, p->set_end.p, n_sets_s,
                      p->dir_edges.p, n_dir, nb, sc.doff.p, sc.boff.p, sc.dkey.p, sc.dval.p, sc.bkey.p,
                      sc.bval.p, s);
   CKL(p);
@@ -950,6 +955,8 @@ int sfb_problem_destroy(sfb_problem* p) {
   for (auto* b : db) b->release();
   p->pair_key.release();
   p->edges_d.release();
+  p->xsys.release();
+  p->pcgs_state.release();
   {
     auto& sc = p->sc;
     DBuf<int>* si[] = {&sc.icount, &sc.per, &sc.dcount, &sc.bcount, &sc.doff, &sc.boff, &sc.dval,
@@ -1766,7 +1773,99 @@ int sfb_linearize_begin(sfb_problem* p, const sfb_weights* w, double w_dense, co
   CK(p, cudaSetDevice(p->ctx->device));
   int rc = enqueue_linearize(p, w, w_dense, cfg);
   if (rc) return rc;
-  *exchange = p->pending_dense_on ? 1 : 0;
+  *exchange = (p->pending_dense_on && p->shard_mode == 0) ? 1 : 0;
+  return SFB_OK;
+}
+
+// Sharded-PCG mode: assemble this rank's partial system and pack
+// [g | jdiag | e_photo e_geo | D (block Jacobi)] into exchange buffer 3.
+int sfb_linearize_end_system(sfb_problem* p) {
+  if (!p) return fail(p, SFB_E_ARG, "null problem");
+  if (p->shard_mode != 1) return fail(p, SFB_E_STATE, "not in sharded-PCG mode");
+  CK(p, cudaSetDevice(p->ctx->device));
+  const int saved = p->precond;
+  p->precond = 0;  // the block inverses need the reduced D (sfb_linearize_finish)
+  int rc = enqueue_linearize_end(p);
+  p->precond = saved;
+  if (rc) return rc;
+  const int n6 = 6 * p->n_blk;
+  CK(p, p->xsys.ensure((size_t)sys_pack_len(n6, 1), p->stream));
+  launch_sys_pack(p->g.p, p->jdiag.p, p->dscal.p, p->D.p, n6, p->precond, p->xsys.p, 0, p->stream);
+  CKL(p);
+  return SFB_OK;
+}
+
+// ... after the all-reduce of buffer 3: unpack, block inverses, energies.
+int sfb_linearize_finish(sfb_problem* p, double e3[3]) {
+  if (!p || !e3) return fail(p, SFB_E_ARG, "null argument");
+  if (p->shard_mode != 1) return fail(p, SFB_E_STATE, "not in sharded-PCG mode");
+  CK(p, cudaSetDevice(p->ctx->device));
+  const int n6 = 6 * p->n_blk;
+  launch_sys_pack(p->g.p, p->jdiag.p, p->dscal.p, p->D.p, n6, p->precond, p->xsys.p, 1, p->stream);
+  CKL(p);
+  if (p->precond && p->n_blk > 0) {
+    CK(p, p->bj_inv.ensure((size_t)p->n_blk * 36, p->stream));
+    launch_block_jacobi_inv(p->D.p, p->jdiag.p, p->n_blk, p->bj_inv.p, p->stream);
+    CKL(p);
+  }
+  CK(p, cudaMemcpyAsync(p->hscal, p->dscal.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+  CK(p, cudaStreamSynchronize(p->stream));
+  for (int k = 0; k < 3; ++k) e3[k] = p->hscal[k];
+  return SFB_OK;
+}
+
+// PCG over the partial systems (sfb_pcg_sharded.cu): per iteration the
+// caller's fn all-reduces (sums) the n_vars partial A.p in place on `stream`.
+int sfb_pcg_sharded(sfb_problem* p, int32_t max_it, double tol, int32_t restart,
+                    sfb_allreduce_fn fn, void* user, int32_t* iters, double* rel, int32_t* status) {
+  if (!p || !fn || !iters || !rel || !status) return fail(p, SFB_E_ARG, "null argument");
+  if (!p->have_system) return fail(p, SFB_E_STATE, "pcg before linearize");
+  if (restart < 1) return fail(p, SFB_E_ARG, "pcg_restart_interval must be >= 1");
+  CK(p, cudaSetDevice(p->ctx->device));
+  cudaStream_t s = p->stream;
+  PcgArgs a = pcg_args(p);
+  a.max_it = max_it;
+  a.tol = tol;
+  a.restart = restart;
+  const int n6 = 6 * p->n_blk;
+  CK(p, p->pcgs_state.ensure(8, s));
+  double* st = p->pcgs_state.p;
+  p->spec_pcg = false;
+  if (p->n_blk > 0) {
+    ProfScope ps(p->prof, 2, s);
+    launch_pcgs_init(a, st, s);
+    CKL(p);
+    for (int k = 1; k <= max_it; ++k) {
+      const int rs = (k % restart) == 0 ? 1 : 0;
+      launch_matvec(a, a.p, a.Ap, s);
+      CKL(p);
+      if (fn(user, a.Ap, n6, (void*)s) != 0) return fail(p, SFB_E_CUDA, "all-reduce callback failed");
+      launch_pcgs_step(a, st, k, rs, s);
+      CKL(p);
+      if (rs) {
+        launch_matvec(a, a.x, a.Ap, s);
+        CKL(p);
+        if (fn(user, a.Ap, n6, (void*)s) != 0) return fail(p, SFB_E_CUDA, "all-reduce callback failed");
+        launch_pcgs_restart(a, st, s);
+        CKL(p);
+      }
+      if ((k & 7) == 0 || k == max_it) {  // stop early once every rank is done
+        CK(p, cudaMemcpyAsync(p->hscal + 24, st, 8 * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(p, cudaStreamSynchronize(s));
+        if (p->hscal[24 + 6] != 0.0) break;
+      }
+    }
+    CK(p, cudaMemcpyAsync(p->hscal + 24, st, 8 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(p, cudaStreamSynchronize(s));
+    *iters = (int32_t)p->hscal[24 + 4];
+    *rel = p->hscal[24 + 3];
+    *status = p->hscal[24 + 5] != 0.0 ? SFB_E_PCG_NONFINITE : SFB_OK;
+  } else {
+    *iters = 0;
+    *rel = 0.0;
+    *status = SFB_OK;
+  }
+  p->have_solution = true;
   return SFB_OK;
 }
 
@@ -1862,6 +1961,14 @@ int sfb_set_preconditioner(sfb_problem* p, int32_t kind) {
   return SFB_OK;
 }
 
+int sfb_set_shard_mode(sfb_problem* p, int32_t mode) {
+  if (!p || mode < 0 || mode > 1) return fail(p, SFB_E_ARG, "shard mode must be 0 or 1");
+  CK(p, cudaSetDevice(p->ctx->device));
+  if (mode == p->shard_mode) return SFB_OK;
+  p->shard_mode = mode;
+  return rebuild_structure(p, p->struct_bidir < 0 ? 0 : p->struct_bidir);
+}
+
 int sfb_exchange_buffer(sfb_problem* p, int32_t which, void** dev_ptr, int64_t* bytes) {
   if (!p || !dev_ptr || !bytes) return fail(p, SFB_E_ARG, "null argument");
   switch (which) {
@@ -1876,6 +1983,10 @@ int sfb_exchange_buffer(sfb_problem* p, int32_t which, void** dev_ptr, int64_t* 
     case 2:
       *dev_ptr = p->f_pass.p;
       *bytes = p->n_cand;
+      return SFB_OK;
+    case 3:
+      *dev_ptr = p->xsys.p;
+      *bytes = (int64_t)sys_pack_len(6 * p->n_blk, p->precond) * (int64_t)sizeof(double);
       return SFB_OK;
     default:
       return fail(p, SFB_E_ARG, "unknown exchange buffer");

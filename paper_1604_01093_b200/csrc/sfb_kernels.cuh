@@ -205,6 +205,14 @@ void launch_rows_keys(const unsigned* pair_key, const int* n_pairs_d, int nb, in
                       unsigned* hkey, int* hval, cudaStream_t s);
 void launch_rows_out(const unsigned* hkey, const int* hval, const int* n_pairs_d, int nb, int n_max,
                      int* row_ptr, int* row_col, int* pair_slot, cudaStream_t s);
+// sharded PCG (sfb_pcg_sharded.cu)
+void launch_pcgs_init(const PcgArgs& a, double* st, cudaStream_t s);
+void launch_pcgs_step(const PcgArgs& a, double* st, int k, int restart, cudaStream_t s);
+void launch_pcgs_restart(const PcgArgs& a, double* st, cudaStream_t s);
+int sys_pack_len(int n6, int with_d);
+void launch_sys_pack(double* g, double* jdiag, double* dscal, double* D, int n6, int with_d,
+                     double* buf, int unpack, cudaStream_t s);
+void launch_matvec(const PcgArgs& a, const double* xin, double* yout, cudaStream_t s);
 void launch_edge_reduce2(const int* edge_item_ptr, const double* item_e2, double* edge_e2, int n_dir,
                          cudaStream_t s);
 void launch_edge_reduce(const int* edge_item_ptr, const double* item_out, double* edge_out,

@@ -169,6 +169,46 @@ class DeviceProblem:
     def set_shard(self, rank: int, world: int) -> None:
         self._ck(self.lib.sfb_set_shard(self.handle, int(rank), int(world)))
 
+    def set_shard_mode(self, mode: int) -> None:
+        """0: exchange per-edge sums, replicated PCG; 1: partial systems and the
+        sharded PCG (one all-reduce of A.p per iteration)."""
+        self._ck(self.lib.sfb_set_shard_mode(self.handle, int(mode)))
+        self.shard_mode = int(mode)
+
+    def linearize_sharded(self, weights, w_dense, config, exchange) -> np.ndarray:
+        """Sharded-PCG linearisation: this rank's partial system, then one
+        all-reduce of [g | Jacobi diagonal | dense energies (| D)]."""
+        e = np.zeros(3)
+        w, cfg = self._w(weights), self._cfg(config)
+        mask = C.c_int32()
+        self._ck(self.lib.sfb_linearize_begin(self.handle, C.byref(w), C.c_double(w_dense),
+                                              C.byref(cfg), C.byref(mask)))
+        self._exchange(exchange, mask.value)
+        self._ck(self.lib.sfb_linearize_end_system(self.handle))
+        exchange(self, 3)
+        self._ck(self.lib.sfb_linearize_finish(self.handle, _abi.ptr(e)))
+        self.version += 1
+        return e
+
+    def pcg_sharded(self, max_iterations, tolerance, restart_interval, allreduce):
+        """PCG over the partial systems; `allreduce(ptr, n, stream)` sums the
+        n-double device buffer across ranks in place on `stream`."""
+        def cb(_user, ptr, n, stream):
+            try:
+                allreduce(int(ptr), int(n), int(stream or 0))
+                return 0
+            except Exception:  # reported as an SfbError by the library
+                import traceback
+                traceback.print_exc()
+                return 1
+        fn = _abi.ALLREDUCE_FN(cb)
+        it, st = C.c_int32(), C.c_int32()
+        rel = C.c_double()
+        self._ck(self.lib.sfb_pcg_sharded(self.handle, int(max_iterations), C.c_double(tolerance),
+                                          int(restart_interval), fn, None, C.byref(it),
+                                          C.byref(rel), C.byref(st)))
+        return it.value, rel.value, st.value
+
     def exchange_buffer(self, which: int):
         """(device pointer, bytes) of exchange buffer `which` (0 per-edge
         linearisation sums f64, 1 per-edge frozen energies f64, 2 filter
@@ -176,6 +216,8 @@ class DeviceProblem:
         ptr, nb = C.c_void_p(), C.c_int64()
         self._ck(self.lib.sfb_exchange_buffer(self.handle, int(which), C.byref(ptr), C.byref(nb)))
         return ptr.value or 0, nb.value
+
+    shard_mode = 0
 
     def _exchange(self, exchange, mask: int) -> None:
         for which in (0, 1):

@@ -2,12 +2,18 @@
 
 One process per GPU (torchrun).  Every rank holds the full frame store and
 the full problem; rank r owns every world-th directed dense edge and every
-world-th frame-pair filter candidate.  The only collectives are the sums of
-the per-edge exchange buffers after each dense pass (and of the filter pass
-flags once per solve).  Each buffer entry has exactly one owning rank, so the
-sum is exact: every rank ends with the bit-identical block system and runs
-the same replicated PCG - no per-PCG-iteration communication and no
-control-flow divergence between ranks.
+world-th frame-pair filter candidate.  Two PCG modes:
+
+* ``pcg="replicated"`` (default): the per-edge sums of each dense pass are
+  summed across ranks (each entry has exactly one owning rank, so the sum is
+  exact), every rank assembles the bit-identical block system and runs the
+  same PCG - no per-PCG-iteration communication.
+* ``pcg="sharded"``: each rank keeps only its partial system
+  (its edges; the correspondence sets on rank 0); one all-reduce of
+  [gradient | Jacobi diagonal | dense energies] per linearisation and one of
+  the partial A.p per PCG iteration; the PCG scalars are then computed
+  redundantly on identical bits.  The summation order of the partial systems
+  differs from a single GPU's, so results agree to rounding, not bitwise.
 
 Usage:
     comm = ShardComm()                      # after dist.init_process_group
@@ -20,7 +26,8 @@ from __future__ import annotations
 import numpy as np
 
 # dtype of each exchange buffer (include/sfb.h: sfb_exchange_buffer)
-EXCHANGE_DTYPES = {0: "f8", 1: "f8", 2: "u1"}
+EXCHANGE_DTYPES = {0: "f8", 1: "f8", 2: "u1", 3: "f8"}
+PCG_MODES = ("replicated", "sharded")
 
 
 class _CudaView:
@@ -37,10 +44,13 @@ class _CudaView:
 class ShardComm:
     """Sums exchange buffers across the ranks of a torch.distributed group."""
 
-    def __init__(self, group=None):
+    def __init__(self, group=None, pcg: str = "replicated"):
         import torch.distributed as dist
+        if pcg not in PCG_MODES:
+            raise ValueError(f"pcg must be one of {PCG_MODES}")
         self._dist = dist
         self.group = group
+        self.pcg = pcg
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
 
@@ -61,11 +71,29 @@ class ShardComm:
         ptr, nbytes = dp.exchange_buffer(which)
         if nbytes == 0:
             return
+        self.allreduce_device(ptr, nbytes, typestr, dp.stream_ptr())
+
+    def allreduce_device(self, ptr: int, nbytes: int, typestr: str, stream: int) -> None:
+        """In-place sum of a device buffer across ranks, ordered on `stream`."""
+        import torch
         dev = torch.device("cuda", torch.cuda.current_device())
         t = torch.as_tensor(_CudaView(ptr, nbytes, typestr), device=dev)
-        # enqueue on the solver's stream so the collective orders with its kernels
-        with torch.cuda.stream(torch.cuda.ExternalStream(dp.stream_ptr(), device=dev)):
+        with torch.cuda.stream(torch.cuda.ExternalStream(stream, device=dev)):
             self._dist.all_reduce(t, op=self._dist.ReduceOp.SUM, group=self.group)
+
+    def pcg_allreduce(self, dp):
+        """The per-PCG-iteration collective of the sharded mode: A.p (n doubles)."""
+        if hasattr(dp, "exchange_array"):  # host-memory problem (CPU / gloo): numpy in place
+            import torch
+
+            def host(arr) -> None:
+                self._dist.all_reduce(torch.from_numpy(arr), op=self._dist.ReduceOp.SUM,
+                                      group=self.group)
+            return host
+
+        def fn(ptr: int, n: int, stream: int) -> None:
+            self.allreduce_device(ptr, 8 * n, "f8", stream)
+        return fn
 
 
 def owned_edges(n_directed: int, rank: int, world: int) -> np.ndarray:

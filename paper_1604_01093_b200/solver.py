@@ -676,6 +676,7 @@ class AlignmentProblem:
         self._device = device
         # data-parallel sharding over frame pairs (paper_1604_01093_b200.shard)
         self._xch = comm if (comm is not None and comm.world > 1) else None
+        self._sharded_pcg = self._xch is not None and getattr(comm, "pcg", "replicated") == "sharded"
         self._dp = None
         self._dp_edges = None
 
@@ -742,6 +743,8 @@ class AlignmentProblem:
                                              device=self._device)
             if self._xch is not None:
                 self._dp.set_shard(self._xch.rank, self._xch.world)
+                if self._sharded_pcg:
+                    self._dp.set_shard_mode(1)
         return self._dp
 
     def _push_poses(self):
@@ -821,6 +824,8 @@ class AlignmentProblem:
             self._sync_edges()
         have_edges = len(pairs) > 0 if self.caches is not None else bool(self.dense_edges)
         tr.mark("filter")
+        if self._sharded_pcg:
+            return self._solve_sharded_pcg(dp, weights, config, max_iterations, have_edges, stats, tr)
         best_energy = np.inf
         dp.save_best()
         consecutive_increases = 0
@@ -883,6 +888,71 @@ class AlignmentProblem:
         tr.mark("pull")
         tr.report()
         return stats
+
+
+def _solve_sharded_pcg_loop(self, dp, weights, config, max_iterations, have_edges, stats, tr):
+    """GN loop of the sharded-PCG mode (ShardComm(pcg="sharded")):
+    the reference's control flow (solver.py:681-750) over partial systems -
+    one all-reduce per linearisation and frozen-energy pass, one per PCG
+    iteration (in sfb_pcg_sharded)."""
+    xch = self._xch
+    allreduce = xch.pcg_allreduce(dp)
+    best_energy = np.inf
+    dp.save_best()
+    consecutive_increases = 0
+    moved = False
+    for it in range(max_iterations):
+        w_dense = dense_ramp_weight(weights, it)
+        e = dp.linearize_sharded(weights, w_dense, config, xch)
+        dense_on = self.caches is not None and w_dense > 0.0 and have_edges
+        energy_before = weights.sparse * float(e[0])
+        if dense_on:
+            energy_before += w_dense * (weights.photo * float(e[1]) + weights.geo * float(e[2]))
+        if energy_before <= 1e-18:
+            stats.converged = True
+            stats.iterations.append(IterationRecord(
+                it, energy_before, energy_before, w_dense, 0, 0.0, 0.0, True))
+            break
+        pcg_it, pcg_rel, st = dp.pcg_sharded(config.pcg_max_iterations, config.pcg_tolerance,
+                                             config.pcg_restart_interval, allreduce)
+        if st == _abi.SFB_E_PCG_NONFINITE:
+            stats.aborted = True
+            break
+        step_norm = dp.apply_step()
+        moved = True
+        ea = dp.energy_frozen(w_dense > 0.0, exchange=xch)
+        tr.mark("pcg+step+energy")
+        energy_after = weights.sparse * float(ea[0])
+        if w_dense > 0.0:
+            energy_after += w_dense * (weights.photo * float(ea[1]) + weights.geo * float(ea[2]))
+        accepted = energy_after <= energy_before
+        stats.iterations.append(IterationRecord(
+            it, energy_before, energy_after, w_dense, pcg_it, pcg_rel, step_norm, accepted))
+        if accepted:
+            consecutive_increases = 0
+        else:
+            consecutive_increases += 1
+            if consecutive_increases >= 2:
+                dp.restore_best()
+                stats.aborted = True
+                break
+        if energy_after < best_energy:
+            best_energy = energy_after
+            dp.save_best()
+        if accepted and (energy_before - energy_after) < config.min_relative_decrease * max(
+                energy_before, 1e-30):
+            stats.converged = True
+            break
+    else:
+        stats.converged = True
+    if moved:
+        self._pull_poses()
+    tr.mark("pull")
+    tr.report()
+    return stats
+
+
+AlignmentProblem._solve_sharded_pcg = _solve_sharded_pcg_loop
 
 
 class _Tracer:

@@ -128,3 +128,133 @@ def test_ownership_partition():
     n, world = 103, 4
     parts = [owned_edges(n, r, world) for r in range(world)]
     assert sorted(np.concatenate(parts).tolist()) == list(range(n))
+
+
+# ---------------------------------------------------------------------------
+# Sharded-PCG protocol (ShardComm(pcg="sharded")): partial
+# systems (own edges; the sparse sets on rank 0), one all-reduce of
+# [g | diag] per linearisation and one of A.p per PCG iteration.
+
+
+def _partial_system(scene, edge_out, edges, rank, world, with_sparse):
+    """Dense n_vars^2 partial normal equations of one rank (host mirror of
+    k_assemble over the rank's own directed edges, solver.py:615-628)."""
+    ids = scene.ids
+    var = {f: k - 1 for k, f in enumerate(ids)}
+    nv = 6 * (len(ids) - 1)
+    A = np.zeros((nv, nv))
+    g = np.zeros(nv)
+    for d, (i, j) in enumerate(edges):
+        if d % world != rank:
+            continue
+        e = edge_out[d]
+        H = np.zeros((6, 6))
+        k = 0
+        for r in range(6):
+            for c in range(r, 6):
+                H[r, c] = H[c, r] = e[k]
+                k += 1
+        ge = e[21:27]
+        vi, vj = var[i], var[j]
+        if vi >= 0:
+            A[6 * vi:6 * vi + 6, 6 * vi:6 * vi + 6] += H
+            g[6 * vi:6 * vi + 6] += ge
+        if vj >= 0:
+            A[6 * vj:6 * vj + 6, 6 * vj:6 * vj + 6] += H
+            g[6 * vj:6 * vj + 6] -= ge
+        if vi >= 0 and vj >= 0:
+            A[6 * vi:6 * vi + 6, 6 * vj:6 * vj + 6] -= H
+            A[6 * vj:6 * vj + 6, 6 * vi:6 * vi + 6] -= H
+    if with_sparse:
+        P = O.Problem(ids, {f: O.pose_of(p) for f, p in scene.init.items()}, scene.corr_sets, None)
+        S_, _, _ = P.linearize(O.DEFAULT_W, 0.0, O.DEFAULT_CFG)
+        S_.dense = np.zeros((nv, nv))
+        A += np.stack([S_.apply(col) for col in np.eye(nv)], axis=1)
+        g += S_.gradient
+    return A, g
+
+
+def pcg_sharded_host(A_r, g_r, allreduce, max_it=50, tol=1e-6, restart=20):
+    """pcg_solve's recurrence (solver.py:463-508) over a partial system: the
+    gradient / diagonal once and A.p every iteration are all-reduced."""
+    gd = np.concatenate([g_r, np.diag(A_r).copy()])
+    allreduce(gd)
+    n = g_r.shape[0]
+    b, diag = -gd[:n], gd[n:]
+    inv = 1.0 / np.maximum(diag, 1e-12)
+    x = np.zeros(n)
+    r = b.copy()
+    z = inv * r
+    p = z.copy()
+    rz = float(r @ z)
+    nb = float(np.sqrt(b @ b))
+    it, rel = 0, 1.0
+    for k in range(1, max_it + 1):
+        it = k
+        q = A_r @ p
+        allreduce(q)
+        pAp = float(p @ q)
+        if pAp <= 0.0:
+            break
+        alpha = rz / pAp
+        x = x + alpha * p
+        if k % restart == 0:
+            q2 = A_r @ x
+            allreduce(q2)
+            r = b - q2
+        else:
+            r = r - alpha * q
+        z = inv * r
+        rel = float(np.sqrt(r @ r)) / nb
+        if rel < tol:
+            break
+        rzn = float(r @ z)
+        p = z + (rzn / rz) * p
+        rz = rzn
+    return x, it, rel
+
+
+def _pcg_worker(rank, world, port, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1604_01093_b200.shard import ShardComm
+        comm = ShardComm(pcg="sharded")
+        scene = GoldenScene("cfg2")
+        hp = HostShardProblem(scene, comm.rank, comm.world)
+        edges = hp.build_dense_edges(comm)
+        hp.edge_out = np.zeros((len(edges), 32))
+        eo = hp.linearize(1.0, None)  # own edges only: no exchange of the per-edge sums
+        A_r, g_r = _partial_system(scene, eo, edges, rank, world, with_sparse=rank == 0)
+        x, it, rel = pcg_sharded_host(A_r, g_r, comm.pcg_allreduce(hp))
+        out_q.put((rank, x, it, rel, int(np.count_nonzero(A_r))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_sharded_pcg_protocol():
+    import torch.multiprocessing as mp
+    scene = GoldenScene("cfg2")
+    full = HostShardProblem(scene)
+    edges = full.build_dense_edges(None)
+    eo = full.linearize(1.0, None)
+    A, g = _partial_system(scene, eo, edges, 0, 1, with_sparse=True)
+    x_ref, it_ref, rel_ref = pcg_sharded_host(A, g, lambda v: None)
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pcg_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=280) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (_, x0, it0, rel0, nz0), (_, x1, it1, rel1, nz1) = res
+    assert np.array_equal(x0, x1) and it0 == it1 and rel0 == rel1  # identical on every rank
+    assert nz0 > 0 and nz1 > 0 and nz0 != nz1                       # really partial systems
+    assert it0 == it_ref
+    assert np.linalg.norm(x0 - x_ref) <= 1e-9 * np.linalg.norm(x_ref)
