@@ -13,8 +13,10 @@ step and the poses read back.  The CPU baseline is the oracle port timed on
 a bounded sample of the same workload and extrapolated to a full solve.
 
 Multi-GPU (torchrun, one process per GPU): the same solve sharded over frame
-pairs (strong scaling); one exact NCCL all-reduce of the per-edge sums per
-dense pass, replicated PCG.
+pairs (strong scaling).  --pcg replicated (default): one exact NCCL
+all-reduce of the per-edge sums per dense pass, replicated PCG; --pcg
+sharded: partial systems, one all-reduce of A.p per PCG iteration
+(DESIGN.md section 6).
 """
 
 from __future__ import annotations
@@ -53,6 +55,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo lets several ranks share one GPU (protocol test only)")
+    ap.add_argument("--pcg", default="replicated", choices=["replicated", "sharded"],
+                    help="multi-GPU PCG: replicated system (per-edge sums exchanged once per "
+                         "dense pass) or sharded partial systems (one all-reduce of A.p per "
+                         "PCG iteration, SURVEY.md 8(e))")
     return ap.parse_args()
 
 
@@ -479,7 +485,7 @@ def main():
     comm = None
     if world > 1:
         from paper_1604_01093_b200.shard import ShardComm
-        comm = ShardComm()  # frame-pair sharding: one exact all-reduce per dense pass
+        comm = ShardComm(pcg=args.pcg)  # frame-pair sharding
     problem = S.AlignmentProblem(ids, scene.init, scene.corr_sets, caches, comm=comm)
     problem.solve(W, C)  # uploads + first solve (warm-up 0)
     dp = problem._dp
@@ -581,7 +587,8 @@ def main():
                    "resolution": list(scene.low_size), "dense_edges": n_edges,
                    "correspondences": n_corr, "n_vars": nv, "gn_iterations": len(records),
                    "pcg_iterations": pcg_iters, "l2": "flushed (384 MB write) between steps",
-                   "parallelism": f"frame-pair shards x{world}" if world > 1 else "single"},
+                   "parallelism": (f"frame-pair shards x{world}, {args.pcg} PCG" if world > 1
+                                   else "single")},
         "roofline": {"bound": "hbm", "kernel": "k_dense_fused",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if peak else None, "traffic": traffic,
