@@ -458,10 +458,59 @@ __device__ __forceinline__ void rset(double (&a)[PCG_RMAX], int j, double v) {
   for (int k = 0; k < PCG_RMAX; ++k) a[k] = (k == j) ? v : a[k];
 }
 
-template <class Mv>
+// Single-cluster synchronisation for small systems (the whole grid is one
+// thread-block cluster of <= 16 CTAs, cfg1-3): a reduction is each CTA's
+// block totals stored into EVERY CTA's shared memory (DSMEM, slot = rank)
+// followed by one hardware cluster barrier (release/acquire at cluster scope,
+// which also publishes the p / z / x writes the neighbours gather from
+// global memory); each CTA then sums the G slots in rank order - identical
+// bits everywhere.  Slots alternate between two buffers: a CTA writes
+// reduction e + 1 only after the barrier of e, and e + 2 only after every CTA
+// passed the barrier of e + 1, i.e. finished reading e.
+#define PCG_CLUSTER_MAX 16
+struct ClusterSync {
+  double (*slot)[PCG_CLUSTER_MAX][4];  // [2][rank][value], shared memory
+  unsigned epoch;
+  __device__ __forceinline__ void barrier() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  }
+  template <int NV>
+  __device__ __forceinline__ void allsum(double (&v)[NV], double (*sh)[PCG_WARPS], int G) {
+    block_allsum<NV>(v, sh);  // thread 0: this CTA's totals
+    const int buf = epoch & 1u;
+    ++epoch;
+    if (threadIdx.x < G) {  // thread t stores this CTA's totals into CTA t
+      uint32_t rank;
+      asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+      const uint32_t local = (uint32_t)__cvta_generic_to_shared(&slot[buf][rank][0]);
+      uint32_t remote;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"((uint32_t)threadIdx.x));
+      __shared__ double tot[4];
+      if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) tot[k] = v[k];
+      }
+      __syncwarp((1u << G) - 1u);  // lanes 0 .. G-1 of warp 0
+#pragma unroll
+      for (int k = 0; k < NV; ++k)
+        asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(remote + 8 * k), "d"(tot[k]) : "memory");
+    }
+    barrier();
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      double t = 0.0;
+      for (int b = 0; b < G; ++b) t += slot[buf][b][k];
+      v[k] = t;
+    }
+  }
+};
+
+template <class Mv, bool CL>
 __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg_reg(PcgArgs a, Mv mv, int rows_per_cta) {
   extern __shared__ __align__(16) double smem[];
   GridBarrier grid{reinterpret_cast<unsigned*>(a.flags), 0u};
+  __shared__ double cl_slot[2][PCG_CLUSTER_MAX][4];
+  ClusterSync csync{cl_slot, 0u};
   __shared__ double sh[4][PCG_WARPS];
   const int G = gridDim.x;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -501,6 +550,7 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg_reg(PcgArgs a, Mv mv, in
   double* partB = a.part + G;
 
   // ---- setup (solver.py:472-481)
+  double tot[2];
   {
     double v[2] = {0.0, 0.0};
     for (int j = 0; j < nrow; ++j) {
@@ -524,12 +574,19 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg_reg(PcgArgs a, Mv mv, in
       v[0] += sum6(bb);
       v[1] += sum6(bz);
     }
-    block_allsum<2>(v, sh);
-    if (threadIdx.x == 0) { partB[blockIdx.x] = v[0]; partB[G + blockIdx.x] = v[1]; }
+    if constexpr (CL) {
+      csync.allsum<2>(v, sh, G);
+      tot[0] = v[0];
+      tot[1] = v[1];
+    } else {
+      block_allsum<2>(v, sh);
+      if (threadIdx.x == 0) { partB[blockIdx.x] = v[0]; partB[G + blockIdx.x] = v[1]; }
+    }
   }
-  grid.sync(G);
-  double tot[2];
-  grid_allsum<2>(partB, tot, G);
+  if constexpr (!CL) {
+    grid.sync(G);
+    grid_allsum<2>(partB, tot, G);
+  }
   const double norm_b = sqrt(tot[0]);
   double rz = tot[1];
   int iterations = 0;
@@ -543,6 +600,7 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg_reg(PcgArgs a, Mv mv, in
     for (int k = 1; k <= a.max_it; ++k) {
       iterations = k;
       TRACE(k, 0);
+      double pAp_a[1];
       {
         double v[1] = {0.0};
         for (int j = 0; j < nrow; ++j) {
@@ -561,18 +619,25 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg_reg(PcgArgs a, Mv mv, in
           v[0] += sum6(pAp);
         }
         TRACE(k, 1);
-        block_allsum<1>(v, sh);
-        if (threadIdx.x == 0) partA[blockIdx.x] = v[0];
+        if constexpr (CL) {
+          csync.allsum<1>(v, sh, G);
+          pAp_a[0] = v[0];
+        } else {
+          block_allsum<1>(v, sh);
+          if (threadIdx.x == 0) partA[blockIdx.x] = v[0];
+        }
       }
-      grid.sync(G);
-      double pAp_a[1];
-      grid_allsum<1>(partA, pAp_a, G);
+      if constexpr (!CL) {
+        grid.sync(G);
+        grid_allsum<1>(partA, pAp_a, G);
+      }
       TRACE(k, 2);
       const double pAp = pAp_a[0];
       if (!isfinite(pAp)) { status = 1; break; }
       if (pAp <= 0.0) break;
       const double alpha = rz / pAp;
       const bool restart = (k % a.restart) == 0;
+      double s3[3];
       {
         double v[3] = {0.0, 0.0, 0.0};
         for (int j = 0; j < nrow; ++j) {
@@ -601,7 +666,8 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg_reg(PcgArgs a, Mv mv, in
           v[2] += sum6(bad);
         }
         if (restart) {
-          grid.sync(G);  // x complete
+          if constexpr (CL) csync.barrier();  // x complete
+          else grid.sync(G);
           for (int j = 0; j < nrow; ++j) {
             const int row = rc.r0 + wid + PCG_WARPS * j;
             const double y = mv.template row<false>(a, rc, row, nullptr, a.x, 0.0, lane);
@@ -620,15 +686,23 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg_reg(PcgArgs a, Mv mv, in
           }
         }
         TRACE(k, 3);
-        block_allsum<3>(v, sh);
-        if (threadIdx.x == 0) {
+        if constexpr (CL) {
+          csync.allsum<3>(v, sh, G);
+          s3[0] = v[0];
+          s3[1] = v[1];
+          s3[2] = v[2];
+        } else {
+          block_allsum<3>(v, sh);
+          if (threadIdx.x == 0) {
 #pragma unroll
-          for (int q = 0; q < 3; ++q) partB[q * G + blockIdx.x] = v[q];
+            for (int q = 0; q < 3; ++q) partB[q * G + blockIdx.x] = v[q];
+          }
         }
       }
-      grid.sync(G);
-      double s3[3];
-      grid_allsum<3>(partB, s3, G);
+      if constexpr (!CL) {
+        grid.sync(G);
+        grid_allsum<3>(partB, s3, G);
+      }
       TRACE(k, 4);
       if (s3[2] != 0.0) { status = 1; break; }
       relative = sqrt(s3[0]) / norm_b;
@@ -734,9 +808,9 @@ static cudaError_t launch_pcg_t(const PcgArgs& a, Mv mv, int n_sm, cudaStream_t 
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k_pcg<DenseMv>, cudaFuncAttributeMaxDynamicSharedMemorySize, PCG_SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_pcg_reg<BsrMv>, cudaFuncAttributeMaxDynamicSharedMemorySize, PCG_SMEM_BYTES);
+    e = cudaFuncSetAttribute(k_pcg_reg<BsrMv, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, PCG_SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_pcg_reg<DenseMv>, cudaFuncAttributeMaxDynamicSharedMemorySize, PCG_SMEM_BYTES);
+    e = cudaFuncSetAttribute(k_pcg_reg<DenseMv, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, PCG_SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
@@ -763,7 +837,43 @@ static cudaError_t launch_pcg_t(const PcgArgs& a, Mv mv, int n_sm, cudaStream_t 
 #define PCG_REG 1
 #endif
   const bool reg = PCG_REG && rows_per_cta <= PCG_WARPS * PCG_RMAX;
-  return cudaLaunchCooperativeKernel(reg ? (void*)k_pcg_reg<Mv> : (void*)k_pcg<Mv>, dim3(G),
+#ifndef PCG_CLUSTER
+#define PCG_CLUSTER 1
+#endif
+  if (PCG_CLUSTER && reg && G > 1 && G <= PCG_CLUSTER_MAX) {
+    // small system: the whole grid as ONE thread-block cluster (hardware
+    // cluster barrier + DSMEM reductions instead of the global grid barrier)
+    static int cl_ok = -1;  // cluster launch of this size available (once)
+    if (cl_ok < 0) {
+      cl_ok = cudaFuncSetAttribute(k_pcg_reg<Mv, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                      cudaSuccess &&
+                  cudaFuncSetAttribute(k_pcg_reg<Mv, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       PCG_SMEM_BYTES) == cudaSuccess
+              ? 1
+              : 0;
+      (void)cudaGetLastError();
+    }
+    if (cl_ok) {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(G);
+      cfg.blockDim = dim3(PCG_THREADS);
+      cfg.dynamicSmemBytes = PCG_SMEM_BYTES;
+      cfg.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = G;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int ncl = 0;
+      if (cudaOccupancyMaxActiveClusters(&ncl, (const void*)k_pcg_reg<Mv, true>, &cfg) == cudaSuccess &&
+          ncl >= 1)
+        return cudaLaunchKernelExC(&cfg, (const void*)k_pcg_reg<Mv, true>, params);
+      (void)cudaGetLastError();  // this cluster size does not fit: grid barrier instead
+    }
+  }
+  return cudaLaunchCooperativeKernel(reg ? (void*)k_pcg_reg<Mv, false> : (void*)k_pcg<Mv>, dim3(G),
                                      dim3(PCG_THREADS), params, PCG_SMEM_BYTES, s);
 }
 
