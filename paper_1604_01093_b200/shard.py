@@ -5,9 +5,10 @@ the full problem; rank r owns every world-th directed dense edge and every
 world-th frame-pair filter candidate.  Two PCG modes:
 
 * ``pcg="replicated"`` (default): the per-edge sums of each dense pass are
-  summed across ranks (each entry has exactly one owning rank, so the sum is
-  exact), every rank assembles the bit-identical block system and runs the
-  same PCG - no per-PCG-iteration communication.
+  all-gathered (each row has exactly one owning rank, which sends only its
+  rows: an exact copy, half the bytes of an all-reduce), every rank
+  assembles the bit-identical block system and runs the same PCG - no
+  per-PCG-iteration communication.
 * ``pcg="sharded"``: each rank keeps only its partial system
   (its edges; the correspondence sets on rank 0); one all-reduce of
   [gradient | Jacobi diagonal | dense energies] per linearisation and one of
@@ -27,6 +28,10 @@ import numpy as np
 
 # dtype of each exchange buffer (include/sfb.h: sfb_exchange_buffer)
 EXCHANGE_DTYPES = {0: "f8", 1: "f8", 2: "u1", 3: "f8"}
+# buffers 0-2 hold rows owned by exactly one rank (row d by rank d % world):
+# they are all-GATHERED (each rank sends only its rows); buffer 3 (the
+# sharded-PCG partial system) is a true sum
+EXCHANGE_ROW = {0: 32, 1: 2, 2: 1}
 PCG_MODES = ("replicated", "sharded")
 
 
@@ -66,12 +71,39 @@ class ShardComm:
             if arr.size == 0:
                 return
             t = torch.from_numpy(arr)
-            self._dist.all_reduce(t, op=self._dist.ReduceOp.SUM, group=self.group)
+            if which in EXCHANGE_ROW:
+                self._gather_owned(t, EXCHANGE_ROW[which])
+            else:
+                self._dist.all_reduce(t, op=self._dist.ReduceOp.SUM, group=self.group)
             return
         ptr, nbytes = dp.exchange_buffer(which)
         if nbytes == 0:
             return
-        self.allreduce_device(ptr, nbytes, typestr, dp.stream_ptr())
+        if which not in EXCHANGE_ROW:
+            self.allreduce_device(ptr, nbytes, typestr, dp.stream_ptr())
+            return
+        dev = torch.device("cuda", torch.cuda.current_device())
+        t = torch.as_tensor(_CudaView(ptr, nbytes, typestr), device=dev)
+        with torch.cuda.stream(torch.cuda.ExternalStream(dp.stream_ptr(), device=dev)):
+            self._gather_owned(t, EXCHANGE_ROW[which])
+
+    def _gather_owned(self, t, row_len: int) -> None:
+        """In place: rows d of `t` (row_len elements each) are valid on rank
+        d % world only; after the call every rank holds all of them.  One
+        all-gather of each rank's rows (half the bytes of the equivalent
+        all-reduce, and an exact copy of the owner's values)."""
+        import torch
+        rows = t.view(-1, row_len)
+        n, world, rank = rows.shape[0], self.world, self.rank
+        per = (n + world - 1) // world
+        send = torch.zeros((per, row_len), dtype=t.dtype, device=t.device)
+        mine = rows[rank::world]
+        send[:mine.shape[0]] = mine
+        recv = [torch.empty_like(send) for _ in range(world)]
+        self._dist.all_gather(recv, send, group=self.group)
+        for r in range(world):
+            cnt = rows[r::world].shape[0]
+            rows[r::world] = recv[r][:cnt]
 
     def allreduce_device(self, ptr: int, nbytes: int, typestr: str, stream: int) -> None:
         """In-place sum of a device buffer across ranks, ordered on `stream`."""
