@@ -160,7 +160,34 @@ __device__ __forceinline__ void block_allsum(double (&v)[NV], double (*sh)[PCG_W
 
 // Every CTA sums the per-CTA partials part[k*G + b] in the same order.
 template <int NV>
+__device__ __forceinline__ void grid_allsum_warp(const double* part, double (&out)[NV], int G);
+#ifndef PCG_W0SUM
+#define PCG_W0SUM 1
+#endif
+template <int NV>
 __device__ __forceinline__ void grid_allsum(const double* part, double (&out)[NV], int G) {
+#if PCG_W0SUM
+  // warp 0 alone reads the G partials (L2 round trip) and shares the totals:
+  // every warp reading them made 8x the requests on the same hot lines
+  __shared__ double tot_sh[4];
+  if (threadIdx.x < 32) {
+    double t[NV];
+    grid_allsum_warp<NV>(part, t, G);
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int k = 0; k < NV; ++k) tot_sh[k] = t[k];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NV; ++k) out[k] = tot_sh[k];
+#else
+  grid_allsum_warp<NV>(part, out, G);
+#endif
+}
+
+template <int NV>
+__device__ __forceinline__ void grid_allsum_warp(const double* part, double (&out)[NV], int G) {
   // all NV x ceil(G/32) loads are issued before any is consumed (one L2
   // round trip); then a fixed-order per-lane sum and butterfly
   const int lane = threadIdx.x & 31;
