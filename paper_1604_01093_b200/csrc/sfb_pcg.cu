@@ -48,8 +48,9 @@ struct GridBarrier {
 struct RowCtx {
   int r0, r1;          // owned rows [r0, r1)
   int s0;              // first slot of r0
-  const double* Bs;    // staged slot blocks (shared) or null
-  const int* cols;     // column block per global slot (shared when staged)
+  const double* Bs;    // staged slot blocks (shared) or null: slots [s0, s_end)
+  const int* cols;     // column block per global slot (shared for staged slots)
+  int s_end;           // end of the staged slots (the rest read from global memory)
   double* gbuf;        // this warp's gather buffer (shared), PCG_GATHER_CAP x 6
 };
 
@@ -72,7 +73,8 @@ __device__ __forceinline__ double row_product(const PcgArgs& a, const RowCtx& rc
     double2 xa[3], xb[3], xc[3];
     const int ka = c0 + lane, kb = ka + 32, kc = ka + 64;
     const bool va = ka < c1, vb = kb < c1, vc = kc < c1;
-    const int wa = va ? rc.cols[ka] : 0, wb = vb ? rc.cols[kb] : 0, wc = vc ? rc.cols[kc] : 0;
+    auto col = [&](int k) { return k < rc.s_end ? rc.cols[k] : a.row_col[k]; };
+    const int wa = va ? col(ka) : 0, wb = vb ? col(kb) : 0, wc = vc ? col(kc) : 0;
 #pragma unroll
     for (int h = 0; h < 3; ++h) {
       xa[h] = va ? __ldcg(reinterpret_cast<const double2*>(pold + 6 * wa) + h) : make_double2(0, 0);
@@ -102,8 +104,8 @@ __device__ __forceinline__ double row_product(const PcgArgs& a, const RowCtx& rc
       // six independent FMA chains (one per column) instead of one 6x longer chain
       double ac[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
       for (int k = c0 + grp; k < c1; k += 5) {
-        const double* Bm = rc.Bs ? rc.Bs + (int64_t)(k - rc.s0) * 36 + r * 6
-                                 : a.Brow + (int64_t)k * 36 + r * 6;
+        const double* Bm = k < rc.s_end ? rc.Bs + (int64_t)(k - rc.s0) * 36 + r * 6
+                                        : a.Brow + (int64_t)k * 36 + r * 6;
         const double* xv = rc.gbuf + 6 * (k - c0);
 #pragma unroll
         for (int c = 0; c < 6; ++c) ac[c] = fma(Bm[c], xv[c], ac[c]);
@@ -125,7 +127,7 @@ __global__ void k_matvec(PcgArgs a, const double* xin, double* yout) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= a.n_blk) return;
-  RowCtx rc{0, 0, 0, nullptr, a.row_col, gb[threadIdx.x >> 5]};
+  RowCtx rc{0, 0, 0, nullptr, a.row_col, 0, gb[threadIdx.x >> 5]};
   const double y = row_product<false>(a, rc, warp, nullptr, xin, 0.0, lane);
   if (lane < 6) yout[6 * warp + lane] = y;
 }
@@ -298,21 +300,23 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg(PcgArgs a, Mv mv, int ro
   rc.Bs = nullptr;
   rc.cols = a.row_col;
   rc.gbuf = smem + wid * PCG_GATHER_CAP * 6;
+  rc.s_end = 0;
   if (mv.stageable() && rc.r1 > rc.r0) {
+    // the matrix (and its column indices) is constant during the solve: stage
+    // this CTA's slot blocks in shared memory once - as many as fit (cfg5's
+    // 37 MB exceed the SMs' shared memory; the remaining slots are read from L2)
     rc.s0 = a.row_ptr[rc.r0];
-    const int64_t ns = a.row_ptr[rc.r1] - rc.s0;
+    const int64_t cap = ((int64_t)PCG_SMEM_BYTES - (int64_t)PCG_GATHER_BYTES) / (36 * 8 + 4);
+    const int64_t ns = min((int64_t)(a.row_ptr[rc.r1] - rc.s0), cap);
     const int64_t n = ns * 36;
-    if ((int64_t)PCG_GATHER_BYTES + n * 8 + ns * 4 <= PCG_SMEM_BYTES) {
-      // the matrix (and its column indices) is constant during the solve:
-      // stage this CTA's rows in shared memory once
-      double* dst = smem + PCG_WARPS * PCG_GATHER_CAP * 6;
-      const double* src = a.Brow + (int64_t)rc.s0 * 36;
-      for (int64_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
-      int* cdst = reinterpret_cast<int*>(dst + n);
-      for (int64_t i = threadIdx.x; i < ns; i += blockDim.x) cdst[i] = a.row_col[rc.s0 + i];
-      rc.Bs = dst;
-      rc.cols = cdst - rc.s0;  // indexed by global slot
-    }
+    double* dst = smem + PCG_WARPS * PCG_GATHER_CAP * 6;
+    const double* src = a.Brow + (int64_t)rc.s0 * 36;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+    int* cdst = reinterpret_cast<int*>(dst + n);
+    for (int64_t i = threadIdx.x; i < ns; i += blockDim.x) cdst[i] = a.row_col[rc.s0 + i];
+    rc.Bs = dst;
+    rc.cols = cdst - rc.s0;  // indexed by global slot
+    rc.s_end = rc.s0 + (int)ns;
   }
   __syncthreads();
   double* pa = a.p;   // p of the previous iteration (read by neighbours)
@@ -550,19 +554,23 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg_reg(PcgArgs a, Mv mv, in
   rc.Bs = nullptr;
   rc.cols = a.row_col;
   rc.gbuf = smem + wid * PCG_GATHER_CAP * 6;
+  rc.s_end = 0;
   if (mv.stageable() && rc.r1 > rc.r0) {
+    // the matrix (and its column indices) is constant during the solve: stage
+    // this CTA's slot blocks in shared memory once - as many as fit (cfg5's
+    // 37 MB exceed the SMs' shared memory; the remaining slots are read from L2)
     rc.s0 = a.row_ptr[rc.r0];
-    const int64_t ns = a.row_ptr[rc.r1] - rc.s0;
+    const int64_t cap = ((int64_t)PCG_SMEM_BYTES - (int64_t)PCG_GATHER_BYTES) / (36 * 8 + 4);
+    const int64_t ns = min((int64_t)(a.row_ptr[rc.r1] - rc.s0), cap);
     const int64_t n = ns * 36;
-    if ((int64_t)PCG_GATHER_BYTES + n * 8 + ns * 4 <= PCG_SMEM_BYTES) {
-      double* dst = smem + PCG_WARPS * PCG_GATHER_CAP * 6;
-      const double* src = a.Brow + (int64_t)rc.s0 * 36;
-      for (int64_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
-      int* cdst = reinterpret_cast<int*>(dst + n);
-      for (int64_t i = threadIdx.x; i < ns; i += blockDim.x) cdst[i] = a.row_col[rc.s0 + i];
-      rc.Bs = dst;
-      rc.cols = cdst - rc.s0;
-    }
+    double* dst = smem + PCG_WARPS * PCG_GATHER_CAP * 6;
+    const double* src = a.Brow + (int64_t)rc.s0 * 36;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+    int* cdst = reinterpret_cast<int*>(dst + n);
+    for (int64_t i = threadIdx.x; i < ns; i += blockDim.x) cdst[i] = a.row_col[rc.s0 + i];
+    rc.Bs = dst;
+    rc.cols = cdst - rc.s0;  // indexed by global slot
+    rc.s_end = rc.s0 + (int)ns;
   }
   __syncthreads();
   // rows of this warp: rc.r0 + wid + PCG_WARPS * j, j < nrow (<= PCG_RMAX)
