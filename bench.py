@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo lets several ranks share one GPU (protocol test only)")
+    ap.add_argument("--p2p", action="store_true",
+                    help="replicated PCG: per-edge sums stored peer-to-peer by the edge-reduction "
+                         "kernel (CUDA IPC, one node) instead of an NCCL all-gather")
     ap.add_argument("--pcg", default="replicated", choices=["replicated", "sharded"],
                     help="multi-GPU PCG: replicated system (per-edge sums exchanged once per "
                          "dense pass) or sharded partial systems (one all-reduce of A.p per "
@@ -485,7 +488,7 @@ def main():
     comm = None
     if world > 1:
         from paper_1604_01093_b200.shard import ShardComm
-        comm = ShardComm(pcg=args.pcg)  # frame-pair sharding
+        comm = ShardComm(pcg=args.pcg, p2p=args.p2p)  # frame-pair sharding
     problem = S.AlignmentProblem(ids, scene.init, scene.corr_sets, caches, comm=comm)
     problem.solve(W, C)  # uploads + first solve (warm-up 0)
     dp = problem._dp
@@ -587,7 +590,8 @@ def main():
                    "resolution": list(scene.low_size), "dense_edges": n_edges,
                    "correspondences": n_corr, "n_vars": nv, "gn_iterations": len(records),
                    "pcg_iterations": pcg_iters, "l2": "flushed (384 MB write) between steps",
-                   "parallelism": (f"frame-pair shards x{world}, {args.pcg} PCG" if world > 1
+                   "parallelism": (f"frame-pair shards x{world}, {args.pcg} PCG"
+                                   + (", p2p edge sums" if args.p2p else "") if world > 1
                                    else "single")},
         "roofline": {"bound": "hbm", "kernel": "k_dense_fused",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -352,6 +352,19 @@ int sfb_set_shard(sfb_problem* p, int32_t rank, int32_t world);
  * n_vars partial A.p through the caller's callback, which must sum the
  * device buffer across ranks in place, ordered on `stream`, and return 0.
  * Every rank then runs pcg_solve's scalar recurrence on identical bits. */
+/* Peer-memory exchange of the per-edge sums (mode 0, ranks on one node): each
+ * rank exports CUDA IPC handles of its per-edge buffer (which 0) and of a
+ * 64-slot flag buffer (which 1), every rank attaches all of them (64-byte
+ * handles, indexed by rank), and with sfb_set_p2p(p, 1) the edge reduction
+ * stores each owned edge's sums straight into every peer's buffer, followed
+ * by a device-side barrier over the flags (system-scope release/acquire):
+ * no host collective for exchange buffer 0 (the _begin calls stop asking for
+ * it).  Re-attach buffer 0 after every sfb_build_dense_edges_end (the buffer
+ * may be reallocated). */
+int sfb_ipc_export(sfb_problem* p, int32_t which, void* handle64, int64_t* bytes);
+int sfb_ipc_attach(sfb_problem* p, int32_t which, int32_t world, const void* handles);
+int sfb_set_p2p(sfb_problem* p, int32_t on);
+
 typedef int (*sfb_allreduce_fn)(void* user, double* dev_buf, int64_t n, void* stream);
 int sfb_set_shard_mode(sfb_problem* p, int32_t mode);
 int sfb_linearize_end_system(sfb_problem* p);

@@ -121,6 +121,9 @@ SIGNATURES = {
     "sfb_set_preconditioner": [_P, _I32],
     "sfb_problem_drop_sets": [_P, _I64, _P],
     "sfb_set_shard_mode": [_P, _I32],
+    "sfb_ipc_export": [_P, _I32, _P, C.POINTER(_I64)],
+    "sfb_ipc_attach": [_P, _I32, _I32, _P],
+    "sfb_set_p2p": [_P, _I32],
     "sfb_linearize_end_system": [_P],
     "sfb_linearize_finish": [_P, _P],
     "sfb_pcg_sharded": [_P, _I32, _D, _I32, ALLREDUCE_FN, _P, C.POINTER(_I32), C.POINTER(_D),

@@ -82,6 +82,15 @@ struct sfb_problem : Handle {
   // data-parallel sharding over directed dense edges
   int shard_rank = 0, shard_world = 1;
   int shard_mode = 0;            // 0: exchange per-edge sums; 1: partial systems + sharded PCG
+  // peer-memory exchange of the per-edge sums (sfb_set_p2p): IPC-mapped
+  // edge_out / flag buffers of the other ranks
+  bool p2p_on = false;
+  DBuf<unsigned> p2p_flags;      // 64 slots: peers store their epochs here
+  unsigned p2p_epoch = 0;
+  std::vector<void*> p2p_open[2];  // opened peer pointers (edge_out, flags)
+  DBuf<double*> peer_edge_d;
+  DBuf<unsigned*> peer_flags_d;
+  bool p2p_ready[2] = {false, false};
   DBuf<double> xsys;             // mode 1: packed [g | jdiag | dense energies | D]
   DBuf<double> pcgs_state;       // mode 1: PCG scalars (sfb_pcg_sharded)
   int n_cand = 0;                // pair-filter candidates of the last filter pass
@@ -462,9 +471,21 @@ int enqueue_linearize(sfb_problem* p, const sfb_weights* w, double w_dense, cons
       CKL(p);
       p->cur = nxt;
       ProfScope ps(p->prof, 5, s);
+      const bool p2p = p->p2p_on && p->shard_world > 1 && p->p2p_ready[0] && p->p2p_ready[1];
+      if (p2p) {  // every rank is done reading the previous sums before anyone pushes new ones
+        launch_p2p_sync(p->peer_flags_d.p, p->p2p_flags.p, p->shard_rank, p->shard_world,
+                        ++p->p2p_epoch, s);
+        CKL(p);
+      }
       launch_edge_reduce(p->edge_item_ptr.p, p->item_out.p, p->edge_out.p, p->n_dir, p->dir_edges.p,
-                         p->poses.p, s);
+                         p->poses.p, s, p2p ? p->peer_edge_d.p : nullptr, p->shard_rank,
+                         p->shard_world);
       CKL(p);
+      if (p2p) {  // every rank's pushes have landed before the assembly reads them
+        launch_p2p_sync(p->peer_flags_d.p, p->p2p_flags.p, p->shard_rank, p->shard_world,
+                        ++p->p2p_epoch, s);
+        CKL(p);
+      }
     } else {
       CK(p, cudaMemsetAsync(p->edge_out.p, 0, sizeof(double) * p->n_dir * SFB_ITEM_STRIDE, s));
     }
@@ -957,6 +978,13 @@ int sfb_problem_destroy(sfb_problem* p) {
   p->edges_d.release();
   p->xsys.release();
   p->pcgs_state.release();
+  for (int w = 0; w < 2; ++w) {
+    for (void* q : p->p2p_open[w]) cudaIpcCloseMemHandle(q);
+    p->p2p_open[w].clear();
+  }
+  p->p2p_flags.release();
+  p->peer_edge_d.release();
+  p->peer_flags_d.release();
   {
     auto& sc = p->sc;
     DBuf<int>* si[] = {&sc.icount, &sc.per, &sc.dcount, &sc.bcount, &sc.doff, &sc.boff, &sc.dval,
@@ -1616,7 +1644,7 @@ int sfb_energy_and_linearize_begin(sfb_problem* p, const sfb_weights* w, int32_t
   int mode = 0;
   int rc = enqueue_linearize(p, w, w_dense_next, cfg, prev_dense ? 1 : 0, &mode);
   if (rc) return rc;
-  *exchange = (p->pending_dense_on ? 1 : 0) | (mode == 2 ? 2 : 0);
+  *exchange = (p->pending_dense_on && !p->p2p_on ? 1 : 0) | (mode == 2 ? 2 : 0);
   return SFB_OK;
 }
 
@@ -1688,7 +1716,7 @@ int sfb_gn_step_begin(sfb_problem* p, int32_t max_it, double tol, int32_t restar
     int mode = 0;
     int rc = enqueue_linearize(p, w, w_dense_next, cfg, prev_dense ? 1 : 0, &mode);
     if (rc) return rc;
-    *exchange = (p->pending_dense_on ? 1 : 0) | (mode == 2 ? 2 : 0);
+    *exchange = (p->pending_dense_on && !p->p2p_on ? 1 : 0) | (mode == 2 ? 2 : 0);
   } else {
     int rc = enqueue_energy_frozen_begin(p, prev_dense);
     if (rc) return rc;
@@ -1773,7 +1801,7 @@ int sfb_linearize_begin(sfb_problem* p, const sfb_weights* w, double w_dense, co
   CK(p, cudaSetDevice(p->ctx->device));
   int rc = enqueue_linearize(p, w, w_dense, cfg);
   if (rc) return rc;
-  *exchange = (p->pending_dense_on && p->shard_mode == 0) ? 1 : 0;
+  *exchange = (p->pending_dense_on && p->shard_mode == 0 && !p->p2p_on) ? 1 : 0;
   return SFB_OK;
 }
 
@@ -1958,6 +1986,69 @@ int sfb_set_preconditioner(sfb_problem* p, int32_t kind) {
     launch_block_jacobi_inv(p->D.p, p->jdiag.p, p->n_blk, p->bj_inv.p, p->stream);
     CKL(p);
   }
+  return SFB_OK;
+}
+
+// ---- peer-memory exchange (one process per GPU on one node) -----------------
+int sfb_ipc_export(sfb_problem* p, int32_t which, void* handle64, int64_t* bytes) {
+  if (!p || !handle64 || !bytes || which < 0 || which > 1) return fail(p, SFB_E_ARG, "bad arguments");
+  CK(p, cudaSetDevice(p->ctx->device));
+  void* ptr = nullptr;
+  if (which == 0) {
+    ptr = p->edge_out.p;
+    *bytes = (int64_t)p->edge_out.n * (int64_t)sizeof(double);
+  } else {
+    if (!p->p2p_flags.p) {
+      CK(p, p->p2p_flags.ensure(64, p->stream));
+      CK(p, cudaMemsetAsync(p->p2p_flags.p, 0, 64 * sizeof(unsigned), p->stream));
+      CK(p, cudaStreamSynchronize(p->stream));
+    }
+    ptr = p->p2p_flags.p;
+    *bytes = 64 * (int64_t)sizeof(unsigned);
+  }
+  if (!ptr) return fail(p, SFB_E_STATE, "buffer not allocated");
+  cudaIpcMemHandle_t h;
+  CK(p, cudaIpcGetMemHandle(&h, ptr));
+  std::memcpy(handle64, &h, sizeof(h));
+  return SFB_OK;
+}
+
+int sfb_ipc_attach(sfb_problem* p, int32_t which, int32_t world, const void* handles) {
+  if (!p || !handles || which < 0 || which > 1 || world != p->shard_world || world > 64)
+    return fail(p, SFB_E_ARG, "bad arguments");
+  CK(p, cudaSetDevice(p->ctx->device));
+  CK(p, cudaStreamSynchronize(p->stream));  // no kernel may still use the old mappings
+  for (void* q : p->p2p_open[which]) cudaIpcCloseMemHandle(q);
+  p->p2p_open[which].clear();
+  p->p2p_ready[which] = false;
+  std::vector<void*> ptrs(world, nullptr);
+  for (int r = 0; r < world; ++r) {
+    if (r == p->shard_rank) {
+      ptrs[r] = which == 0 ? (void*)p->edge_out.p : (void*)p->p2p_flags.p;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, (const char*)handles + 64 * r, sizeof(h));
+    void* q = nullptr;
+    CK(p, cudaIpcOpenMemHandle(&q, h, cudaIpcMemLazyEnablePeerAccess));
+    p->p2p_open[which].push_back(q);
+    ptrs[r] = q;
+  }
+  if (which == 0) {
+    CK(p, p->peer_edge_d.ensure(world, p->stream));
+    CK(p, cudaMemcpyAsync(p->peer_edge_d.p, ptrs.data(), sizeof(void*) * world, cudaMemcpyHostToDevice, p->stream));
+  } else {
+    CK(p, p->peer_flags_d.ensure(world, p->stream));
+    CK(p, cudaMemcpyAsync(p->peer_flags_d.p, ptrs.data(), sizeof(void*) * world, cudaMemcpyHostToDevice, p->stream));
+  }
+  CK(p, cudaStreamSynchronize(p->stream));
+  p->p2p_ready[which] = true;
+  return SFB_OK;
+}
+
+int sfb_set_p2p(sfb_problem* p, int32_t on) {
+  if (!p) return fail(p, SFB_E_ARG, "null problem");
+  p->p2p_on = on != 0;
   return SFB_OK;
 }
 

@@ -809,8 +809,17 @@ void launch_dense_energy(const DenseArgs& a, double* item_e2, cudaStream_t s) {
 // slot), then map the camera-j accumulators to the pose increments:
 // H_e = M_j K M_j^T, g_e = M_j k with M_j = [[R_j, -[t_j]x R_j], [0, -R_j]]
 // (both dense terms' J_i = M_j v, see k_dense_fused).
+// Peer-memory exchange (sharded runs, sfb_set_p2p): each owned edge's sums
+// are also stored straight into every peer's edge_out (P2P over NVLink) by
+// the warp that computes them - the all-gather fused into the reduction.
+struct EdgePeers {
+  double* const* dst;  // world pointers (own rank's entry unused), or null
+  int rank, world;
+};
+
 __global__ void k_edge_reduce(const int* edge_item_ptr, const double* item_out, double* edge_out,
-                              int n_dir, const int2* dir_edges, const PoseDev* poses) {
+                              int n_dir, const int2* dir_edges, const PoseDev* poses,
+                              EdgePeers peers) {
   __shared__ double sK[8][36], sM[8][36], sk[8][6];
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int wl = threadIdx.x >> 5;
@@ -820,9 +829,7 @@ __global__ void k_edge_reduce(const int* edge_item_ptr, const double* item_out, 
   for (int i = edge_item_ptr[warp]; i < edge_item_ptr[warp + 1]; ++i)
     s += item_out[(int64_t)i * SFB_ITEM_STRIDE + lane];
   double* out = edge_out + (int64_t)warp * SFB_ITEM_STRIDE;
-  if (lane >= 27) {
-    out[lane] = s;  // energies pass through
-  }
+  double val = s;  // lanes >= 27: energies pass through
   // unpack K (packed upper triangle) and k into shared memory
   for (int r = 0; r < 6; ++r)
     for (int c = r; c < 6; ++c)
@@ -855,21 +862,54 @@ __global__ void k_edge_reduce(const int* edge_item_ptr, const double* item_out, 
       for (int l = 0; l < 6; ++l) mk += sK[wl][k * 6 + l] * sM[wl][c * 6 + l];
       h += sM[wl][r * 6 + k] * mk;
     }
-    out[lane] = h;
+    val = h;
   } else if (lane < 27) {
     const int r = lane - 21;
     double g = 0.0;
     for (int k = 0; k < 6; ++k) g += sM[wl][r * 6 + k] * sk[wl][k];
-    out[lane] = g;
+    val = g;
+  }
+  if (peers.dst == nullptr) {
+    out[lane] = val;
+  } else if (warp % peers.world == peers.rank) {  // owned edge: local row + every peer's
+    out[lane] = val;
+    for (int r = 0; r < peers.world; ++r)
+      if (r != peers.rank) peers.dst[r][(int64_t)warp * SFB_ITEM_STRIDE + lane] = val;
+  }  // (other rows arrive from their owners: writing zeros here would race them)
+}
+
+// Cross-rank barrier over peer memory after the pushes: fence (system scope),
+// publish this rank's epoch in every peer's flag slot, wait for every peer's.
+__global__ void k_p2p_sync(unsigned* const* peer_flags, unsigned* my_flags, int rank, int world,
+                           unsigned epoch) {
+  if (threadIdx.x != 0) return;
+  __threadfence_system();
+  for (int r = 0; r < world; ++r)
+    if (r != rank)
+      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(peer_flags[r] + rank), "r"(epoch) : "memory");
+  for (int r = 0; r < world; ++r) {
+    if (r == rank) continue;
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(my_flags + r) : "memory");
+    } while (v < epoch);
   }
 }
 
+void launch_p2p_sync(unsigned* const* peer_flags, unsigned* my_flags, int rank, int world,
+                     unsigned epoch, cudaStream_t s) {
+  sfb_count_launch();
+  k_p2p_sync<<<1, 32, 0, s>>>(peer_flags, my_flags, rank, world, epoch);
+}
+
 void launch_edge_reduce(const int* edge_item_ptr, const double* item_out, double* edge_out,
-                        int n_dir, const int2* dir_edges, const PoseDev* poses, cudaStream_t s) {
+                        int n_dir, const int2* dir_edges, const PoseDev* poses, cudaStream_t s,
+                        double* const* peer_dst, int rank, int world) {
   if (n_dir <= 0) return;
   sfb_count_launch();
   k_edge_reduce<<<(n_dir * 32 + 255) / 256, 256, 0, s>>>(edge_item_ptr, item_out, edge_out, n_dir,
-                                                         dir_edges, poses);
+                                                         dir_edges, poses,
+                                                         EdgePeers{peer_dst, rank, world});
 }
 
 // Frozen-energy item pairs -> per-edge pairs (zero for edges without items).

@@ -216,7 +216,10 @@ void launch_matvec(const PcgArgs& a, const double* xin, double* yout, cudaStream
 void launch_edge_reduce2(const int* edge_item_ptr, const double* item_e2, double* edge_e2, int n_dir,
                          cudaStream_t s);
 void launch_edge_reduce(const int* edge_item_ptr, const double* item_out, double* edge_out,
-                        int n_dir, const int2* dir_edges, const PoseDev* poses, cudaStream_t s);
+                        int n_dir, const int2* dir_edges, const PoseDev* poses, cudaStream_t s,
+                        double* const* peer_dst = nullptr, int rank = 0, int world = 1);
+void launch_p2p_sync(unsigned* const* peer_flags, unsigned* my_flags, int rank, int world,
+                     unsigned epoch, cudaStream_t s);
 void launch_assemble(const AssembleArgs& a, cudaStream_t s);
 void launch_sum_energies(const double* set_out, int n_sets, const double* edge_out, int n_dir,
                          const double* item_e2, int n_items, double* out3, int mode,

@@ -209,6 +209,22 @@ class DeviceProblem:
                                           C.byref(rel), C.byref(st)))
         return it.value, rel.value, st.value
 
+    def ipc_export(self, which: int) -> bytes:
+        """CUDA IPC handle (64 bytes) of buffer `which` (0 per-edge sums, 1 p2p flags)."""
+        h = (C.c_char * 64)()
+        nb = C.c_int64()
+        self._ck(self.lib.sfb_ipc_export(self.handle, int(which), h, C.byref(nb)))
+        return bytes(h)
+
+    def ipc_attach(self, which: int, handles) -> None:
+        """Map every rank's buffer `which` (handles indexed by rank)."""
+        blob = b"".join(handles)
+        buf = C.create_string_buffer(blob, len(blob))
+        self._ck(self.lib.sfb_ipc_attach(self.handle, int(which), len(handles), buf))
+
+    def set_p2p(self, on: bool) -> None:
+        self._ck(self.lib.sfb_set_p2p(self.handle, 1 if on else 0))
+
     def exchange_buffer(self, which: int):
         """(device pointer, bytes) of exchange buffer `which` (0 per-edge
         linearisation sums f64, 1 per-edge frozen energies f64, 2 filter

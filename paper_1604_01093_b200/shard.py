@@ -49,15 +49,33 @@ class _CudaView:
 class ShardComm:
     """Sums exchange buffers across the ranks of a torch.distributed group."""
 
-    def __init__(self, group=None, pcg: str = "replicated"):
+    def __init__(self, group=None, pcg: str = "replicated", p2p: bool = False):
         import torch.distributed as dist
         if pcg not in PCG_MODES:
             raise ValueError(f"pcg must be one of {PCG_MODES}")
         self._dist = dist
         self.group = group
         self.pcg = pcg
+        # replicated mode: the per-edge sums go peer-to-peer from the edge
+        # reduction kernel into every rank's buffer (CUDA IPC, one node)
+        self.p2p = bool(p2p) and pcg == "replicated"
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        self._p2p_handles = {}
+
+    def p2p_setup(self, dp) -> None:
+        """Exchange and map the IPC handles of every rank's per-edge buffer and
+        flags (again whenever a rank's buffer was reallocated)."""
+        mine = (dp.ipc_export(0), dp.ipc_export(1))
+        allh = [None] * self.world
+        self._dist.all_gather_object(allh, mine, group=self.group)
+        key = id(dp)
+        for which in (0, 1):
+            hs = [h[which] for h in allh]
+            if self._p2p_handles.get((key, which)) != hs:
+                dp.ipc_attach(which, hs)
+                self._p2p_handles[(key, which)] = hs
+        dp.set_p2p(True)
 
     @property
     def active(self) -> bool:

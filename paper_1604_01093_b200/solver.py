@@ -781,6 +781,8 @@ class AlignmentProblem:
         dp.set_preconditioner(_precond_kind(config))
         self._push_poses()
         self._sync_edges()
+        if self._xch is not None and getattr(self._xch, "p2p", False):
+            self._xch.p2p_setup(dp)
         e = dp.linearize(weights, w_dense, config, exchange=self._xch)
         dense_on = self.caches is not None and w_dense > 0.0 and bool(self.dense_edges)
         energy = weights.sparse * float(e[0])
@@ -822,6 +824,8 @@ class AlignmentProblem:
             self._dp_edges = self.dense_edges
         else:
             self._sync_edges()
+        if self._xch is not None and getattr(self._xch, "p2p", False):
+            self._xch.p2p_setup(dp)  # the structure rebuild may have moved the edge buffer
         have_edges = len(pairs) > 0 if self.caches is not None else bool(self.dense_edges)
         tr.mark("filter")
         if self._sharded_pcg:

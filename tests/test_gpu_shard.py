@@ -31,7 +31,7 @@ def _solve(name, comm=None):
     return R, t, recs, list(p.dense_edges)
 
 
-def _worker(rank, world, port, name, q):
+def _worker(rank, world, port, name, q, p2p=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), SFB_DEVICE="0")
     import torch
     import torch.distributed as dist
@@ -39,7 +39,7 @@ def _worker(rank, world, port, name, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_1604_01093_b200.shard import ShardComm
-        q.put((rank, _solve(name, ShardComm())))
+        q.put((rank, _solve(name, ShardComm(p2p=p2p))))
     except Exception as e:  # surface worker failures in the parent
         q.put((rank, repr(e)))
     finally:
@@ -47,15 +47,18 @@ def _worker(rank, world, port, name, q):
 
 
 @pytest.mark.timeout(600)
-@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
-def test_sharded_solve_bit_identical(name):
+@pytest.mark.parametrize("name,p2p", [("cfg2", False), ("cfg3", False), ("cfg2", True), ("cfg3", True)])
+def test_sharded_solve_bit_identical(name, p2p):
+    """p2p: the per-edge sums go from the edge-reduction kernel straight into
+    the other rank's buffer (CUDA IPC; here two processes share one GPU)
+    followed by the device-side flag barrier - no host collective for them."""
     import torch.multiprocessing as mp
     R1, t1, recs1, edges1 = _solve(name)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     world = 2
-    procs = [ctx.Process(target=_worker, args=(r, world, port, name, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, name, q, p2p)) for r in range(world)]
     for p in procs:
         p.start()
     out = {}
