@@ -63,6 +63,7 @@ struct sfb_problem : Handle {
   DBuf<uint8_t> tile_any[2];     // per (edge, source tile): any frozen association
   int cur = 0;                   // buffer holding the latest linearisation
   DBuf<double> item_out, edge_out, item_e2;
+  DBuf<double> edge_rel;         // per directed edge: pose_j^-1 o pose_i (12 f64), per dense pass
   DBuf<int2> stride_counts;      // per frame source counts on the stride grid
   int stride_counts_for = 0;     // stride they were computed for (0: none)
   DBuf<double> edge_e2;          // frozen-energy sums per directed edge (2 each)
@@ -335,6 +336,7 @@ int rebuild_structure(sfb_problem* p, int bidir) {
   }
   CK(p, p->item_out.ensure((size_t)std::max(1, p->n_items) * SFB_ITEM_STRIDE, s));
   CK(p, p->edge_out.ensure((size_t)std::max(1, p->n_dir) * SFB_ITEM_STRIDE, s));
+  CK(p, p->edge_rel.ensure((size_t)std::max(1, p->n_dir) * 12, s));
   CK(p, p->item_e2.ensure((size_t)std::max(1, p->n_items) * 2, s));
   CK(p, p->edge_e2.ensure((size_t)std::max(1, p->n_dir) * 2, s));
   CK(p, p->D.ensure((size_t)std::max(1, nb) * 36, s));
@@ -361,6 +363,8 @@ DenseArgs dense_args(sfb_problem* p) {
   a.poses = p->poses.p;
   a.items = p->items.p;
   a.dir_edges = p->dir_edges.p;
+  a.edge_rel = p->edge_rel.p;
+  a.n_dir = p->n_dir;
   a.photo_off = p->photo_off.p;
   a.geo_off = p->geo_off.p;
   a.photo_mask = p->photo_mask[p->cur].p;
@@ -976,6 +980,7 @@ int sfb_problem_destroy(sfb_problem* p) {
   for (auto* b : db) b->release();
   p->pair_key.release();
   p->edges_d.release();
+  p->edge_rel.release();
   p->xsys.release();
   p->pcgs_state.release();
   for (int w = 0; w < 2; ++w) {

@@ -624,8 +624,10 @@ __global__ void __launch_bounds__(DENSE_THREADS, DENSE_TMEM_BLOCKS) k_dense_fuse
   __shared__ uint32_t tm_base;
   const int4 it = a.items[blockIdx.x];
   const int2 de = a.dir_edges[it.x];
+  if (a.edge_rel && threadIdx.x < 12)  // precomputed by k_edge_rel (12 parallel loads)
+    (&rel.R[0])[threadIdx.x] = a.edge_rel[12 * (int64_t)it.x + threadIdx.x];
   if (threadIdx.x == 0) {
-    rel = xf_relative_exact(a.poses[de.x], a.poses[de.y], a.rd);
+    if (!a.edge_rel) rel = xf_relative_exact(a.poses[de.x], a.poses[de.y], a.rd);
     const FrameDev Fi = a.frames[de.x];
     Fj = a.frames[de.y];
     const int2 nsrc = src_counts(a, Fi, de.x);
@@ -724,12 +726,32 @@ __global__ void __launch_bounds__(DENSE_THREADS, DENSE_TMEM_BLOCKS) k_dense_fuse
   }
 }
 
+// relative = pose_j^-1 o pose_i with NumPy's rounding (frames.py:168,
+// solver.py:221) for every directed edge, once per dense pass, so the pass's
+// CTAs start with 12 parallel loads instead of one thread's serial chain
+__global__ void k_edge_rel(const int2* dir_edges, const PoseDev* poses, Rounding rd, int n_dir,
+                           double* out) {
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= n_dir) return;
+  const int2 e = dir_edges[d];
+  const Xf r = xf_relative_exact(poses[e.x], poses[e.y], rd);
+#pragma unroll
+  for (int k = 0; k < 9; ++k) out[12 * (int64_t)d + k] = r.R[k];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) out[12 * (int64_t)d + 9 + k] = r.t[k];
+}
+
 void launch_dense_linearize(const DenseArgs& a, cudaStream_t s) {
   if (a.n_items <= 0) return;
   const bool prev = a.photo_mask_prev != nullptr;
+  const DenseArgs& b = a;
+  if (a.edge_rel && a.n_dir > 0) {
+    sfb_count_launch();
+    k_edge_rel<<<(a.n_dir + 127) / 128, 128, 0, s>>>(a.dir_edges, a.poses, a.rd, a.n_dir, a.edge_rel);
+  }
   sfb_count_launch();
-  if (prev) k_dense_fused<true><<<a.n_items, DENSE_THREADS, 0, s>>>(a);
-  else k_dense_fused<false><<<a.n_items, DENSE_THREADS, 0, s>>>(a);
+  if (prev) k_dense_fused<true><<<a.n_items, DENSE_THREADS, 0, s>>>(b);
+  else k_dense_fused<false><<<a.n_items, DENSE_THREADS, 0, s>>>(b);
 }
 
 // Frozen-association energy at the current poses.

@@ -40,6 +40,8 @@ struct DenseArgs {
   const PoseDev* poses;
   const int4* items;        // (dir edge, begin, end, 0)
   const int2* dir_edges;    // (src frame, dst frame)
+  double* edge_rel;         // scratch: 12 f64 per directed edge (relative transforms), or null
+  int n_dir;
   const int64_t* photo_off; // per dir edge: u32-word offset
   const int64_t* geo_off;   // per dir edge: u16 offset
   uint32_t* photo_mask;
