@@ -195,7 +195,7 @@ def _time_edges(args):
     """Worker: oracle linearise + frozen energy on a list of directed edges."""
     scene_name, edges = args
     from oracle import scanfuse_oracle as O
-    from paper_1604_01093_b200 import synth
+    from scenes import synth
     scene = _scene_cache(scene_name)
     poses = {f: O.pose_of(p) for f, p in scene.init.items()}
     t0 = time.perf_counter()
@@ -241,7 +241,7 @@ _SCENES = {}
 
 def _scene_cache(name):
     if name not in _SCENES:
-        from paper_1604_01093_b200 import synth
+        from scenes import synth
         _SCENES[name] = synth.make(name)
     return _SCENES[name]
 
@@ -470,7 +470,7 @@ def main():
 
     from paper_1604_01093_b200 import _abi
     from paper_1604_01093_b200 import solver as S
-    from paper_1604_01093_b200 import synth
+    from scenes import synth
     from paper_1604_01093_b200.runtime import runtime
 
     scene = synth.make(args.config)

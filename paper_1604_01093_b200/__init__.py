@@ -9,4 +9,5 @@ include/sfb.h).
 __version__ = "0.1.0"
 
 from .se3 import Intrinsics, RigidTransform, TwistParams, exp_twist, exp_twist_vector  # noqa: F401
-from .cache import CachedFrame, CorrespondenceSet, RgbdFrame, build_cache  # noqa: F401
+from .cache import CachedFrame, CorrespondenceSet, RgbdFrame, build_cache_device  # noqa: F401
+from .frames import build_cache  # noqa: F401  (device, the reference's frames.build_cache)

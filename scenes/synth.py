@@ -22,8 +22,10 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .cache import CachedFrame, CorrespondenceSet, RgbdFrame, build_cache
-from .se3 import Intrinsics, RigidTransform, TwistParams, exp_twist
+from paper_1604_01093_b200.cache import CachedFrame, CorrespondenceSet, RgbdFrame
+from paper_1604_01093_b200.se3 import Intrinsics, RigidTransform, TwistParams, exp_twist
+
+from .host_cache import build_cache
 
 K_FULL = Intrinsics(525.0, 525.0, 319.5, 239.5, 640, 480)
 

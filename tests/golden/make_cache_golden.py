@@ -41,7 +41,7 @@ def digest(a) -> str:
 
 def cache_inputs():
     """[(name, color (H,W,3) u8, depth (H,W) f32, (low_w, low_h), K)]"""
-    from paper_1604_01093_b200 import synth
+    from scenes import synth
     out = []
     sc = synth.make("cfg2")
     for f in sorted(sc.renders):

@@ -27,7 +27,7 @@ _S = {}
 
 def _scene(name):
     if name not in _S:
-        from paper_1604_01093_b200 import synth
+        from scenes import synth
         from scanfuse import geometry as RG
         sc = synth.make(name)
         poses = {f: RG.RigidTransform(np.array(p.rotation), np.array(p.translation))

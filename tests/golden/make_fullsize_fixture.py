@@ -30,7 +30,7 @@ def _work(k):
     from scanfuse import filters as RF
     from scanfuse import geometry as RG
     from scanfuse import solver as RS
-    from paper_1604_01093_b200 import synth
+    from scenes import synth
     sc = synth.make("cfg4")
     poses = {f: RG.RigidTransform(np.array(p.rotation), np.array(p.translation))
              for f, p in sc.init.items()}

@@ -4,7 +4,7 @@ Run in the build container only (the reference is not on the GPU box):
 
     PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py [cfg1 cfg2 cfg3 units]
 
-Inputs come from paper_1604_01093_b200.synth (deterministic); every output
+Inputs come from scenes.synth (deterministic); every output
 (edge lists, linearisation snapshot, per-iteration records, final poses,
 association sizes, Jacobians, overlaps) is produced by scanfuse 0.1.0 from
 /root/reference/pkg/src.  The caches fed to the reference are built by the
@@ -28,7 +28,7 @@ from scanfuse import geometry as RG  # noqa: E402
 from scanfuse import solver as RS  # noqa: E402
 from scipy import ndimage  # noqa: E402
 
-from paper_1604_01093_b200 import synth  # noqa: E402
+from scenes import synth  # noqa: E402
 from paper_1604_01093_b200.cache import RgbdFrame  # noqa: E402
 
 K = RG.Intrinsics(525.0, 525.0, 319.5, 239.5, 640, 480)

@@ -45,7 +45,7 @@ from scanfuse import frames as RFr  # noqa: E402
 from scanfuse import geometry as RG  # noqa: E402
 from scanfuse import solver as RS  # noqa: E402
 
-from paper_1604_01093_b200 import synth  # noqa: E402
+from scenes import synth  # noqa: E402
 
 N_WORK = int(os.environ.get("GOLDEN_WORKERS", os.cpu_count() or 8))
 

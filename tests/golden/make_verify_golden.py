@@ -31,7 +31,7 @@ from scanfuse import filters as RF  # noqa: E402
 from scanfuse import frames as RFr  # noqa: E402
 from scanfuse import geometry as RG  # noqa: E402
 
-from paper_1604_01093_b200 import synth  # noqa: E402
+from scenes import synth  # noqa: E402
 
 
 def exp_so3(w):

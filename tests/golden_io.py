@@ -6,7 +6,7 @@ from pathlib import Path
 
 import numpy as np
 
-from paper_1604_01093_b200 import synth
+from scenes import synth
 from paper_1604_01093_b200.cache import CachedFrame, CorrespondenceSet
 from paper_1604_01093_b200.se3 import Intrinsics, RigidTransform
 

@@ -97,7 +97,7 @@ def test_view_cos_threshold_is_exact_preimage(deg):
 
 
 def test_synth_deterministic():
-    from paper_1604_01093_b200 import synth
+    from scenes import synth
     a, b = synth.make("cfg2"), synth.make("cfg2")
     assert synth.cache_digest(a.caches) == synth.cache_digest(b.caches)
     assert all(np.array_equal(x.points_i, y.points_i) for x, y in zip(a.corr_sets, b.corr_sets))
@@ -115,7 +115,8 @@ def test_native_set_stacking_matches_numpy_path():
     import copy
     from paper_1604_01093_b200 import _build
     _build.build_host()
-    from paper_1604_01093_b200 import _sfbhost, synth
+    from paper_1604_01093_b200 import _sfbhost
+    from scenes import synth
     from paper_1604_01093_b200 import solver as S
     sc = synth.make("cfg3")
     index = {f: k for k, f in enumerate(sc.frame_ids)}
@@ -149,7 +150,8 @@ def test_native_set_stacking_matches_numpy_path():
 def test_native_frame_descriptors():
     from paper_1604_01093_b200 import _build
     _build.build_host()
-    from paper_1604_01093_b200 import _sfbhost, synth
+    from paper_1604_01093_b200 import _sfbhost
+    from scenes import synth
     from paper_1604_01093_b200.runtime import _DESC_DTYPE
     sc = synth.make("cfg2")
     caches = [sc.caches[f] for f in sc.frame_ids]

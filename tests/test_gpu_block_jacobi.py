@@ -14,9 +14,9 @@ import pytest
 
 from golden_io import GOLDEN, pose_errors
 from paper_1604_01093_b200 import solver as S
-from paper_1604_01093_b200 import synth
+from scenes import synth
 from paper_1604_01093_b200.se3 import RigidTransform
-from paper_1604_01093_b200.synth import chunk_corr_sets, chunk_ground_truth, make_corr_set
+from scenes.synth import chunk_corr_sets, chunk_ground_truth, make_corr_set
 
 pytestmark = pytest.mark.gpu
 

@@ -30,6 +30,7 @@ def _groups():
 
 def test_device_build_cache_bit_exact():
     from paper_1604_01093_b200 import cache as CA
+    from scenes import host_cache as HC
     from paper_1604_01093_b200 import se3
     g = json.loads((GOLDEN / "cache_digests.json").read_text())
     checked = 0
@@ -38,7 +39,7 @@ def test_device_build_cache_bit_exact():
         frames = [CA.RgbdFrame(i, col, dep) for i, (_, col, dep) in enumerate(items)]
         dev = CA.build_cache_device(frames, k, lw, lh)
         for (name, col, dep), c in zip(items, dev):
-            host = CA.build_cache(CA.RgbdFrame(0, col, dep), k, lw, lh)
+            host = HC.build_cache(CA.RgbdFrame(0, col, dep), k, lw, lh)
             for p in PLANES:
                 a, b = np.asarray(getattr(c, p)), np.asarray(getattr(host, p))
                 diff = int(np.count_nonzero(~((a == b) | (np.isnan(a) & np.isnan(b)))))
@@ -53,7 +54,9 @@ def test_device_caches_are_resident_and_solve_like_host_caches():
     and a cfg2 solve on them reproduces the reference's golden result."""
     from golden_io import GoldenScene, pose_errors
     from paper_1604_01093_b200 import cache as CA
-    from paper_1604_01093_b200 import se3, synth
+    from scenes import host_cache as HC
+    from paper_1604_01093_b200 import se3
+    from scenes import synth
     from paper_1604_01093_b200 import solver as S
     from paper_1604_01093_b200.runtime import runtime
     s = GoldenScene("cfg2")
@@ -77,8 +80,10 @@ def test_device_caches_are_resident_and_solve_like_host_caches():
 
 def test_dense_verify_on_device_caches_matches_host_caches():
     from paper_1604_01093_b200 import cache as CA
+    from scenes import host_cache as HC
     from paper_1604_01093_b200 import filters as F
-    from paper_1604_01093_b200 import se3, synth
+    from paper_1604_01093_b200 import se3
+    from scenes import synth
     sc = synth.make("cfg2")
     kr = sc.render_k
     k = se3.Intrinsics(kr.fx, kr.fy, kr.cx, kr.cy, kr.width, kr.height)
@@ -114,8 +119,9 @@ class TestReferenceBuildCache:
 
     def _dev(self, frame):
         from paper_1604_01093_b200 import cache as CA
+        from scenes import host_cache as HC
         c = CA.build_cache_device([frame], self._k())[0]
-        h = CA.build_cache(frame, self._k())
+        h = HC.build_cache(frame, self._k())
         for p in PLANES:
             a, b = np.asarray(getattr(c, p)), np.asarray(getattr(h, p))
             assert a.dtype == b.dtype and np.array_equal(a, b), p

@@ -41,7 +41,7 @@ def _run_threads(fns):
 
 def test_concurrent_dense_verify_matches_serial():
     from paper_1604_01093_b200 import filters as F
-    from paper_1604_01093_b200 import synth
+    from scenes import synth
     sc = synth.make("cfg3")
     rng = np.random.default_rng(3)
     batches = []
@@ -71,7 +71,7 @@ def _solve(sc):
 
 
 def test_concurrent_solves_match_serial():
-    from paper_1604_01093_b200 import synth
+    from scenes import synth
     a, b = synth.make("cfg3"), synth.make("cfg2")
     sa, sb = _solve(a), _solve(b)
     for _ in range(2):
@@ -83,7 +83,7 @@ def test_concurrent_solves_match_serial():
 
 def test_frame_store_releases_dropped_caches():
     from paper_1604_01093_b200 import solver as S
-    from paper_1604_01093_b200 import synth
+    from scenes import synth
     from paper_1604_01093_b200.runtime import runtime
     rt = runtime(0)
     rt.clear_frames()

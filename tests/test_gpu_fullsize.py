@@ -23,7 +23,7 @@ _SC = {}
 
 def _scene(name):
     if name not in _SC:
-        from paper_1604_01093_b200 import synth
+        from scenes import synth
         _SC[name] = synth.make(name)
     return _SC[name]
 

@@ -11,7 +11,7 @@ import pytest
 
 from golden_io import GoldenScene, load, pose_errors
 from paper_1604_01093_b200 import solver as S
-from paper_1604_01093_b200 import synth
+from scenes import synth
 from paper_1604_01093_b200.cache import RgbdFrame
 from paper_1604_01093_b200.se3 import RigidTransform
 

@@ -26,12 +26,13 @@ def _mods():
 
 
 def flat_cache(depth=2.0, intensity=0.4, index=0):
-    """test_filters.py:52-58 with this package's build_cache."""
+    """test_filters.py:52-58 with the scene generator's build_cache."""
+    from scenes import host_cache as HC
     F, CA, se3 = _mods()
     k = se3.Intrinsics(525.0, 525.0, 319.5, 239.5, 640, 480)
     color = np.full((480, 640, 3), 100, dtype=np.uint8)
     frame = CA.RgbdFrame(index=index, color=color, depth=np.full((480, 640), depth, np.float32))
-    c = CA.build_cache(frame, k)
+    c = HC.build_cache(frame, k)
     c.intensity_low[:] = intensity
     c.grad_low[:] = 0.0
     return c
@@ -52,7 +53,7 @@ def _same(res, ref):
 
 def test_golden_pairs_bit_exact():
     F, CA, se3 = _mods()
-    from paper_1604_01093_b200 import synth
+    from scenes import synth
     sc = synth.make("cfg3")
     g = np.load(GOLDEN / "verify.npz")
     pairs = []
@@ -75,7 +76,7 @@ def test_golden_pairs_bit_exact():
 
 def test_error_max_override_and_oracle():
     F, CA, se3 = _mods()
-    from paper_1604_01093_b200 import synth
+    from scenes import synth
     sc = synth.make("cfg3")
     T = sc.truth[20].inverse().compose(sc.truth[17])
     cfg = F.FilterConfig()

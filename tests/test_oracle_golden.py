@@ -9,7 +9,7 @@ import pytest
 
 from golden_io import GoldenScene, load, pose_errors
 from oracle import scanfuse_oracle as O
-from paper_1604_01093_b200 import synth
+from scenes import synth
 from paper_1604_01093_b200.se3 import RigidTransform
 
 FIELDS = ("energy_before", "energy_after", "dense_weight", "pcg_iterations", "pcg_residual",
@@ -125,7 +125,7 @@ def test_oracle_dense_verify_matches_reference_golden():
     pair (tests/golden/make_verify_golden.py): counts, pass flags and the mean
     errors bit-for-bit."""
     from oracle import scanfuse_oracle as O
-    from paper_1604_01093_b200 import synth
+    from scenes import synth
     sc = synth.make("cfg3")
     g = load("verify")
     for k, (a, b) in enumerate(g["pairs"]):
@@ -138,7 +138,7 @@ def test_oracle_dense_verify_matches_reference_golden():
 
 
 def test_host_build_cache_matches_reference_digests():
-    """This package's NumPy build_cache (the scene generator's producer and the
+    """The scene generator's NumPy build_cache (scenes/host_cache.py, also the
     GPU test's diagnostic) is bit-identical to scanfuse.frames.build_cache on
     every golden input (tests/golden/make_cache_golden.py)."""
     import json
@@ -148,9 +148,10 @@ def test_host_build_cache_matches_reference_digests():
     from make_cache_golden import PLANES, cache_inputs, digest
     from paper_1604_01093_b200 import cache as CA
     from paper_1604_01093_b200 import se3
+    from scenes.host_cache import build_cache
     g = json.loads((GOLDEN / "cache_digests.json").read_text())
     for name, col, dep, (lw, lh), kk in cache_inputs():
-        c = CA.build_cache(CA.RgbdFrame(0, col, dep), se3.Intrinsics(*kk), lw, lh)
+        c = build_cache(CA.RgbdFrame(0, col, dep), se3.Intrinsics(*kk), lw, lh)
         for p in PLANES:
             assert digest(getattr(c, p)) == g[name][p], (name, p)
 

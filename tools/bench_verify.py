@@ -21,7 +21,8 @@ import numpy as np
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 
-from paper_1604_01093_b200 import _abi, synth  # noqa: E402
+from paper_1604_01093_b200 import _abi  # noqa: E402
+from scenes import synth
 from paper_1604_01093_b200 import filters as F  # noqa: E402
 from paper_1604_01093_b200 import solver as S  # noqa: E402
 from paper_1604_01093_b200.runtime import runtime  # noqa: E402

@@ -8,7 +8,8 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import bench  # noqa: E402
-from paper_1604_01093_b200 import solver as S, synth  # noqa: E402
+from paper_1604_01093_b200 import solver as S  # noqa: E402
+from scenes import synth
 from paper_1604_01093_b200.device_problem import DeviceProblem  # noqa: E402
 from paper_1604_01093_b200.runtime import runtime  # noqa: E402
 

@@ -2,7 +2,8 @@
 import argparse, sys, time
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
-from paper_1604_01093_b200 import solver as S, synth
+from paper_1604_01093_b200 import solver as S
+from scenes import synth
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="cfg4")

@@ -17,7 +17,8 @@ os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
 os.environ.setdefault("MASTER_PORT", "29533")
 torch.cuda.set_device(0)
 dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
-from paper_1604_01093_b200 import solver as S, synth  # noqa: E402
+from paper_1604_01093_b200 import solver as S  # noqa: E402
+from scenes import synth
 from paper_1604_01093_b200.shard import ShardComm  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg4"

@@ -4,7 +4,8 @@ import sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import numpy as np  # noqa: E402
-from paper_1604_01093_b200 import solver as S, synth, _abi  # noqa: E402
+from paper_1604_01093_b200 import solver as S, _abi  # noqa: E402
+from scenes import synth
 sc = synth.make(sys.argv[1] if len(sys.argv) > 1 else "cfg4")
 W, Cf = S.EnergyWeights(**sc.weights), S.SolverConfig(**sc.config)
 p = S.AlignmentProblem(sc.frame_ids, sc.init, sc.corr_sets, sc.caches)

@@ -8,7 +8,7 @@ from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 
 from paper_1604_01093_b200 import solver as S  # noqa: E402
-from paper_1604_01093_b200 import synth  # noqa: E402
+from scenes import synth  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="cfg4")

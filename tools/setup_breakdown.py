@@ -8,7 +8,8 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import torch  # noqa: E402
 
 import bench  # noqa: E402
-from paper_1604_01093_b200 import device_problem as DPm, solver as S, synth  # noqa: E402
+from paper_1604_01093_b200 import device_problem as DPm, solver as S  # noqa: E402
+from scenes import synth
 from paper_1604_01093_b200.runtime import runtime  # noqa: E402
 
 sc = synth.make(sys.argv[1] if len(sys.argv) > 1 else "cfg5")
