@@ -355,6 +355,9 @@ __device__ __forceinline__ void tm_chunk(uint32_t tm, const double (&jp)[2][6], 
   if constexpr (4 * Q + 3 < 27) tm_set(u, 3, tm_update<4 * Q + 3>(tm_d(u, 3), jp, rp, jg, rg));
   TM_ST8(tm + 8 * Q, u);
 }
+#ifndef DENSE_F32GUARD
+#define DENSE_F32GUARD 1
+#endif
 #ifndef DENSE_TMEM_BLOCKS
 #define DENSE_TMEM_BLOCKS 4
 #endif
@@ -449,10 +452,21 @@ __device__ __forceinline__ void dense_tile(const DenseArgs& a, const TileCtx& c,
   const double va = fma(tv, rz, Fj.cy);
   // associate_photo: decide with a 1e-6 px guard band, exact quotient inside it
   bool ph_in = false;
+#if DENSE_F32GUARD
+  // classify in float32 with a 1e-3 px band (float rounding of ua is <= 2e-5
+  // px at these image sizes): the FP64 pipe only sees the rare band cases
+  const float uf = __double2float_rn(ua), vf = __double2float_rn(va);
+#endif
   {
+#if DENSE_F32GUARD
+    const float EB = 1e-3f, wf = (float)c.wm1, hf = (float)c.hm1;
+    const bool in_c = uf > EB && uf < wf - EB && vf > EB && vf < hf - EB;
+    const bool out_c = uf < -EB || uf > wf + EB || vf < -EB || vf > hf + EB;
+#else
     const double E = 1e-6;
     const bool in_c = ua > E && ua < c.wm1 - E && va > E && va < c.hm1 - E;
     const bool out_c = ua < -E || ua > c.wm1 + E || va < -E || va > c.hm1 + E;
+#endif
     ph_in = ph && front && in_c;
     if (ph && !(in_c | out_c)) {
       const double u = __dadd_rn(__ddiv_rn(tu, z), Fj.cx);
@@ -472,7 +486,11 @@ __device__ __forceinline__ void dense_tile(const DenseArgs& a, const TileCtx& c,
       z = front ? q2 : 1.0;
     }
     double u = ua, v = va;
+#if DENSE_F32GUARD
+    const bool finite_uv = fabsf(uf) < 1e9f && fabsf(vf) < 1e9f;
+#else
     const bool finite_uv = fabs(u) < 1e9 && fabs(v) < 1e9;
+#endif
     double xr = finite_uv ? rint_magic(u) : 0.0, yr = finite_uv ? rint_magic(v) : 0.0;
     // np.round ties: recompute the exact quotient when within 1e-6 px of a .5
     if (ge && finite_uv &&
@@ -482,10 +500,20 @@ __device__ __forceinline__ void dense_tile(const DenseArgs& a, const TileCtx& c,
       xr = rint_magic(u);
       yr = rint_magic(v);
     }
+#if DENSE_F32GUARD
+    // |u|, |v| < 1e9: the rounded values are exact 32-bit integers in the
+    // magic sum's low word; bounds as unsigned integer compares
+    const int xi = __double2loint(__dadd_rn(xr, 6755399441055744.0));
+    const int yi = __double2loint(__dadd_rn(yr, 6755399441055744.0));
+    const bool inside = ge && front && finite_uv && (unsigned)xi < (unsigned)Fj.w &&
+                        (unsigned)yi < (unsigned)Fj.h;
+    const int ti = inside ? yi * Fj.w + xi : 0;
+#else
     const bool inside = ge && front && finite_uv && xr >= 0.0 && xr < c.dwj && yr >= 0.0 && yr < c.dhj;
     const int ti = inside ? __double2loint(__dadd_rn(yr, 6755399441055744.0)) * Fj.w +
                                 __double2loint(__dadd_rn(xr, 6755399441055744.0))
                           : 0;
+#endif
     const float4 PT = __ldg(&Fj.P[ti]);
     const float4 NT = __ldg(&Fj.N[ti]);
     const float4 N = __ldg(&c.Ni[p]);
