@@ -358,6 +358,11 @@ __device__ __forceinline__ void tm_chunk(uint32_t tm, const double (&jp)[2][6], 
 #ifndef DENSE_F32GUARD
 #define DENSE_F32GUARD 1
 #endif
+// DENSE_TMA_P=1: stage each warp's source strip by cp.async.bulk (measured
+// 27% slower on the B200; kept as a compile-time variant)
+#ifndef DENSE_TMA_P
+#define DENSE_TMA_P 0
+#endif
 #ifndef DENSE_TMEM_BLOCKS
 #define DENSE_TMEM_BLOCKS 4
 #endif
@@ -406,7 +411,8 @@ template <bool PREV, bool FAST>
 __device__ __forceinline__ void dense_tile(const DenseArgs& a, const TileCtx& c, const Xf& rel,
                                            const FrameDev& Fj, uint32_t tm, int t, int tx, int ty,
                                            unsigned st, unsigned char* tstate, double& acc27,
-                                           double& acc28, double& eprev_p, double& eprev_g) {
+                                           double& acc28, double& eprev_p, double& eprev_g,
+                                           const float4* Ps) {
   const int lane = threadIdx.x & 31;
   const bool vis = st & 1u;
   const bool prev_here = PREV && (st & 2u);
@@ -415,7 +421,8 @@ __device__ __forceinline__ void dense_tile(const DenseArgs& a, const TileCtx& c,
   const bool live = x < c.wi && y < c.hi;
   const int p = live ? y * c.wi + x : 0;  // pixel (0: safe index)
   const int m = t * 256 + threadIdx.x;    // slot
-  const float4 P = __ldg(&c.Pi[p]);
+  // source point: this warp's strip staged in shared memory by TMA (Ps), or L1
+  const float4 P = Ps ? Ps[threadIdx.x & 31] : __ldg(&c.Pi[p]);
   const unsigned fl = live ? __float_as_uint(P.w) : 0u;
   const bool sok = vis && stride_ok(p, c.wi, a.stride);
   const bool ph = a.do_photo && sok && (fl & SFB_FLAG_VD);
@@ -633,13 +640,71 @@ __device__ __forceinline__ void dense_tiles(const DenseArgs& a, const TileCtx& c
                                             const FrameDev& Fj, uint32_t tm, int4 it,
                                             unsigned char* tile_state, double& acc27, double& acc28,
                                             double& eprev_p, double& eprev_g) {
+#if DENSE_TMA_P
+  // The source points of each warp's 16x2 strip come in by TMA bulk copies
+  // (cp.async.bulk, one per row) into a per-warp double buffer in shared
+  // memory, issued one live tile ahead and completed on a per-warp mbarrier,
+  // so a tile's dependency chain starts from shared memory.
+  __shared__ __align__(16) float4 pstrip[DENSE_THREADS / 32][2][32];
+  __shared__ __align__(8) unsigned long long pbar[DENSE_THREADS / 32][2];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    for (int b = 0; b < 2; ++b)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&pbar[w][b])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  unsigned phase = 0;  // bit b: parity of buffer b's next completion
+  auto issue = [&](int t, int b) {
+    if (lane != 0) return;
+    const int x0 = (t % c.tiles_x) * SFB_TILE, y0 = (t / c.tiles_x) * SFB_TILE + 2 * w;
+    const int nx = min(SFB_TILE, c.wi - x0);
+    const int nrow = y0 >= c.hi ? 0 : (y0 + 1 < c.hi ? 2 : 1);
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&pbar[w][b]);
+    const uint32_t bytes = (uint32_t)(nrow * nx * 16);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    for (int r = 0; r < nrow; ++r) {
+      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&pstrip[w][b][16 * r]);
+      const float4* src = c.Pi + (int64_t)(y0 + r) * c.wi + x0;
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(dst), "l"(src), "r"((uint32_t)(nx * 16)), "r"(bar) : "memory");
+    }
+  };
+  auto next_live = [&](int t) {
+    while (t < it.z && !(tile_state[t - it.y] & 3u)) ++t;
+    return t;
+  };
+  int t = next_live(it.y);
+  int b = 0;
+  if (t < it.z) issue(t, 0);
+  while (t < it.z) {
+    const int tn = next_live(t + 1);
+    __syncwarp();  // every lane is done with buffer b ^ 1 (read two tiles ago)
+    if (tn < it.z) issue(tn, b ^ 1);
+    {
+      const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&pbar[w][b]);
+      const uint32_t par = (phase >> b) & 1u;
+      uint32_t done = 0;
+      while (!done)
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(done) : "r"(bar), "r"(par) : "memory");
+      phase ^= 1u << b;
+    }
+    const unsigned st = tile_state[t - it.y];
+    dense_tile<PREV, FAST>(a, c, rel, Fj, tm, t, t % c.tiles_x, t / c.tiles_x, st,
+                           &tile_state[t - it.y], acc27, acc28, eprev_p, eprev_g, &pstrip[w][b][0]);
+    b ^= 1;
+    t = tn;
+  }
+#else
   int tx = it.y % c.tiles_x, ty = it.y / c.tiles_x;
   for (int t = it.y; t < it.z; ++t, (++tx == c.tiles_x ? (tx = 0, ++ty) : 0)) {
     const unsigned st = tile_state[t - it.y];
     if (!(st & 3u)) continue;  // nothing to associate, nothing frozen
     dense_tile<PREV, FAST>(a, c, rel, Fj, tm, t, tx, ty, st, &tile_state[t - it.y], acc27, acc28,
-                           eprev_p, eprev_g);
+                           eprev_p, eprev_g, nullptr);
   }
+#endif
 }
 
 template <bool PREV>
