@@ -847,68 +847,133 @@ void launch_dense_linearize(const DenseArgs& a, cudaStream_t s) {
   else k_dense_fused<false><<<a.n_items, DENSE_THREADS, 0, s>>>(b);
 }
 
-// Frozen-association energy at the current poses.
-__global__ void __launch_bounds__(DENSE_THREADS) k_dense_energy(DenseArgs a, double* item_e2) {
-  __shared__ double sh[12 * 2];  // rel (photo) and back (geo), plain
+// Frozen-association energy at the current poses (the last GN iteration's
+// energy_after, _energy_with_frozen_associations :662-672; the others are
+// fused into the next k_dense_fused<PREV>): the same formulation as the fused
+// pass's PREV sums - q = rel d (FMA chain), reciprocal-multiply projection,
+// one bilinear sample, geo residual n' . (q - t) with n' = R_rel n - over
+// the frozen sets only.  Tiles without a frozen association are skipped by
+// their flag, warps without one warp-uniformly; each pixel's loads issue
+// together (clamped indices, predicate selects).
+__device__ __forceinline__ void bilinear_val2_fast(const FrameDev& f, double x, double y, double val[2]) {
+  const int xf = __double2int_rd(x), yf = __double2int_rd(y);
+  const int x0 = min(max(xf, 0), f.w - 2), y0 = min(max(yf, 0), f.h - 2);
+  double ax = x - (double)x0, ay = y - (double)y0;
+  ax = xf < 0 ? 0.0 : (xf > f.w - 2 ? 1.0 : ax);
+  ay = yf < 0 ? 0.0 : (yf > f.h - 2 ? 1.0 : ay);
+  const float4 t0 = __ldg(&f.T[2 * (y0 * f.w + x0)]);
+  const float4 t1 = __ldg(&f.T[2 * (y0 * f.w + x0) + 1]);
+  const double v00[2] = {t0.x, t0.y}, v01[2] = {t0.z, t0.w};
+  const double v10[2] = {t1.x, t1.y}, v11[2] = {t1.z, t1.w};
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const double d01 = v01[c] - v00[c], d10 = v10[c] - v00[c];
+    const double dxy = (v11[c] - v10[c]) - d01;
+    val[c] = fma(ay, fma(ax, dxy, d10), fma(ax, d01, v00[c]));
+  }
+}
+
+#ifndef ENERGY_ILP
+#define ENERGY_ILP 2  // flagged tiles evaluated together per iteration
+#endif
+#ifndef ENERGY_BLOCKS
+#define ENERGY_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(DENSE_THREADS, ENERGY_BLOCKS) k_dense_energy(DenseArgs a, double* item_e2) {
+  __shared__ Xf rel;
+  __shared__ FrameDev Fj;
+  __shared__ const float4* sPi;
+  __shared__ const float4* sNi;
+  __shared__ const float2* sGi;
+  __shared__ int swi, stx;
+  __shared__ unsigned char tflag[DENSE_MAX_TILES];
   const int4 it = a.items[blockIdx.x];
   const int2 de = a.dir_edges[it.x];
+  const int toff = (int)(a.geo_off[it.x] >> 8);
+  if (threadIdx.x < 12) (&rel.R[0])[threadIdx.x] = a.edge_rel[12 * (int64_t)it.x + threadIdx.x];
   if (threadIdx.x == 0) {
-    const PoseDev& Pi = a.poses[de.x];
-    const PoseDev& Pj = a.poses[de.y];
-    double iR[9], itt[3];
-    // relative = pose_j^-1 o pose_i (solver.py:267); back = pose_i^-1 o pose_j (:281)
-    xf_inverse_plain(Pj.R, Pj.t, iR, itt);
-    for (int r = 0; r < 3; ++r) {
-      for (int c = 0; c < 3; ++c)
-        sh[r * 3 + c] = iR[r * 3 + 0] * Pi.R[0 * 3 + c] + iR[r * 3 + 1] * Pi.R[1 * 3 + c] + iR[r * 3 + 2] * Pi.R[2 * 3 + c];
-      sh[9 + r] = iR[r * 3 + 0] * Pi.t[0] + iR[r * 3 + 1] * Pi.t[1] + iR[r * 3 + 2] * Pi.t[2] + itt[r];
-    }
-    xf_inverse_plain(Pi.R, Pi.t, iR, itt);
-    for (int r = 0; r < 3; ++r) {
-      for (int c = 0; c < 3; ++c)
-        sh[12 + r * 3 + c] = iR[r * 3 + 0] * Pj.R[0 * 3 + c] + iR[r * 3 + 1] * Pj.R[1 * 3 + c] + iR[r * 3 + 2] * Pj.R[2 * 3 + c];
-      sh[21 + r] = iR[r * 3 + 0] * Pj.t[0] + iR[r * 3 + 1] * Pj.t[1] + iR[r * 3 + 2] * Pj.t[2] + itt[r];
-    }
+    const FrameDev& Fi = a.frames[de.x];
+    Fj = a.frames[de.y];
+    sPi = Fi.P;
+    sNi = Fi.N;
+    sGi = Fi.G;
+    swi = Fi.w;
+    stx = Fi.tiles_x;
   }
-  const FrameDev Fi = a.frames[de.x];
-  const FrameDev Fj = a.frames[de.y];
+  for (int t = it.y + threadIdx.x; t < it.z; t += blockDim.x) tflag[t - it.y] = a.tile_any[toff + t];
   __syncthreads();
   const uint32_t* pmask = a.photo_mask + a.photo_off[it.x];
   const uint16_t* gtgt = a.geo_tgt + a.geo_off[it.x];
+  const int lane = threadIdx.x & 31;
+  auto next = [&](int t) {
+    while (t < it.z && !tflag[t - it.y]) ++t;  // nothing frozen in skipped tiles
+    return t;
+  };
   double acc[2] = {0.0, 0.0};
-  const int toff = (int)(a.geo_off[it.x] >> 8);
-  for (int t = it.y; t < it.z; ++t) {  // tile-major slots, as k_dense_fused
-    if (!a.tile_any[toff + t]) continue;  // nothing frozen in this tile
-    const int m = t * 256 + threadIdx.x;
-    const bool ph = a.do_photo && ((pmask[m >> 5] >> (m & 31)) & 1u);
-    const int tg = a.do_geo ? (int)gtgt[m] : 0xFFFF;
-    if (!ph && tg == 0xFFFF) continue;
-    const int p = ((t / Fi.tiles_x) * SFB_TILE + (threadIdx.x / SFB_TILE)) * Fi.w +
-                  (t % Fi.tiles_x) * SFB_TILE + (threadIdx.x & (SFB_TILE - 1));
-    const float4 P = __ldg(&Fi.P[p]);
-    if (ph) {
-      double q[3];
-      xf_apply(sh, sh + 9, P.x, P.y, P.z, q);
-      const double zs = q[2] > 0.0 ? q[2] : 1.0;
-      // reciprocal-multiply projection as k_dense_fused's frozen energy; the
-      // F2I-floor bilinear issues its tap loads sooner than the FP64 rint form
-      const double rz = __drcp_rn(zs);
-      const double u = fma(Fj.fx * q[0], rz, Fj.cx);
-      const double v = fma(Fj.fy * q[1], rz, Fj.cy);
-      double val[2], ddx[2], ddy[2];
-      bilinear_grad2(Fj, u, v, val, ddx, ddy);
-      const float2 ref = __ldg(&Fi.G[p]);
-      const double r0 = (double)ref.x - val[0], r1 = (double)ref.y - val[1];
-      acc[0] += r0 * r0 + r1 * r1;
+  int t0 = next(it.y);
+  while (t0 < it.z) {
+    // ENERGY_ILP flagged tiles at once, each stage's loads of all of them in
+    // flight together (the pass is bound by its dependent-load chain)
+    int tt[ENERGY_ILP];
+    tt[0] = t0;
+#pragma unroll
+    for (int k = 1; k < ENERGY_ILP; ++k) tt[k] = tt[k - 1] < it.z ? next(tt[k - 1] + 1) : it.z;
+    t0 = tt[ENERGY_ILP - 1] < it.z ? next(tt[ENERGY_ILP - 1] + 1) : it.z;
+    uint32_t wb[ENERGY_ILP];
+    int tg[ENERGY_ILP];
+#pragma unroll
+    for (int k = 0; k < ENERGY_ILP; ++k) {
+      const bool ok = tt[k] < it.z;
+      const int m = (ok ? tt[k] : it.y) * 256 + threadIdx.x;
+      wb[k] = ok && a.do_photo ? pmask[m >> 5] : 0u;
+      tg[k] = ok && a.do_geo ? (int)gtgt[m] : 0xFFFF;
     }
-    if (tg != 0xFFFF) {
-      const float4 N = __ldg(&Fi.N[p]);
-      const float4 PT = __ldg(&Fj.P[tg]);
-      double mp[3];
-      xf_apply(sh + 12, sh + 21, PT.x, PT.y, PT.z, mp);
-      const double r = (double)N.x * ((double)P.x - mp[0]) + (double)N.y * ((double)P.y - mp[1]) +
-                       (double)N.z * ((double)P.z - mp[2]);
-      acc[1] += r * r;
+    bool ph[ENERGY_ILP], ge[ENERGY_ILP];
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < ENERGY_ILP; ++k) {
+      ph[k] = (wb[k] >> lane) & 1u;
+      ge[k] = tg[k] != 0xFFFF;
+      any |= ph[k] || ge[k];
+    }
+    if (!__any_sync(0xffffffffu, any)) continue;  // warp-uniform
+    float4 P[ENERGY_ILP], N[ENERGY_ILP], PP[ENERGY_ILP];
+    float2 G[ENERGY_ILP];
+#pragma unroll
+    for (int k = 0; k < ENERGY_ILP; ++k) {
+      const int t = tt[k] < it.z ? tt[k] : it.y;
+      const int p = ((t / stx) * SFB_TILE + (threadIdx.x / SFB_TILE)) * swi + (t % stx) * SFB_TILE +
+                    (threadIdx.x & (SFB_TILE - 1));
+      const int pc = (ph[k] || ge[k]) ? p : 0;  // inactive lanes: a safe index
+      P[k] = __ldg(&sPi[pc]);
+      N[k] = __ldg(&sNi[ge[k] ? pc : 0]);
+      PP[k] = __ldg(&Fj.P[ge[k] ? tg[k] : 0]);
+      G[k] = __ldg(&sGi[ph[k] ? pc : 0]);
+    }
+    double ua[ENERGY_ILP], va[ENERGY_ILP];
+#pragma unroll
+    for (int k = 0; k < ENERGY_ILP; ++k) {
+      const double d0 = P[k].x, d1 = P[k].y, d2 = P[k].z;
+      const double q0 = __dadd_rn(__fma_rn(d2, rel.R[2], __fma_rn(d1, rel.R[1], __dmul_rn(d0, rel.R[0]))), rel.t[0]);
+      const double q1 = __dadd_rn(__fma_rn(d2, rel.R[5], __fma_rn(d1, rel.R[4], __dmul_rn(d0, rel.R[3]))), rel.t[1]);
+      const double q2 = __dadd_rn(__fma_rn(d2, rel.R[8], __fma_rn(d1, rel.R[7], __dmul_rn(d0, rel.R[6]))), rel.t[2]);
+      const double n0 = N[k].x, n1 = N[k].y, n2 = N[k].z;
+      const double nr0 = __fma_rn(n2, rel.R[2], __fma_rn(n1, rel.R[1], __dmul_rn(n0, rel.R[0])));
+      const double nr1 = __fma_rn(n2, rel.R[5], __fma_rn(n1, rel.R[4], __dmul_rn(n0, rel.R[3])));
+      const double nr2 = __fma_rn(n2, rel.R[8], __fma_rn(n1, rel.R[7], __dmul_rn(n0, rel.R[6])));
+      const double r = nr0 * (q0 - (double)PP[k].x) + nr1 * (q1 - (double)PP[k].y) + nr2 * (q2 - (double)PP[k].z);
+      acc[1] += ge[k] ? r * r : 0.0;
+      const double z = q2 > 0.0 ? q2 : 1.0;
+      const double rz = rcp_depth(z);
+      ua[k] = ph[k] ? fma(__dmul_rn(Fj.fx, q0), rz, Fj.cx) : 0.0;
+      va[k] = ph[k] ? fma(__dmul_rn(Fj.fy, q1), rz, Fj.cy) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < ENERGY_ILP; ++k) {
+      double val[2];
+      bilinear_val2_fast(Fj, ua[k], va[k], val);
+      const double r0 = (double)G[k].x - val[0], r1 = (double)G[k].y - val[1];
+      acc[0] += ph[k] ? r0 * r0 + r1 * r1 : 0.0;
     }
   }
   block_reduce_store<2>(acc, item_e2 + 2 * (int64_t)blockIdx.x);
@@ -916,6 +981,8 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_dense_energy(DenseArgs a, dou
 
 void launch_dense_energy(const DenseArgs& a, double* item_e2, cudaStream_t s) {
   if (a.n_items <= 0) return;
+  sfb_count_launch();
+  k_edge_rel<<<(a.n_dir + 127) / 128, 128, 0, s>>>(a.dir_edges, a.poses, a.rd, a.n_dir, a.edge_rel);
   sfb_count_launch();
   k_dense_energy<<<a.n_items, DENSE_THREADS, 0, s>>>(a, item_e2);
 }
@@ -1056,11 +1123,17 @@ void launch_edge_reduce2(const int* edge_item_ptr, const double* item_e2, double
 //  B lists (per pair):    0 set +H_ij   1 set +H_ij^T   4 dense -H
 __device__ __forceinline__ double sym_full(const double* h, int r, int c) { return h[sym6(r, c)]; }
 
-__global__ void k_assemble(AssembleArgs a) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (warp < a.n_blk) {
-    const int v = warp;
+// Diagonal rows: one CTA of ASM_DIAG_WARPS warps per block row; warp w sums
+// the contributions w, w + W, ... of the row's list in list order, 8 loads in
+// flight, and the warps' partials are added in warp order (deterministic).
+// Pair blocks: one warp per pair (short lists).
+#define ASM_DIAG_WARPS 4
+#define ASM_BATCH 8
+__global__ void __launch_bounds__(ASM_DIAG_WARPS * 32) k_assemble(AssembleArgs a) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if ((int)blockIdx.x < a.n_blk) {
+    __shared__ double sd[ASM_DIAG_WARPS][3][32];
+    const int v = blockIdx.x;
     double d0 = 0.0, d1 = 0.0, gv = 0.0;
     const int e0 = lane, e1 = lane + 32;  // matrix entries handled by this lane
     // one contribution's (diagonal entry pair, gradient entry); loads only,
@@ -1090,16 +1163,19 @@ __global__ void k_assemble(AssembleArgs a) {
       }
     };
     const int k0 = a.d_ptr[v], k1 = a.d_ptr[v + 1];
-    for (int kb = k0; kb < k1; kb += 32) {
-      const int ent_l = kb + lane < k1 ? a.d_ent[kb + lane] : 0;  // 32 list entries at once
-      const int nk = min(32, k1 - kb);
+    constexpr int SPAN = 32 * ASM_DIAG_WARPS;
+    for (int kb = k0; kb < k1; kb += SPAN) {
+      // this warp's entries of the span: kb + wid + W * j, j < 32
+      const int kl = kb + wid + ASM_DIAG_WARPS * lane;
+      const int ent_l = kl < k1 ? a.d_ent[kl] : 0;
+      const int nk = max(0, min(32, (k1 - kb - wid + ASM_DIAG_WARPS - 1) / ASM_DIAG_WARPS));
       int j = 0;
-      for (; j + 4 <= nk; j += 4) {
-        double x0[4], x1[4], xg[4];
+      for (; j + ASM_BATCH <= nk; j += ASM_BATCH) {
+        double x0[ASM_BATCH], x1[ASM_BATCH], xg[ASM_BATCH];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) fetch(__shfl_sync(0xffffffffu, ent_l, j + u), x0[u], x1[u], xg[u]);
+        for (int u = 0; u < ASM_BATCH; ++u) fetch(__shfl_sync(0xffffffffu, ent_l, j + u), x0[u], x1[u], xg[u]);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {  // list order: the sums are assembled deterministically
+        for (int u = 0; u < ASM_BATCH; ++u) {  // list order within the warp
           d0 += x0[u];
           d1 += x1[u];
           gv += xg[u];
@@ -1113,17 +1189,33 @@ __global__ void k_assemble(AssembleArgs a) {
         gv += xg;
       }
     }
-    double* D = a.D + (int64_t)v * 36;
-    double* S = a.Brow + (int64_t)a.row_ptr[v] * 36;
-    D[e0] = d0;
-    S[e0] = d0;
-    if (e1 < 36) {
-      D[e1] = d1;
-      S[e1] = d1;
+    sd[wid][0][lane] = d0;
+    sd[wid][1][lane] = d1;
+    sd[wid][2][lane] = gv;
+    __syncthreads();
+    if (wid == 0) {
+      d0 = sd[0][0][lane];
+      d1 = sd[0][1][lane];
+      gv = sd[0][2][lane];
+#pragma unroll
+      for (int w = 1; w < ASM_DIAG_WARPS; ++w) {
+        d0 += sd[w][0][lane];
+        d1 += sd[w][1][lane];
+        gv += sd[w][2][lane];
+      }
+      double* D = a.D + (int64_t)v * 36;
+      double* S = a.Brow + (int64_t)a.row_ptr[v] * 36;
+      D[e0] = d0;
+      S[e0] = d0;
+      if (e1 < 36) {
+        D[e1] = d1;
+        S[e1] = d1;
+      }
+      if (lane < 6) a.g[v * 6 + lane] = gv;
     }
-    if (lane < 6) a.g[v * 6 + lane] = gv;
-  } else if (warp < a.n_blk + a.n_pairs) {
-    const int q = warp - a.n_blk;
+  } else {
+    const int q = ((int)blockIdx.x - a.n_blk) * ASM_DIAG_WARPS + wid;
+    if (q >= a.n_pairs) return;
     double b0 = 0.0, b1 = 0.0;
     const int e0 = lane, e1 = lane + 32;
     for (int k = a.b_ptr[q]; k < a.b_ptr[q + 1]; ++k) {
@@ -1159,34 +1251,69 @@ __global__ void k_assemble(AssembleArgs a) {
 }
 
 void launch_assemble(const AssembleArgs& a, cudaStream_t s) {
-  const int warps = a.n_blk + a.n_pairs;
-  if (warps <= 0) return;
+  const int blocks = a.n_blk + (a.n_pairs + ASM_DIAG_WARPS - 1) / ASM_DIAG_WARPS;
+  if (blocks <= 0) return;
   sfb_count_launch();
-  k_assemble<<<(warps * 32 + 255) / 256, 256, 0, s>>>(a);
+  k_assemble<<<blocks, ASM_DIAG_WARPS * 32, 0, s>>>(a);
 }
 
 // Deterministic single-block sums of the per-set / per-edge / per-item energies.
 // mode 0: out = {sum set E, sum edge e_photo, sum edge e_geo}
 // mode 1: out = {sum set E, sum item_e2[2i], sum item_e2[2i+1]}
-__global__ void k_sum_energies(const double* set_out, int n_sets, const double* edge_out,
+__global__ void __launch_bounds__(1024) k_sum_energies(const double* set_out, int n_sets, const double* edge_out,
                                int n_dir, const double* item_e2, int n_items, double* out3,
                                int mode) {
   // mode 0 writes 5 values: {set E, edge e_photo, edge e_geo, edge prev e_photo, edge prev e_geo}
   __shared__ double sh[5][32];
   double s[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-  for (int i = threadIdx.x; i < n_sets; i += blockDim.x) s[0] += set_out[(int64_t)i * SFB_SET_STRIDE + SFB_SET_E];
+  // each thread's values in index order, 8 strided loads in flight per batch
+  constexpr int U = 8;
+  const int bd = blockDim.x;
+  for (int i0 = threadIdx.x; i0 < n_sets; i0 += U * bd) {
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * bd;
+      v[u] = i < n_sets ? set_out[(int64_t)i * SFB_SET_STRIDE + SFB_SET_E] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) s[0] += v[u];
+  }
   if (mode == 0) {
-    for (int i = threadIdx.x; i < n_dir; i += blockDim.x) {
-      const double* e = edge_out + (int64_t)i * SFB_ITEM_STRIDE;
-      s[1] += e[SFB_ITEM_EP];
-      s[2] += e[SFB_ITEM_EG];
-      s[3] += e[SFB_ITEM_PP];
-      s[4] += e[SFB_ITEM_PG];
+    constexpr int UE = 4;
+    for (int i0 = threadIdx.x; i0 < n_dir; i0 += UE * bd) {
+      double v[UE][4];
+#pragma unroll
+      for (int u = 0; u < UE; ++u) {
+        const int i = i0 + u * bd;
+        const double* e = edge_out + (int64_t)(i < n_dir ? i : 0) * SFB_ITEM_STRIDE;
+        const bool ok = i < n_dir;
+        v[u][0] = ok ? e[SFB_ITEM_EP] : 0.0;
+        v[u][1] = ok ? e[SFB_ITEM_EG] : 0.0;
+        v[u][2] = ok ? e[SFB_ITEM_PP] : 0.0;
+        v[u][3] = ok ? e[SFB_ITEM_PG] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < UE; ++u) {
+        s[1] += v[u][0];
+        s[2] += v[u][1];
+        s[3] += v[u][2];
+        s[4] += v[u][3];
+      }
     }
   } else {
-    for (int i = threadIdx.x; i < n_items; i += blockDim.x) {
-      s[1] += item_e2[2 * (int64_t)i];
-      s[2] += item_e2[2 * (int64_t)i + 1];
+    for (int i0 = threadIdx.x; i0 < n_items; i0 += U * bd) {
+      double2 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * bd;
+        v[u] = i < n_items ? reinterpret_cast<const double2*>(item_e2)[i] : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        s[1] += v[u].x;
+        s[2] += v[u].y;
+      }
     }
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
