@@ -118,6 +118,7 @@ struct sfb_problem : Handle {
   bool have_solution = false;
   // scalars
   DBuf<double> dscal;       // device scalars
+  DBuf<double> esum;        // k_sum_energies scratch (CTA partials + ticket)
   double* hscal = nullptr;  // pinned mirror
   Prof prof;
   // pair-filter scratch
@@ -537,10 +538,10 @@ int enqueue_linearize_end(sfb_problem* p) {
     }
   }
   launch_sum_energies(p->set_out.p, p->n_sets, p->edge_out.p, dense_on ? p->n_dir : 0, nullptr, 0,
-                      p->dscal.p, 0, s);
+                      p->dscal.p, 0, p->esum.p, s);
   CKL(p);
   if (p->pending_prev_mode == 2) {  // separate frozen-energy pass: sums -> dscal[16..18]
-    launch_sum_energies(nullptr, 0, nullptr, 0, p->edge_e2.p, p->n_dir, p->dscal.p + 16, 1, s);
+    launch_sum_energies(nullptr, 0, nullptr, 0, p->edge_e2.p, p->n_dir, p->dscal.p + 16, 1, p->esum.p, s);
     CKL(p);
   }
   p->dense_active = dense_on;
@@ -585,7 +586,7 @@ int enqueue_energy_frozen_begin(sfb_problem* p, int dense) {
 int enqueue_energy_frozen_end(sfb_problem* p, double* dout3) {
   const bool d = p->pending_energy_dense;
   launch_sum_energies(p->set_out.p, p->n_sets, nullptr, 0, p->edge_e2.p, d ? p->n_dir : 0, dout3,
-                      1, p->stream);
+                      1, p->esum.p, p->stream);
   CKL(p);
   return SFB_OK;
 }
@@ -949,9 +950,12 @@ int sfb_problem_create(sfb_ctx* c, int32_t n_frames, const int32_t* slots, int32
   if (p->g.ensure(nv) || p->x.ensure(nv) || p->r.ensure(nv) || p->z.ensure(nv) || p->pv.ensure(nv) ||
       p->Ap.ensure(nv) || p->inv_diag.ensure(nv) || p->bvec.ensure(nv) || p->jdiag.ensure(nv) ||
       p->pv2.ensure(nv) || p->tmp.ensure(2 * nv) ||
-      p->part.ensure(4 * 1024) || p->flags.ensure(64) || p->dscal.ensure(64))
+      p->part.ensure(4 * 1024) || p->flags.ensure(64) || p->dscal.ensure(64) ||
+      p->esum.ensure(SUM_ENERGY_SCRATCH))
     return bail(SFB_E_OOM, "vectors");
   if (pinned_scalars(&p->hscal) != cudaSuccess) return bail(SFB_E_OOM, "pinned");
+  if (cudaMemsetAsync(p->esum.p, 0, sizeof(double) * SUM_ENERGY_SCRATCH, s) != cudaSuccess)
+    return bail(SFB_E_CUDA, "energy-sum scratch");
   // host arrays are borrowed for the call only: the async copies above must
   // have landed before returning (they may come from reusable staging)
   if (p->n_corr > 0 && cudaStreamSynchronize(s) != cudaSuccess) return bail(SFB_E_CUDA, "points upload");
@@ -976,7 +980,7 @@ int sfb_problem_destroy(sfb_problem* p) {
                         &p->item_out, &p->edge_out, &p->item_e2, &p->D, &p->B, &p->g, &p->x,
                         &p->r, &p->z, &p->pv, &p->Ap, &p->inv_diag, &p->bvec, &p->part, &p->tmp, &p->jdiag,
                         &p->pv2, &p->Brow, &p->bj_inv,
-                        &p->dscal};
+                        &p->dscal, &p->esum};
   for (auto* b : db) b->release();
   p->pair_key.release();
   p->edges_d.release();

@@ -223,9 +223,11 @@ void launch_edge_reduce(const int* edge_item_ptr, const double* item_out, double
 void launch_p2p_sync(unsigned* const* peer_flags, unsigned* my_flags, int rank, int world,
                      unsigned epoch, cudaStream_t s);
 void launch_assemble(const AssembleArgs& a, cudaStream_t s);
+// scratch: SUM_ENERGY_SCRATCH doubles, zero before the first launch
+#define SUM_ENERGY_SCRATCH 168
 void launch_sum_energies(const double* set_out, int n_sets, const double* edge_out, int n_dir,
                          const double* item_e2, int n_items, double* out3, int mode,
-                         cudaStream_t s);
+                         double* scratch, cudaStream_t s);
 cudaError_t launch_pcg(const PcgArgs& a, int n_sm, cudaStream_t s);
 cudaError_t launch_pcg_dense(const PcgArgs& a, const double* A, int n_sm, cudaStream_t s);
 void launch_matvec(const PcgArgs& a, const double* xin, double* yout, cudaStream_t s);

@@ -16,6 +16,7 @@
 //  * every CTA sums the per-CTA partials in the same order, so all scalars,
 //    breaks and restarts are grid-uniform and bit-reproducible.
 #include "sfb_kernels.cuh"
+#include <type_traits>
 
 #define PCG_THREADS 256
 #define PCG_WARPS (PCG_THREADS / 32)
@@ -61,9 +62,14 @@ template <bool FOLD>
 __device__ __forceinline__ double row_product(const PcgArgs& a, const RowCtx& rc, int v,
                                               const double* __restrict__ z,
                                               const double* __restrict__ pold, double beta,
-                                              int lane) {
+                                              int lane, int part = 0, int nparts = 1) {
   const int grp = lane / 6, r = lane - 6 * grp;
-  const int e0 = a.row_ptr[v], e1 = a.row_ptr[v + 1];
+  int e0 = a.row_ptr[v], e1 = a.row_ptr[v + 1];
+  if (nparts > 1) {  // this warp's share of the row's slots (split rows)
+    const int n = e1 - e0;
+    e1 = e0 + (n * (part + 1)) / nparts;
+    e0 = e0 + (n * part) / nparts;
+  }
   double acc = 0.0;
   for (int c0 = e0; c0 < e1; c0 += PCG_GATHER_CAP) {
     const int c1 = min(e1, c0 + PCG_GATHER_CAP);
@@ -237,17 +243,20 @@ __device__ __forceinline__ double sum6(double v) {
 struct BsrMv {
   template <bool FOLD>
   __device__ __forceinline__ double row(const PcgArgs& a, const RowCtx& rc, int v, const double* z,
-                                        const double* pold, double beta, int lane) const {
-    return row_product<FOLD>(a, rc, v, z, pold, beta, lane);
+                                        const double* pold, double beta, int lane, int part = 0,
+                                        int nparts = 1) const {
+    return row_product<FOLD>(a, rc, v, z, pold, beta, lane, part, nparts);
   }
   __device__ __forceinline__ bool stageable() const { return true; }
+  static constexpr bool kSplit = true;  // rows may be split over warps
 };
 
 struct DenseMv {
   const double* A;  // (6 n_blk)^2 row-major, zero padded
   template <bool FOLD>
   __device__ __forceinline__ double row(const PcgArgs& a, const RowCtx&, int v, const double* z,
-                                        const double* pold, double beta, int lane) const {
+                                        const double* pold, double beta, int lane, int = 0,
+                                        int = 1) const {
     const int n6 = 6 * a.n_blk;
     double out = 0.0;
     for (int r = 0; r < 6; ++r) {
@@ -263,6 +272,7 @@ struct DenseMv {
     return out;
   }
   __device__ __forceinline__ bool stageable() const { return false; }
+  static constexpr bool kSplit = false;
 };
 
 #ifdef PCG_TRACE
@@ -477,6 +487,10 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg(PcgArgs a, Mv mv, int ro
 #ifndef PCG_RMAX
 #define PCG_RMAX 2
 #endif
+#ifndef PCG_SPLIT_MAX
+#define PCG_SPLIT_MAX 8     // warps per block row at most (k_pcg_reg<.., SPLIT>)
+#endif
+#define PCG_CLUSTER_SMALL 2  // unsplit grids of <= this many CTAs stay one cluster
 
 __device__ __forceinline__ double rsel(const double (&a)[PCG_RMAX], int j) {
   double v = a[0];
@@ -536,7 +550,7 @@ struct ClusterSync {
   }
 };
 
-template <class Mv, bool CL>
+template <class Mv, bool CL, int SPLIT>
 __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg_reg(PcgArgs a, Mv mv, int rows_per_cta) {
   extern __shared__ __align__(16) double smem[];
   GridBarrier grid{reinterpret_cast<unsigned*>(a.flags), 0u};
@@ -545,7 +559,11 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg_reg(PcgArgs a, Mv mv, in
   __shared__ double sh[4][PCG_WARPS];
   const int G = gridDim.x;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const bool own = lane < 6;
+  // SPLIT warps per block row (each sums its share of the row's slots; the
+  // first holds the row's vectors): PCG_WARPS / SPLIT row groups per CTA
+  constexpr int RW = PCG_WARPS / SPLIT;
+  const int rgw = wid / SPLIT, part = wid % SPLIT;
+  const bool own = lane < 6 && part == 0;
   if (a.skip && *a.skip != 0.0) return;  // grid-uniform
   RowCtx rc;
   rc.r0 = min(a.n_blk, blockIdx.x * rows_per_cta);
@@ -573,8 +591,32 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg_reg(PcgArgs a, Mv mv, in
     rc.s_end = rc.s0 + (int)ns;
   }
   __syncthreads();
-  // rows of this warp: rc.r0 + wid + PCG_WARPS * j, j < nrow (<= PCG_RMAX)
-  const int nrow = rc.r1 > rc.r0 + wid ? (rc.r1 - rc.r0 - wid + PCG_WARPS - 1) / PCG_WARPS : 0;
+  // rows of this warp: rc.r0 + rgw + RW * j, j < nrow (<= PCG_RMAX)
+  const int nrow = rc.r1 > rc.r0 + rgw ? (rc.r1 - rc.r0 - rgw + RW - 1) / RW : 0;
+  // y = A xin over this CTA's rows, the row parts added in part order
+  __shared__ double ysh[PCG_WARPS][PCG_RMAX][6];
+  auto rows_product = [&](auto fold_tag, const double* zin, const double* xin, double bt,
+                          double (&yv)[PCG_RMAX]) {
+    constexpr bool FOLD = decltype(fold_tag)::value;
+#pragma unroll
+    for (int j = 0; j < PCG_RMAX; ++j) {
+      yv[j] = 0.0;
+      if (j < nrow) yv[j] = mv.template row<FOLD>(a, rc, rc.r0 + rgw + RW * j, zin, xin, bt, lane, part, SPLIT);
+    }
+    if constexpr (SPLIT > 1) {
+      if (part > 0 && lane < 6) {
+#pragma unroll
+        for (int j = 0; j < PCG_RMAX; ++j) ysh[wid][j][lane] = yv[j];
+      }
+      __syncthreads();
+      if (part == 0) {
+#pragma unroll
+        for (int j = 0; j < PCG_RMAX; ++j)
+#pragma unroll
+          for (int h = 1; h < SPLIT; ++h) yv[j] += ysh[wid + h][j][lane < 6 ? lane : 0];
+      }
+    }
+  };
   double xr[PCG_RMAX], rr_[PCG_RMAX], zr[PCG_RMAX], br[PCG_RMAX], idr[PCG_RMAX], pr[PCG_RMAX],
       apr[PCG_RMAX];
 #pragma unroll
@@ -589,7 +631,7 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg_reg(PcgArgs a, Mv mv, in
   {
     double v[2] = {0.0, 0.0};
     for (int j = 0; j < nrow; ++j) {
-      const int row = rc.r0 + wid + PCG_WARPS * j;
+      const int row = rc.r0 + rgw + RW * j;
       double bb = 0.0, bz = 0.0;
       const int i = 6 * row + (own ? lane : 0);
       const double bi = own ? -a.g[i] : 0.0;
@@ -638,10 +680,12 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg_reg(PcgArgs a, Mv mv, in
       double pAp_a[1];
       {
         double v[1] = {0.0};
+        double yv[PCG_RMAX];
+        if (fold) rows_product(std::true_type{}, a.z, pa, beta, yv);
+        else rows_product(std::false_type{}, a.z, pa, beta, yv);
         for (int j = 0; j < nrow; ++j) {
-          const int row = rc.r0 + wid + PCG_WARPS * j;
-          const double y = fold ? mv.template row<true>(a, rc, row, a.z, pa, beta, lane)
-                                : mv.template row<false>(a, rc, row, a.z, pa, beta, lane);
+          const int row = rc.r0 + rgw + RW * j;
+          const double y = rsel(yv, j);
           double pAp = 0.0;
           if (own) {
             const double pold = rsel(pr, j);
@@ -676,7 +720,7 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg_reg(PcgArgs a, Mv mv, in
       {
         double v[3] = {0.0, 0.0, 0.0};
         for (int j = 0; j < nrow; ++j) {
-          const int row = rc.r0 + wid + PCG_WARPS * j;
+          const int row = rc.r0 + rgw + RW * j;
           double rrv = 0.0, rzv = 0.0, bad = 0.0;
           if (own) {
             const int i = 6 * row + lane;
@@ -703,9 +747,11 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg_reg(PcgArgs a, Mv mv, in
         if (restart) {
           if constexpr (CL) csync.barrier();  // x complete
           else grid.sync(G);
+          double yv[PCG_RMAX];
+          rows_product(std::false_type{}, nullptr, a.x, 0.0, yv);
           for (int j = 0; j < nrow; ++j) {
-            const int row = rc.r0 + wid + PCG_WARPS * j;
-            const double y = mv.template row<false>(a, rc, row, nullptr, a.x, 0.0, lane);
+            const int row = rc.r0 + rgw + RW * j;
+            const double y = rsel(yv, j);
             double rrv = 0.0, rzv = 0.0;
             const double ri = own ? rsel(br, j) - y : 0.0;
             const double zi = precond(a, row, ri, rsel(idr, j), lane);
@@ -752,7 +798,7 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg_reg(PcgArgs a, Mv mv, in
     }
   }
   for (int j = 0; j < nrow; ++j)
-    if (own) a.x[6 * (rc.r0 + wid + PCG_WARPS * j) + lane] = rsel(xr, j);
+    if (own) a.x[6 * (rc.r0 + rgw + RW * j) + lane] = rsel(xr, j);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     a.out_scalars[0] = (double)iterations;
     a.out_scalars[1] = relative;
@@ -843,14 +889,36 @@ static cudaError_t launch_pcg_t(const PcgArgs& a, Mv mv, int n_sm, cudaStream_t 
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k_pcg<DenseMv>, cudaFuncAttributeMaxDynamicSharedMemorySize, PCG_SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_pcg_reg<BsrMv, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, PCG_SMEM_BYTES);
+    e = cudaFuncSetAttribute(k_pcg_reg<BsrMv, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, PCG_SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_pcg_reg<DenseMv, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, PCG_SMEM_BYTES);
+    e = cudaFuncSetAttribute(k_pcg_reg<BsrMv, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, PCG_SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_pcg_reg<BsrMv, false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, PCG_SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_pcg_reg<BsrMv, false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, PCG_SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_pcg_reg<DenseMv, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, PCG_SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  // one CTA per SM at most (co-residency, cheapest barrier); rows split evenly
-  int G = (a.n_blk + PCG_WARPS - 1) / PCG_WARPS;
+  // one CTA per SM at most (co-residency, cheapest barrier); rows split
+  // evenly.  A block row is summed by `split` warps when the grid still fits
+  // the SMs that way (more SMs gathering the neighbour vectors).
+  static const int split_env = [] {
+    const char* v = getenv("SFB_PCG_SPLIT");
+    return v ? atoi(v) : 0;
+  }();
+  // Default: the widest split whose grid (one row group per warp group) still
+  // fits the SMs, except for tiny systems (<= 2 CTAs unsplit), which run as
+  // one cluster.  Measured per 50-iteration solve: cfg4 split 2 388 us vs
+  // 457 unsplit; cfg3 split 8 318 vs 398 (cluster of 13); cfg2 cluster 216
+  // vs 278-292 split.
+  int split = PCG_SPLIT_MAX;
+  if ((a.n_blk + PCG_WARPS - 1) / PCG_WARPS <= PCG_CLUSTER_SMALL) split = 1;
+  if (split_env == 1 || split_env == 2 || split_env == 4 || split_env == 8) split = split_env;
+  if (!Mv::kSplit) split = 1;
+  while (split > 1 && (a.n_blk + PCG_WARPS / split - 1) / (PCG_WARPS / split) > n_sm) split /= 2;
+  int G = (a.n_blk + PCG_WARPS / split - 1) / (PCG_WARPS / split);
   if (G > n_sm) G = n_sm;
   static const int forced = [] {
     const char* v = getenv("SFB_PCG_BLOCKS");
@@ -871,18 +939,19 @@ static cudaError_t launch_pcg_t(const PcgArgs& a, Mv mv, int n_sm, cudaStream_t 
 #ifndef PCG_REG
 #define PCG_REG 1
 #endif
-  const bool reg = PCG_REG && rows_per_cta <= PCG_WARPS * PCG_RMAX;
+  if (rows_per_cta > (PCG_WARPS / split) * PCG_RMAX) split = 1;
+  const bool reg = PCG_REG && rows_per_cta <= (PCG_WARPS / split) * PCG_RMAX;
 #ifndef PCG_CLUSTER
 #define PCG_CLUSTER 1
 #endif
-  if (PCG_CLUSTER && reg && G > 1 && G <= PCG_CLUSTER_MAX) {
+  if (PCG_CLUSTER && reg && split == 1 && G > 1 && G <= PCG_CLUSTER_MAX) {
     // small system: the whole grid as ONE thread-block cluster (hardware
     // cluster barrier + DSMEM reductions instead of the global grid barrier)
     static int cl_ok = -1;  // cluster launch of this size available (once)
     if (cl_ok < 0) {
-      cl_ok = cudaFuncSetAttribute(k_pcg_reg<Mv, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+      cl_ok = cudaFuncSetAttribute(k_pcg_reg<Mv, true, 1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
                       cudaSuccess &&
-                  cudaFuncSetAttribute(k_pcg_reg<Mv, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                  cudaFuncSetAttribute(k_pcg_reg<Mv, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        PCG_SMEM_BYTES) == cudaSuccess
               ? 1
               : 0;
@@ -902,14 +971,24 @@ static cudaError_t launch_pcg_t(const PcgArgs& a, Mv mv, int n_sm, cudaStream_t 
       cfg.attrs = at;
       cfg.numAttrs = 1;
       int ncl = 0;
-      if (cudaOccupancyMaxActiveClusters(&ncl, (const void*)k_pcg_reg<Mv, true>, &cfg) == cudaSuccess &&
+      if (cudaOccupancyMaxActiveClusters(&ncl, (const void*)k_pcg_reg<Mv, true, 1>, &cfg) == cudaSuccess &&
           ncl >= 1)
-        return cudaLaunchKernelExC(&cfg, (const void*)k_pcg_reg<Mv, true>, params);
+        return cudaLaunchKernelExC(&cfg, (const void*)k_pcg_reg<Mv, true, 1>, params);
       (void)cudaGetLastError();  // this cluster size does not fit: grid barrier instead
     }
   }
-  return cudaLaunchCooperativeKernel(reg ? (void*)k_pcg_reg<Mv, false> : (void*)k_pcg<Mv>, dim3(G),
-                                     dim3(PCG_THREADS), params, PCG_SMEM_BYTES, s);
+  void* kfn = (void*)k_pcg<Mv>;
+  if (reg) {
+    if constexpr (Mv::kSplit) {
+      kfn = split == 8   ? (void*)k_pcg_reg<Mv, false, 8>
+            : split == 4 ? (void*)k_pcg_reg<Mv, false, 4>
+            : split == 2 ? (void*)k_pcg_reg<Mv, false, 2>
+                         : (void*)k_pcg_reg<Mv, false, 1>;
+    } else {
+      kfn = (void*)k_pcg_reg<Mv, false, 1>;
+    }
+  }
+  return cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(PCG_THREADS), params, PCG_SMEM_BYTES, s);
 }
 
 cudaError_t launch_pcg(const PcgArgs& a, int n_sm, cudaStream_t s) {
