@@ -22,6 +22,7 @@ sharded: partial systems, one all-reduce of A.p per PCG iteration
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -505,6 +506,7 @@ def main():
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             flush.fill_(1.0)  # evict L2 (126 MB) between timed solves
+            gc.collect()  # no cyclic-GC pass inside a timed solve (see the e2e leg)
             torch.cuda.synchronize()
             problem.poses = dict(scene.init)
             barrier()
@@ -550,6 +552,11 @@ def main():
         for k in range(max(1, args.steps)):
             rt.clear_frames()
             problem.close()
+            # a full cyclic-GC pass over the scene's ~10^5 host objects takes
+            # ~50 ms (cfg5); collect before each step, outside the timed
+            # region, so no generation-2 pass lands inside one (as timeit
+            # keeps the collector out of its timings)
+            gc.collect()
             torch.cuda.synchronize()
             barrier()
             t0 = time.perf_counter()
