@@ -904,10 +904,8 @@ static cudaError_t launch_pcg_t(const PcgArgs& a, Mv mv, int n_sm, cudaStream_t 
   // one CTA per SM at most (co-residency, cheapest barrier); rows split
   // evenly.  A block row is summed by `split` warps when the grid still fits
   // the SMs that way (more SMs gathering the neighbour vectors).
-  static const int split_env = [] {
-    const char* v = getenv("SFB_PCG_SPLIT");
-    return v ? atoi(v) : 0;
-  }();
+  const char* split_s = getenv("SFB_PCG_SPLIT");  // tuning / tests: force 1, 2, 4 or 8
+  const int split_env = split_s ? atoi(split_s) : 0;
   // Default: the widest split whose grid (one row group per warp group) still
   // fits the SMs, except for tiny systems (<= 2 CTAs unsplit), which run as
   // one cluster.  Measured per 50-iteration solve: cfg4 split 2 388 us vs
