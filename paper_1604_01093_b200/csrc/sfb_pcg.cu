@@ -62,13 +62,18 @@ template <bool FOLD>
 __device__ __forceinline__ double row_product(const PcgArgs& a, const RowCtx& rc, int v,
                                               const double* __restrict__ z,
                                               const double* __restrict__ pold, double beta,
-                                              int lane, int part = 0, int nparts = 1) {
+                                              int lane, int part = 0, int nparts = 1,
+                                              int pe0 = -1, int pe1 = -1) {
   const int grp = lane / 6, r = lane - 6 * grp;
-  int e0 = a.row_ptr[v], e1 = a.row_ptr[v + 1];
-  if (nparts > 1) {  // this warp's share of the row's slots (split rows)
-    const int n = e1 - e0;
-    e1 = e0 + (n * (part + 1)) / nparts;
-    e0 = e0 + (n * part) / nparts;
+  int e0 = pe0, e1 = pe1;  // the warp's slot range when the caller holds it
+  if (pe0 < 0) {
+    e0 = a.row_ptr[v];
+    e1 = a.row_ptr[v + 1];
+    if (nparts > 1) {  // this warp's share of the row's slots (split rows)
+      const int n = e1 - e0;
+      e1 = e0 + (n * (part + 1)) / nparts;
+      e0 = e0 + (n * part) / nparts;
+    }
   }
   double acc = 0.0;
   for (int c0 = e0; c0 < e1; c0 += PCG_GATHER_CAP) {
@@ -244,8 +249,8 @@ struct BsrMv {
   template <bool FOLD>
   __device__ __forceinline__ double row(const PcgArgs& a, const RowCtx& rc, int v, const double* z,
                                         const double* pold, double beta, int lane, int part = 0,
-                                        int nparts = 1) const {
-    return row_product<FOLD>(a, rc, v, z, pold, beta, lane, part, nparts);
+                                        int nparts = 1, int e0 = -1, int e1 = -1) const {
+    return row_product<FOLD>(a, rc, v, z, pold, beta, lane, part, nparts, e0, e1);
   }
   __device__ __forceinline__ bool stageable() const { return true; }
   static constexpr bool kSplit = true;  // rows may be split over warps
@@ -256,7 +261,7 @@ struct DenseMv {
   template <bool FOLD>
   __device__ __forceinline__ double row(const PcgArgs& a, const RowCtx&, int v, const double* z,
                                         const double* pold, double beta, int lane, int = 0,
-                                        int = 1) const {
+                                        int = 1, int = -1, int = -1) const {
     const int n6 = 6 * a.n_blk;
     double out = 0.0;
     for (int r = 0; r < 6; ++r) {
@@ -487,6 +492,9 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg(PcgArgs a, Mv mv, int ro
 #ifndef PCG_RMAX
 #define PCG_RMAX 2
 #endif
+#ifndef PCG_ROWREG
+#define PCG_ROWREG 1  // slot ranges in registers (0: re-read row_ptr per matvec)
+#endif
 #ifndef PCG_SPLIT_MAX
 #define PCG_SPLIT_MAX 8     // warps per block row at most (k_pcg_reg<.., SPLIT>)
 #endif
@@ -595,13 +603,28 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg_reg(PcgArgs a, Mv mv, in
   const int nrow = rc.r1 > rc.r0 + rgw ? (rc.r1 - rc.r0 - rgw + RW - 1) / RW : 0;
   // y = A xin over this CTA's rows, the row parts added in part order
   __shared__ double ysh[PCG_WARPS][PCG_RMAX][6];
+  // this warp's slot range of each of its rows, held in registers for the
+  // solve (row_ptr would otherwise be re-read from L2 after every grid
+  // barrier: the barrier's acquire invalidates L1)
+  int re0[PCG_RMAX], re1[PCG_RMAX];
+#pragma unroll
+  for (int j = 0; j < PCG_RMAX; ++j) {
+    re0[j] = re1[j] = -1;
+    if (PCG_ROWREG && Mv::kSplit && j < nrow) {  // (DenseMv has no row_ptr)
+      const int v = rc.r0 + rgw + RW * j;
+      const int b0 = a.row_ptr[v], n = a.row_ptr[v + 1] - b0;
+      re0[j] = b0 + (n * part) / SPLIT;
+      re1[j] = b0 + (n * (part + 1)) / SPLIT;
+    }
+  }
   auto rows_product = [&](auto fold_tag, const double* zin, const double* xin, double bt,
                           double (&yv)[PCG_RMAX]) {
     constexpr bool FOLD = decltype(fold_tag)::value;
 #pragma unroll
     for (int j = 0; j < PCG_RMAX; ++j) {
       yv[j] = 0.0;
-      if (j < nrow) yv[j] = mv.template row<FOLD>(a, rc, rc.r0 + rgw + RW * j, zin, xin, bt, lane, part, SPLIT);
+      if (j < nrow)
+        yv[j] = mv.template row<FOLD>(a, rc, rc.r0 + rgw + RW * j, zin, xin, bt, lane, part, SPLIT, re0[j], re1[j]);
     }
     if constexpr (SPLIT > 1) {
       if (part > 0 && lane < 6) {
