@@ -43,6 +43,12 @@ struct GridBarrier {
     }
     __syncthreads();
   }
+  // Barrier + all-sum of the G per-CTA partials in one step, for a CTA that
+  // has just run block_allsum (whose barrier already ordered every thread's
+  // writes before thread 0's release): warp 0 alone arrives, polls and reads
+  // the partials (grid_allsum_warp's fixed order); one CTA barrier after.
+  template <int NV>
+  __device__ __forceinline__ void sync_allsum(const double* part, double (&out)[NV], unsigned G);
 };
 
 // Per-CTA view of the block rows it owns.
@@ -220,6 +226,33 @@ __device__ __forceinline__ void grid_allsum_warp(const double* part, double (&ou
     for (int c = 0; c < MAXC; ++c) s += v[k][c];
     out[k] = warp_sum(s);
   }
+}
+
+template <int NV>
+__device__ __forceinline__ void GridBarrier::sync_allsum(const double* part, double (&out)[NV],
+                                                         unsigned G) {
+  __shared__ double tot_w0[4];
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) {
+      ++epoch;
+      const unsigned target = epoch * G;
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+      unsigned v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+      } while (v < target);
+    }
+    __syncwarp();  // lane 0's acquire orders the warp's partial loads below
+    double t[NV];
+    grid_allsum_warp<NV>(part, t, (int)G);
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int k = 0; k < NV; ++k) tot_w0[k] = t[k];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NV; ++k) out[k] = tot_w0[k];
 }
 
 // z = M^-1 r for one block row: scalar Jacobi (the reference's pcg_solve,
@@ -492,6 +525,9 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg(PcgArgs a, Mv mv, int ro
 #ifndef PCG_RMAX
 #define PCG_RMAX 2
 #endif
+#ifndef PCG_W0SYNC
+#define PCG_W0SYNC 1  // barrier + all-sum by warp 0 with one CTA barrier (0: GridBarrier::sync + grid_allsum)
+#endif
 #ifndef PCG_ROWREG
 #define PCG_ROWREG 1  // slot ranges in registers (0: re-read row_ptr per matvec)
 #endif
@@ -684,8 +720,12 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg_reg(PcgArgs a, Mv mv, in
     }
   }
   if constexpr (!CL) {
+#if PCG_W0SYNC
+    grid.sync_allsum<2>(partB, tot, G);
+#else
     grid.sync(G);
     grid_allsum<2>(partB, tot, G);
+#endif
   }
   const double norm_b = sqrt(tot[0]);
   double rz = tot[1];
@@ -730,8 +770,12 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg_reg(PcgArgs a, Mv mv, in
         }
       }
       if constexpr (!CL) {
+#if PCG_W0SYNC
+        grid.sync_allsum<1>(partA, pAp_a, G);
+#else
         grid.sync(G);
         grid_allsum<1>(partA, pAp_a, G);
+#endif
       }
       TRACE(k, 2);
       const double pAp = pAp_a[0];
@@ -804,8 +848,12 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg_reg(PcgArgs a, Mv mv, in
         }
       }
       if constexpr (!CL) {
+#if PCG_W0SYNC
+        grid.sync_allsum<3>(partB, s3, G);
+#else
         grid.sync(G);
         grid_allsum<3>(partB, s3, G);
+#endif
       }
       TRACE(k, 4);
       if (s3[2] != 0.0) { status = 1; break; }
