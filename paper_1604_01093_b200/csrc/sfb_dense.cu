@@ -1034,7 +1034,7 @@ struct EdgePeers {
 __global__ void k_edge_reduce(const int* edge_item_ptr, const double* item_out, double* edge_out,
                               int n_dir, const int2* dir_edges, const PoseDev* poses,
                               EdgePeers peers) {
-  __shared__ double sK[8][36], sM[8][36], sk[8][6];
+  __shared__ double sK[8][36], sM[8][36], sW[8][36], sk[8][6];
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int wl = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -1049,21 +1049,40 @@ __global__ void k_edge_reduce(const int* edge_item_ptr, const double* item_out, 
     for (int c = r; c < 6; ++c)
       if (lane == sym6(r, c)) sK[wl][r * 6 + c] = sK[wl][c * 6 + r] = s;
   if (lane >= 21 && lane < 27) sk[wl][lane - 21] = s;
-  if (lane == 0) {
+  // M_j = [[R, -[t]x R], [0, -R]], one or two entries per lane
+  {
     const PoseDev& Pj = poses[dir_edges[warp].y];
     const double* R = Pj.R;
     const double* t = Pj.t;
-    const double T[9] = {0, -t[2], t[1], t[2], 0, -t[0], -t[1], t[0], 0};  // [t]x
-    for (int r = 0; r < 6; ++r)
-      for (int c = 0; c < 6; ++c) sM[wl][r * 6 + c] = 0.0;
-    for (int r = 0; r < 3; ++r)
-      for (int c = 0; c < 3; ++c) {
+    for (int e = lane; e < 36; e += 32) {
+      const int r = e / 6, c = e % 6;
+      double m = 0.0;
+      if (r < 3 && c < 3) {
+        m = R[r * 3 + c];
+      } else if (r < 3) {
+        // row r of [t]x = {{0, -t2, t1}, {t2, 0, -t0}, {-t1, t0, 0}}
+        const double a0 = r == 0 ? 0.0 : (r == 1 ? t[2] : -t[1]);
+        const double a1 = r == 0 ? -t[2] : (r == 1 ? 0.0 : t[0]);
+        const double a2 = r == 0 ? t[1] : (r == 1 ? -t[0] : 0.0);
         double tr = 0.0;
-        for (int k = 0; k < 3; ++k) tr += T[r * 3 + k] * R[k * 3 + c];
-        sM[wl][r * 6 + c] = R[r * 3 + c];
-        sM[wl][r * 6 + c + 3] = -tr;
-        sM[wl][(r + 3) * 6 + c + 3] = -R[r * 3 + c];
+        tr += a0 * R[c - 3];
+        tr += a1 * R[3 + (c - 3)];
+        tr += a2 * R[6 + (c - 3)];
+        m = -tr;
+      } else if (c >= 3) {
+        m = -R[(r - 3) * 3 + (c - 3)];
       }
+      sM[wl][e] = m;
+    }
+  }
+  __syncwarp();
+  // W = K M^T (W[k][c] = sum_l K[k][l] M[c][l]), one or two entries per lane,
+  // then H = M W: two 6-long chains per entry instead of one 42-long one
+  for (int e = lane; e < 36; e += 32) {
+    const int k = e / 6, c = e % 6;
+    double mk = 0.0;
+    for (int l = 0; l < 6; ++l) mk += sK[wl][k * 6 + l] * sM[wl][c * 6 + l];
+    sW[wl][e] = mk;
   }
   __syncwarp();
   if (lane < 21) {
@@ -1071,11 +1090,7 @@ __global__ void k_edge_reduce(const int* edge_item_ptr, const double* item_out, 
     while (c >= 6 - r) { c -= 6 - r; ++r; }  // packed index -> (r, c >= r)
     c += r;
     double h = 0.0;
-    for (int k = 0; k < 6; ++k) {
-      double mk = 0.0;
-      for (int l = 0; l < 6; ++l) mk += sK[wl][k * 6 + l] * sM[wl][c * 6 + l];
-      h += sM[wl][r * 6 + k] * mk;
-    }
+    for (int k = 0; k < 6; ++k) h += sM[wl][r * 6 + k] * sW[wl][k * 6 + c];
     val = h;
   } else if (lane < 27) {
     const int r = lane - 21;
