@@ -150,9 +150,6 @@ __global__ void k_enumerate_pairs(int n, int2* out) {
   out[q] = make_int2(a, b);
 }
 
-__global__ void k_jacobi_diag(const double* D, const int* d_ptr, const int* d_ent,
-                              const double* set_out, int n_blk, double* out);
-
 PcgArgs pcg_args(sfb_problem* p) {
   PcgArgs a{};
   a.n_blk = p->n_blk;
@@ -523,14 +520,11 @@ int enqueue_linearize_end(sfb_problem* p) {
   aa.row_ptr = p->row_ptr.p;
   aa.pair_slot = p->row_ent.p;
   aa.Brow = p->Brow.p;
+  aa.jdiag = p->jdiag.p;  // the Jacobi diagonal, fused into the assembly
   ProfScope ps(p->prof, 5, s);
   launch_assemble(aa, s);
   CKL(p);
   if (p->n_blk > 0) {
-    sfb_count_launch();
-    k_jacobi_diag<<<(6 * p->n_blk + 255) / 256, 256, 0, s>>>(p->D.p, p->d_ptr.p, p->d_ent.p,
-                                                             p->set_out.p, p->n_blk, p->jdiag.p);
-    CKL(p);
     if (p->precond) {
       CK(p, p->bj_inv.ensure((size_t)p->n_blk * 36, s));
       launch_block_jacobi_inv(p->D.p, p->jdiag.p, p->n_blk, p->bj_inv.p, s);
@@ -1456,20 +1450,6 @@ int sfb_get_gradient(sfb_problem* p, double* g) {
 
 }  // extern "C"
 
-namespace {
-__global__ void k_jacobi_diag(const double* D, const int* d_ptr, const int* d_ent,
-                              const double* set_out, int n_blk, double* out) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= 6 * n_blk) return;
-  const int v = i / 6, c = i % 6;
-  double d = D[(int64_t)v * 36 + c * 7];
-  // _jacobi_diagonal (solver.py:412-428) has no cross term for a set whose
-  // two frames coincide; remove the H_ij + H_ij^T diagonal it would add.
-  for (int k = d_ptr[v]; k < d_ptr[v + 1]; ++k)
-    if ((d_ent[k] & 7) == 2) d -= 2.0 * set_out[(int64_t)(d_ent[k] >> 3) * SFB_SET_STRIDE + 72 + c * 7];
-  out[i] = d;
-}
-}  // namespace
 
 extern "C" {
 

@@ -1259,6 +1259,25 @@ __global__ void __launch_bounds__(ASM_DIAG_WARPS * 32) k_assemble(AssembleArgs a
         S[e1] = d1;
       }
       if (lane < 6) a.g[v * 6 + lane] = gv;
+      if (a.jdiag) {
+        // _jacobi_diagonal (solver.py:412-428): D's diagonal without the
+        // H_ij + H_ij^T cross term of a set whose two frames coincide,
+        // subtracted in list order (the arithmetic of the former separate pass)
+        const bool dl = (lane % 7 == 0 && lane < 35) || lane == 3;  // entries 0,7,..,28 (d0) and 35 (d1)
+        const int c = lane == 3 ? 5 : lane / 7;
+        double jd = lane == 3 ? d1 : d0;
+        for (int kb = k0; kb < k1; kb += 32) {
+          const int ent = kb + lane < k1 ? a.d_ent[kb + lane] : 0;
+          unsigned m = __ballot_sync(0xffffffffu, kb + lane < k1 && (ent & 7) == 2);
+          while (m) {
+            const int j = __ffs(m) - 1;
+            m &= m - 1;
+            const int id = __shfl_sync(0xffffffffu, ent, j) >> 3;
+            if (dl) jd -= 2.0 * a.set_out[(int64_t)id * SFB_SET_STRIDE + 72 + c * 7];
+          }
+        }
+        if (dl) a.jdiag[v * 6 + c] = jd;
+      }
     }
   } else {
     const int q = ((int)blockIdx.x - a.n_blk) * ASM_DIAG_WARPS + wid;

@@ -78,6 +78,7 @@ struct AssembleArgs {
   const int* row_ptr;    // matvec slots: row_ptr[v] is v's diagonal slot
   const int* pair_slot;  // 2 per pair: slot in row a (as is), in row b (transposed)
   double* Brow;          // slots * 36
+  double* jdiag;         // n_blk * 6 Jacobi diagonal (solver.py:412-428), or null
   int dense_on;
 };
 
