@@ -886,6 +886,9 @@ __device__ __forceinline__ void bilinear_val2_fast(const FrameDev& f, double x, 
 #ifndef ENERGY_BLOCKS
 #define ENERGY_BLOCKS 4
 #endif
+#ifndef ENERGY_NEXT
+#define ENERGY_NEXT 1  // next flagged tile by table lookup (0: scan the flags)
+#endif
 #ifndef ENERGY_PF
 #define ENERGY_PF 0  // 1: next group's frozen-set words one group ahead (measured 1.73 vs 1.63 ms: off)
 #endif
@@ -915,10 +918,29 @@ __global__ void __launch_bounds__(DENSE_THREADS, ENERGY_BLOCKS) k_dense_energy(D
   const uint32_t* pmask = a.photo_mask + a.photo_off[it.x];
   const uint16_t* gtgt = a.geo_tgt + a.geo_off[it.x];
   const int lane = threadIdx.x & 31;
+#if ENERGY_NEXT
+  // nxt[i]: the first flagged tile >= i (nt: none), by warp 0 from the back
+  // in 32-tile chunks, so next() is one shared-memory read, not a scan
+  __shared__ uint16_t nxt[DENSE_MAX_TILES];
+  const int nt = it.z - it.y;
+  if (threadIdx.x < 32) {
+    int carry = nt;
+    for (int base = ((nt - 1) / 32) * 32; base >= 0; base -= 32) {
+      const int i = base + lane;
+      const unsigned m = __ballot_sync(0xffffffffu, i < nt && tflag[i] != 0);
+      const unsigned hi = m >> lane;  // flagged tiles >= i in this chunk
+      if (i < nt) nxt[i] = (uint16_t)(hi ? i + __ffs(hi) - 1 : carry);
+      carry = m ? base + __ffs(m) - 1 : carry;
+    }
+  }
+  __syncthreads();
+  auto next = [&](int t) { return t < it.z ? it.y + (int)nxt[t - it.y] : it.z; };
+#else
   auto next = [&](int t) {
     while (t < it.z && !tflag[t - it.y]) ++t;  // nothing frozen in skipped tiles
     return t;
   };
+#endif
   double acc[2] = {0.0, 0.0};
   // ENERGY_ILP flagged tiles at once, each stage's loads of all of them in
   // flight together (the pass is bound by its dependent-load chain); the
